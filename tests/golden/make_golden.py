@@ -1,0 +1,268 @@
+#!/usr/bin/env python3
+"""Generate the golden fixtures in tests/golden/ from the UNMODIFIED reference.
+
+Run in the build container (the only place /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Everything here calls the reference's own public functions (parpf.accel,
+parpf.core, parpf.resampling, parpf.filters.run_filter,
+parpf.ensemble.run_ensemble).  The only additions are the config adapters the
+BASELINE configs need: subclasses of the reference's
+Lorenz63Model / StateSpaceModel that call the reference kernels, and a
+recording wrapper around parpf.filters.multinomial_resample_indices that
+captures (u, ancestors) per step without changing what it returns.
+
+The fixtures pin oracle/parpf_oracle.py (tests/test_oracle_golden.py, CPU) and
+are the golden side of the GPU parity tests (tests/test_gpu_parity.py).
+Observations for the filter runs come from oracle.lorenz_truth/fhn_truth;
+they are inputs, stored verbatim in the fixtures.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+
+import parpf  # noqa: E402  (reference, via PYTHONPATH)
+from parpf import accel, core, resampling  # noqa: E402
+import parpf.filters as ref_filters  # noqa: E402
+from parpf.core import StateSpaceModel  # noqa: E402
+from parpf.models.lorenz63 import Lorenz63Model  # noqa: E402
+
+from oracle import parpf_oracle as orc  # noqa: E402  (observations only)
+
+
+# --------------------------------------------------------------------------
+# reference-side config adapters
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class RefLorenzCfg(Lorenz63Model):
+    """cfg0/cfg2 on the reference Lorenz63Model: noise 0.5*z, obs (x1,x3)."""
+
+    noise_scale: float = 0.5
+
+    def __post_init__(self):
+        super().__post_init__()
+        self.dim_y = 2
+
+    def sample_transition(self, x_prev, t, rng):
+        x_prev = np.atleast_2d(np.asarray(x_prev, dtype=np.float64))
+        noise = rng.standard_normal((self.substeps, x_prev.shape[0], 3))
+        return self._propagate(x_prev, self.noise_scale * noise)
+
+    def log_likelihood(self, y, x, t):
+        y = np.asarray(y, dtype=np.float64).reshape(-1)
+        x = np.asarray(x)
+        r0 = y[0] - x[:, 0]
+        r1 = y[1] - x[:, 2]
+        return -(r0 * r0 + r1 * r1) / (2.0 * self.obs_var)
+
+
+class RefFhnCfg(StateSpaceModel):
+    """cfg3/cfg4 classical FH-N lattice on the reference numpy twin."""
+
+    def __init__(self, rows, cols, substeps, stim_row, stim_col, dt=0.01,
+                 noise_std=0.05, obs_var=0.01):
+        self.rows, self.cols, self.substeps = rows, cols, substeps
+        self.stim_row, self.stim_col = stim_row, stim_col
+        self.dt, self.obs_var = dt, obs_var
+        self.nodes = rows * cols
+        self.dim_x = 2 * self.nodes
+        self.obs_indices = orc.electrode_indices(rows, cols)
+        self.dim_y = self.obs_indices.shape[0]
+        self.sig = noise_std * math.sqrt(dt)
+        deg = np.full((rows, cols), 4.0)
+        deg[0, :] -= 1
+        deg[-1, :] -= 1
+        deg[:, 0] -= 1
+        deg[:, -1] -= 1
+        self.deg = deg
+
+    def sample_prior(self, rng, n):
+        x = np.zeros((n, self.dim_x))
+        v = x[:, : self.nodes].reshape(n, self.rows, self.cols)
+        v[:, self.stim_row:self.stim_row + 3, self.stim_col:self.stim_col + 3] = 1.0
+        return x
+
+    def sample_transition(self, x_prev, t, rng):
+        x_prev = np.atleast_2d(np.asarray(x_prev, dtype=np.float64))
+        n = x_prev.shape[0]
+        U = x_prev[:, : self.nodes].reshape(n, self.rows, self.cols)
+        V = x_prev[:, self.nodes:].reshape(n, self.rows, self.cols)
+        for _ in range(self.substeps):
+            zu = rng.standard_normal((n, self.rows, self.cols))
+            zv = rng.standard_normal((n, self.rows, self.cols))
+            U, V = accel.fhn_euler_block_numpy(
+                U, V, -self.deg * U, zu, self.dt, 1.0, (-1.0, 1.13, -0.13, 0.0),
+                (0.01, -0.005, 0.0), self.sig)
+            V = V + self.sig * zv
+        return np.concatenate([U.reshape(n, -1), V.reshape(n, -1)], axis=1)
+
+    def log_likelihood(self, y, x, t):
+        y = np.asarray(y, dtype=np.float64).reshape(-1)
+        x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+        resid = y - x[:, : self.nodes][:, self.obs_indices]
+        return -0.5 / self.obs_var * np.sum(resid * resid, axis=1)
+
+    def error_projection(self, states):
+        return np.asarray(states)[..., : self.nodes]
+
+
+# --------------------------------------------------------------------------
+# recording wrapper around the reference resampler
+# --------------------------------------------------------------------------
+
+
+class _Recorder:
+    def __init__(self):
+        self.calls = []
+        self._orig = ref_filters.multinomial_resample_indices
+
+    def __call__(self, weights, n_out, rng):
+        # identical arithmetic to resampling.py:29-43, with u captured
+        w = resampling._check_weights(weights)
+        cum = np.cumsum(w)
+        u = resampling._sorted_uniforms(n_out, rng)
+        idx = accel.resample_indices(cum, u)
+        self.calls.append((u, idx))
+        return idx
+
+    def __enter__(self):
+        ref_filters.multinomial_resample_indices = self
+        return self
+
+    def __exit__(self, *exc):
+        ref_filters.multinomial_resample_indices = self._orig
+
+
+def _filter_with_steps(model, obs, n, seed):
+    with _Recorder() as rec:
+        out = parpf.run_filter(model, obs, "bootstrap", n, seed)
+    return out, rec.calls
+
+
+# --------------------------------------------------------------------------
+# fixtures
+# --------------------------------------------------------------------------
+
+
+def gen_kernels():
+    rng = np.random.default_rng(20260101)
+    d = {}
+    # normalize_log_weights (core.py:116-138)
+    cases = [np.zeros(4), np.array([5.0]), np.array([0.0, np.log(2.0)]),
+             np.array([-np.inf, 0.0, -np.inf]), np.array([-1e4, -1e4 + np.log(3.0)]),
+             rng.normal(size=1000) * 10.0, rng.normal(size=4096)]
+    for i, c in enumerate(cases):
+        w, lm = core.normalize_log_weights(c)
+        d[f"nlw_in_{i}"] = c
+        d[f"nlw_w_{i}"] = w
+        d[f"nlw_lm_{i}"] = np.array(lm)
+    d["nlw_count"] = np.array(len(cases))
+    # resample_indices (accel.py:175-203), incl. the tie case (test_accel.py:57-64)
+    rcases = [(np.array([0.2, 0.2, 1.0]), np.array([0.1, 0.2, 0.2000000001, 0.99]))]
+    for n, m in ((1, 5), (10, 10), (1000, 313), (4096, 4096), (3, 7)):
+        w = rng.dirichlet(np.ones(n))
+        if n == 3:
+            w = np.array([0.5, 0.0, 0.5])
+        cum = np.cumsum(w)
+        e = rng.standard_exponential(m + 1)
+        c = np.cumsum(e)
+        rcases.append((cum, c[:m] / c[m]))
+    # u beyond the last cum (clamp) - cum ends below 1 by rounding
+    rcases.append((np.array([0.25, 0.5, 0.75, 0.9999999999999]), np.array([0.3, 0.99999999999999, 1.0])))
+    for i, (cum, u) in enumerate(rcases):
+        d[f"ri_cum_{i}"] = cum
+        d[f"ri_u_{i}"] = u
+        d[f"ri_idx_{i}"] = accel.resample_indices(cum, u)
+        assert np.array_equal(d[f"ri_idx_{i}"], accel.resample_indices_numpy(cum, u))
+    d["ri_count"] = np.array(len(rcases))
+    # multinomial_resample_indices with a seeded Generator
+    w = rng.dirichlet(np.ones(500))
+    d["mri_w"] = w
+    d["mri_idx"] = resampling.multinomial_resample_indices(w, 500, np.random.default_rng(77))
+    # lorenz_euler_block (accel.py:60-102), same shapes as test_accel.py:22-27
+    st = rng.normal(size=(257, 3)) * 10.0
+    nz = rng.normal(size=(100, 257, 3))
+    d["lz_states"], d["lz_noise"] = st, nz
+    d["lz_out"] = accel.lorenz_euler_block(st, nz, 1e-3, 10.0, 28.0, 8.0 / 3.0)
+    assert np.array_equal(d["lz_out"], accel.lorenz_euler_block_numpy(st, nz, 1e-3, 10.0, 28.0, 8.0 / 3.0))
+    # fhn_euler_block numpy twin (accel.py:110-129): rectangular + square
+    for tag, shape, params in (
+        ("rect", (5, 30, 50), (0.01, 1.0, (-1.0, 1.13, -0.13, 0.0), (0.01, -0.005, 0.0), 0.005)),
+        ("sq", (33, 16, 16), (5e-3, 4.5e-3, (-1.0, 0.0, 3.6, 0.0), (2.1, -0.6, 0.6), 0.05)),
+    ):
+        U, V, drive, noise = (rng.normal(size=shape) for _ in range(4))
+        dt, cpl, cubic, beta, sig = params
+        u2, v2 = accel.fhn_euler_block_numpy(U, V, drive, noise, dt, cpl, cubic, beta, sig)
+        for k, a in (("U", U), ("V", V), ("drive", drive), ("noise", noise), ("u_new", u2), ("v_new", v2)):
+            d[f"fhn_{tag}_{k}"] = a
+        d[f"fhn_{tag}_params"] = np.array([dt, cpl, *cubic, *beta, sig])
+    np.savez_compressed(os.path.join(HERE, "kernels.npz"), **d)
+
+
+def gen_lorenz():
+    d = {}
+    truth0, states, obs = orc.lorenz_truth(seed=2024, n_obs=25)
+    model = RefLorenzCfg(substeps=40, obs_var=2.0, prior_mean=tuple(truth0), prior_var=1.0)
+    d["truth0"], d["states"], d["obs"] = truth0, states, obs
+    # one filter with per-step ancestors
+    seed = np.random.SeedSequence(31337)
+    out, calls = _filter_with_steps(model, obs, 64, seed)
+    d["f_est"], d["f_lnc"] = out.estimates, out.log_norm_const
+    d["f_u"] = np.stack([c[0] for c in calls])
+    d["f_anc"] = np.stack([c[1] for c in calls])
+    d["f_seed_entropy"] = np.array(31337)
+    # an ensemble (ensemble.py:76-111): M=4, N=100, master seed 5
+    ens = parpf.run_ensemble(model, obs, "bootstrap", 4, 100, 5)
+    d["e_mean"] = ens.mean_estimates
+    d["e_est"] = np.stack([fo.estimates for fo in ens.filter_outputs])
+    d["e_lnc"] = np.stack([fo.log_norm_const for fo in ens.filter_outputs])
+    d["e_master"] = np.array(5)
+    # collapse: an infinite observation makes every log weight -inf at step 3
+    obs_c = obs[:6].copy()
+    obs_c[2] = np.inf
+    outc = parpf.run_filter(model, obs_c, "bootstrap", 32, 11)
+    d["c_obs"], d["c_est"], d["c_lnc"] = obs_c, outc.estimates, outc.log_norm_const
+    d["c_steps"] = np.array(outc.collapse_steps)
+    np.savez_compressed(os.path.join(HERE, "lorenz.npz"), **d)
+
+
+def gen_fhn():
+    d = {}
+    m, states, obs = orc.fhn_truth(seed=7, n_obs=3)
+    model = RefFhnCfg(m.rows, m.cols, m.substeps, m.stim_row, m.stim_col)
+    d["obs"] = obs
+    d["stim"] = np.array([m.stim_row, m.stim_col])
+    out, calls = _filter_with_steps(model, obs, 8, np.random.SeedSequence(99))
+    d["f_est_v"] = out.estimates[:, : m.nodes]
+    d["f_est_w"] = out.estimates[:, m.nodes:]
+    d["f_lnc"] = out.log_norm_const
+    d["f_u"] = np.stack([c[0] for c in calls])
+    d["f_anc"] = np.stack([c[1] for c in calls])
+    ens = parpf.run_ensemble(model, obs[:2], "bootstrap", 2, 4, 17)
+    d["e_mean_v"] = ens.mean_estimates[:, : m.nodes]
+    d["e_lnc"] = np.stack([fo.log_norm_const for fo in ens.filter_outputs])
+    np.savez_compressed(os.path.join(HERE, "fhn.npz"), **d)
+
+
+if __name__ == "__main__":
+    print("reference backend:", accel.backend_name())
+    gen_kernels()
+    gen_lorenz()
+    gen_fhn()
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
