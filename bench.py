@@ -1,0 +1,383 @@
+#!/usr/bin/env python3
+"""Benchmark of the filter-bank hot path (BASELINE.json metric:
+particle-steps/s = M x N x Euler steps per second, whole job).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4]
+    python bench.py --impl reference ...      # the reference CPU path arm
+
+A "step" is one observation interval of the whole bank: propagate (n_sub
+Euler steps per particle, fused gather + log-likelihood) -> per-filter
+logsumexp + multinomial resampling -> per-filter estimate (-> one
+disjoint-support NCCL all-reduce of the estimate for N>1 GPUs).
+
+Default workload: BASELINE cfg4 (FitzHugh-Nagumo 30x50 lattice, fp32,
+M=64 filters x N=4096 particles, 50 Euler steps per observation), the
+largest single-GPU config and the HBM showcase; filters are sharded
+M/N_gpu per rank (strong scaling: the total bank is fixed).  cfg2 (Lorenz,
+M x N = 2^22) is available via --config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "particle-steps/s (M x N x Euler steps)"
+
+CONFIGS = {
+    # name: (kind, M, N, dtype, description)
+    "cfg4": dict(kind="fhn", M=64, N=4096, dtype="float32",
+                 desc="FitzHugh-Nagumo 30x50 lattice, M=64 x N=4096, 50 Euler steps/obs, fp32"),
+    "cfg3": dict(kind="fhn", M=8, N=512, dtype="float32",
+                 desc="FitzHugh-Nagumo 30x50 lattice, M=8 x N=512, 50 Euler steps/obs, fp32"),
+    "cfg2": dict(kind="lorenz", M=4096, N=1024, dtype="float32",
+                 desc="Lorenz-63, M=4096 x N=1024 (M*N=2^22), 40 Euler steps/obs, fp32"),
+    "cfg2m256": dict(kind="lorenz", M=256, N=16384, dtype="float32",
+                     desc="Lorenz-63, M=256 x N=16384 (M*N=2^22), 40 Euler steps/obs, fp32"),
+    "cfg0": dict(kind="lorenz", M=4, N=1000, dtype="float64",
+                 desc="Lorenz-63, M=4 x N=1000, 40 Euler steps/obs, fp64"),
+}
+
+# Algorithmic work per particle-step
+FHN_BYTES_PER_PS = 24000.0   # 16 B/node/Euler step (v,w read+write fp32) x 1500 nodes
+LORENZ_FLOP_PER_PS = 20.0    # FMA = 2 (accel.py:73-75)
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def _barrier(world):
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def _max_over_ranks(x, world):
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _make_model_and_obs(cfg, n_obs, seed=2026):
+    from paper_1407_8071_b200 import simulate
+    from paper_1407_8071_b200.models import FhnLatticeModel, Lorenz63Model
+
+    if cfg["kind"] == "fhn":
+        model, _, obs = simulate.fhn_truth(seed, n_obs, FhnLatticeModel())
+    else:
+        base = Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3")
+        truth0, _, obs = simulate.lorenz_truth(seed, n_obs, base)
+        model = Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                              prior_mean=tuple(truth0), prior_var=1.0)
+    return model, obs
+
+
+# ----------------------------------------------------------------- CPU baseline
+
+def cpu_baseline(cfg, budget_s=12.0, steps=1):
+    """Reference CPU path (oracle port: numpy driver + C kernels, the role of
+    the reference's numba twins) on a bounded sample of the workload, all
+    host cores via a fork pool over filters (ensemble.py:100-105)."""
+    from concurrent.futures import ProcessPoolExecutor
+    from multiprocessing import get_context
+
+    from oracle import ckernels
+    from oracle import parpf_oracle as orc
+
+    ckernels.install()
+    cores = orc.cpu_cores()
+    if cfg["kind"] == "fhn":
+        model, _, obs = orc.fhn_truth(seed=2026, n_obs=max(steps, 1))
+        n_part, per_ps = 16, None
+        n_sub = model.substeps
+    else:
+        truth0, _, obs = orc.lorenz_truth(seed=2026, n_obs=max(steps, 1))
+        model = orc.LorenzConfigModel(prior_mean=tuple(truth0))
+        n_part = 1024 if cfg["N"] >= 1024 else cfg["N"]
+        n_sub = model.substeps
+    # calibrate: one filter, one step
+    t0 = time.perf_counter()
+    orc.run_filter(model, obs[:1], n_part, 0)
+    one = max(time.perf_counter() - t0, 1e-6)
+    per_worker = max(1, int(budget_s / max(steps, 1) / one))
+    n_filters = cores * per_worker if cfg["kind"] == "lorenz" else cores
+    if cfg["kind"] == "fhn":
+        n_part = max(4, min(256, int(16 * budget_s / max(steps, 1) / one)))
+        n_filters = cores
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=cores, mp_context=get_context("fork")) as pool:
+        list(pool.map(orc._filter_task,
+                      [(model, obs[:steps], n_part, s, False)
+                       for s in orc.filter_seeds(1, n_filters)]))
+    wall = time.perf_counter() - t0
+    ps = n_filters * n_part * n_sub * steps
+    return {"value": ps / wall, "unit": "particle-steps/s", "cores": cores, "kind": "port",
+            "sample": (f"{n_filters} filters x {n_part} particles x {steps} obs x {n_sub} Euler "
+                       f"steps of the {cfg['kind']} config model, fp64 numpy driver + C kernels "
+                       f"(oracle/), fork pool of {cores} workers; {wall:.1f} s wall")}
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, budget_s=2.0, steps=1)
+    vals = []
+    t0 = time.perf_counter()
+    cb = None
+    for _ in range(args.steps):
+        cb = cpu_baseline(cfg, budget_s=max(3.0, 60.0 / max(args.steps, 1)), steps=1)
+        vals.append(cb["value"])
+    wall = time.perf_counter() - t0
+    value = float(np.median(vals))
+    cb["value"] = value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "particle-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------- our arm
+
+def run_ours(args, cfg):
+    import torch
+
+    import paper_1407_8071_b200 as pf
+    from paper_1407_8071_b200 import _lib, dist as pdist, philox
+
+    rank, world, local = _dist_setup()
+    M, N = cfg["M"], cfg["N"]
+    if M % world:
+        raise SystemExit(f"M={M} not divisible by {world} GPUs")
+    T = args.warmup + args.steps
+    model, obs = _make_model_and_obs(cfg, T)
+    n_sub = model.substeps
+    lo, hi = pdist.shard_range(M, rank, world)
+    keys = philox.filter_keys(7, M)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    est_dim = 3 if cfg["kind"] == "lorenz" else model.nodes
+    est_full = torch.zeros((T, M, est_dim), dtype=torch.float64, device=dev)
+    bank = pf.FilterBank(model, hi - lo, N, keys[lo:hi], T, dtype=cfg["dtype"],
+                         filter_offset=lo, estimate="projection", est_buffer=est_full,
+                         est_row_offset=lo)
+    bank.load_observations(obs)
+    bank.init()
+    exch = pdist.EstimateExchange(est_full) if world > 1 else None
+
+    for k in range(args.warmup):
+        bank.step(k)
+        if exch:
+            exch.step_done(k)
+    if exch:
+        exch.finish()
+    # dominant-kernel timing: events around the propagate launch, same stream
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    bank.kernel_events = None
+    _barrier(world)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record()
+        for i in range(args.steps):
+            k = args.warmup + i
+            bank.kernel_events = kev[i]
+            bank.step(k)
+            if exch:
+                exch.step_done(k)
+        if exch:
+            exch.finish()
+        end.record()
+        torch.cuda.synchronize()
+    bank.kernel_events = None
+    _barrier(world)
+    local_s = start.elapsed_time(end) / 1e3
+    elapsed = _max_over_ranks(local_s, world)
+    bank.check_status()
+    ps_total = M * N * n_sub * args.steps
+    value = ps_total / elapsed
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    kern_share = kern_ms * args.steps / (local_s * 1e3)
+    ps_per_launch = (hi - lo) * N * n_sub
+
+    peaks, peak_src = _peaks()
+    if cfg["kind"] == "fhn":
+        achieved = ps_per_launch * FHN_BYTES_PER_PS / (kern_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
+                "kernel": "fhn_interval_kernel<float,0>",
+                "algorithmic": f"{FHN_BYTES_PER_PS:.0f} B/particle-step x {ps_per_launch} "
+                               f"particle-steps per launch"}
+        phys = ps_per_launch / n_sub * (2 * 2 * model.nodes * 4 + 4 + 4)
+        roof["physical_bytes_per_launch"] = phys
+        roof["physical_gbs"] = phys / (kern_ms / 1e3) / 1e9
+    else:
+        achieved = ps_per_launch * LORENZ_FLOP_PER_PS / (kern_ms / 1e3) / 1e12
+        roof = {"bound": "fp32", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+                "peak_source": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (SURVEY §8d)",
+                "kernel": "lorenz_pw_kernel<float,0>",
+                "algorithmic": f"{LORENZ_FLOP_PER_PS:.0f} flop/particle-step x {ps_per_launch}"}
+    roof["kernel_ms"] = kern_ms
+    roof["kernel_share_of_step"] = kern_share
+    roof["traffic"] = _ncu_traffic(args.config)
+
+    # e2e through the public API (host observations in, host results out)
+    _barrier(world)
+    e2e_obs = obs[: args.steps]
+    t0 = time.perf_counter()
+    out = pf.run_ensemble(model, e2e_obs, "bootstrap", M, N, 7, dtype=cfg["dtype"],
+                          estimate="projection")
+    torch.cuda.synchronize()
+    e2e_local = time.perf_counter() - t0
+    e2e_s = _max_over_ranks(e2e_local, world)
+    e2e = {"value": ps_total / e2e_s, "unit": "particle-steps/s",
+           "h2d_bytes_per_step": int(model.dim_y * 8),
+           "d2h_bytes_per_step": int(M * est_dim * 8 + M * 8 + M * 4),
+           "api": "paper_1407_8071_b200.run_ensemble (host numpy observations -> "
+                  "EnsembleOutput), includes bank allocation + prior init"}
+    del out
+
+    line = None
+    if rank == 0:
+        cb = None
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(cfg)
+        line = {"metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg["dtype"] ==
+                "float32" else "f64", "data": "synthetic",
+                "config": {"workload": args.config, "desc": cfg["desc"], "M": M, "N": N,
+                           "euler_steps_per_obs": n_sub, "parallelism": f"filters/{world}",
+                           "l2": "inputs larger than L2 (state "
+                                 f"{2 * M * N * model.dim_x * 4 / 1e9:.2f} GB)"
+                           if cfg["kind"] == "fhn" else "state < L2; compute-bound kernel"},
+                "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+                "gpu_launches": 3 * args.steps,
+                "clocks": clocks.summary()}
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def _ncu_traffic(config):
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(config)
+    except OSError:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

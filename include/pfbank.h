@@ -1,0 +1,183 @@
+/*
+ * pfbank.h - C ABI of the B200-native particle-filter bank (libpfbank.so).
+ *
+ * Drop-in boundary for the hot path of the reference `parpf`
+ * (arXiv 1407.8071): a bank of M independent bootstrap particle filters
+ * with N particles each.  The reference is pure Python; its "FFI" for this
+ * path is the module-level kernel rebinding in parpf/accel.py:206-213 plus
+ * the Python entry points it feeds.  Each entry point below cites the
+ * reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/parpf/).
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers owned by the caller
+ *    (e.g. PyTorch CUDA tensors); parameter structs and `mean3`-style small
+ *    vectors marked "host" are host pointers.  Nothing is allocated inside,
+ *    nothing synchronises the host.  Every call is stream-ordered on
+ *    `stream` (a cudaStream_t passed as void*; NULL = legacy default).
+ *  - Return codes: PF_OK (0); PF_EINVAL for bad arguments (the Python layer
+ *    raises ValueError, matching core.py:127-133, resampling.py:12-17,
+ *    filters.py:90-91, ensemble.py:87-90); PF_ECUDA for a CUDA launch error
+ *    (RuntimeError).  pf_last_error() returns a thread-local message.
+ *  - Per-filter runtime outcomes are device flags, not return codes:
+ *    status[f] |= PF_ST_DIVERGED (non-finite state: the reference raises
+ *    NumericalDivergenceError, lorenz63.py:48-49 / fhn.py:186-187),
+ *    status[f] |= PF_ST_NAN_WEIGHT (core.py:132-133 ValueError);
+ *    collapsed[f] = 1 on total weight underflow (core.py:130-131 ->
+ *    filters.py:105-109: uniform weights, lnc unchanged, identity ancestors).
+ *  - Particle layouts (row index p = f*N + i, filter-major):
+ *      Lorenz : three planes x[d*M*N + p], d = 0..2   (T = float|double)
+ *      FH-N   : rows x[p*2*nodes + {0: v block, nodes: w block} + node]
+ *  - Randomness: production mode draws Philox4x32-10 keyed by a per-filter
+ *    64-bit key keys[2f], keys[2f+1] with counters built from
+ *    (particle, time, draw, purpose), so results do not depend on how
+ *    filters are sharded over GPUs.  Oracle ("tape") mode instead reads
+ *    caller-supplied standard normals / sorted uniforms (fp64), which lets
+ *    the test harness feed the reference's exact draws.
+ */
+#ifndef PFBANK_H
+#define PFBANK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PF_OK 0
+#define PF_EINVAL (-22)
+#define PF_ECUDA (-5)
+
+#define PF_ST_DIVERGED 1u
+#define PF_ST_NAN_WEIGHT 2u
+
+typedef enum pf_dtype { PF_F32 = 0, PF_F64 = 1 } pf_dtype;
+
+/* Stochastic Lorenz-63 (models/lorenz63.py:22-69 + BASELINE cfg0/cfg2
+ * adapter).  obs_dim = 1 observes x1 (stock Lorenz63Model.log_likelihood,
+ * lorenz63.py:62-65); obs_dim = 2 observes (x1, x3). */
+typedef struct pf_lorenz_params {
+  double s, r, b, dt;
+  double noise_scale; /* multiplies the N(0,1) draws before the sqrt(dt) scaling */
+  double obs_var;
+  int32_t n_sub;   /* Euler substeps per observation interval */
+  int32_t obs_dim; /* 1 or 2 */
+} pf_lorenz_params;
+
+/* Lattice FitzHugh-Nagumo in the reference kernel's general form
+ * (accel.py:110-129): u' = u + dt(p3(u) - w) + dt(coupling*nb + drive)
+ * + sig_v*z; w' = w + dt(b0 u + b1 w + b2) [+ sig_w*z'], with
+ * drive = degree_drive * deg(i,j) * u (degree_drive = -1 gives the Neumann
+ * 5-point Laplacian of BASELINE cfg3/cfg4).  Observation: Gaussian on u at
+ * `n_obs` electrode nodes (fhn.py:199-207). */
+typedef struct pf_fhn_params {
+  int32_t rows, cols, n_sub, n_obs;
+  double dt, coupling;
+  double cubic[4]; /* a3, a2, a1, a0 */
+  double beta[3];  /* b0, b1, b2 */
+  double sig_v, sig_w;
+  double degree_drive;
+  double obs_var;
+} pf_fhn_params;
+
+/* ---- library ------------------------------------------------------- */
+const char *pf_last_error(void);
+int pf_version(void);
+int pf_device_sm_count(int *out);
+
+/* Philox4x32-10 known-answer helper: out[4] for ctr[4], key[2] (device). */
+int pf_philox_kat(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t n, void *stream);
+
+/* ---- L1 operator drop-ins (accel.py) --------------------------------- */
+/* accel.lorenz_euler_block (accel.py:60-102): states (n,3), noise
+ * (n_sub,n,3), fp64, reference evaluation order, no FMA -> bit-exact. */
+int pf_op_lorenz_euler_block(const double *states, const double *noise, int64_t n,
+                             int64_t n_sub, double dt, double s, double r, double b,
+                             double *out, void *stream);
+
+/* accel.fhn_euler_block (accel.py:110-167) for (n, J1, J2) fp64 lattices
+ * (rectangular allowed, unlike the reference jit twin accel.py:135). */
+int pf_op_fhn_euler_block(const double *U, const double *V, const double *drive,
+                          const double *noise, int64_t n, int32_t J1, int32_t J2, double dt,
+                          double coupling, const double *cubic4_host,
+                          const double *beta3_host, double sig_sqdt, double *u_new,
+                          double *v_new, void *stream);
+
+/* accel.resample_indices (accel.py:175-203): smallest k with cum[k] >= u,
+ * clamped to n-1; int64 out. */
+int pf_op_resample_indices(const double *cum, int64_t n, const double *u, int64_t m,
+                           int64_t *idx_out, void *stream);
+
+/* core.normalize_log_weights (core.py:116-138) for M segments of N.
+ * weights_out (M*N) fp64, log_mean_raw_out (M) fp64; collapsed[f] set
+ * on total underflow (weights untouched), status NaN flag on NaN. */
+int pf_op_normalize_log_weights(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
+                                double *weights_out, double *log_mean_raw_out,
+                                uint8_t *collapsed, uint32_t *status, void *stream);
+
+/* Explicit ancestor gather of a 3-plane state (filters.py:111 / cfg1):
+ * x_out[d][p] = x_in[d][anc[p]]. */
+int pf_gather_planes(pf_dtype dtype, const void *x_in, const int32_t *anc, int64_t MN,
+                     int32_t dims, void *x_out, void *stream);
+
+/* ---- L2-L4 bank kernels --------------------------------------------- */
+/* bf_init prior (filters.py:87-94 + lorenz63.py:42-44): x = mean + sd*z,
+ * z from Philox (purpose PRIOR) or z_tape (M,N,3) fp64. */
+int pf_lorenz_prior(pf_dtype dtype, void *x, int64_t M, int64_t N, const double *mean3_host,
+                    double prior_sd, const uint32_t *keys, const double *z_tape,
+                    void *stream);
+
+/* Broadcast one fp64 state row to every particle (deterministic priors,
+ * fhn.py:144-147 and the cfg3/4 stimulated point mass). */
+int pf_fill_rows(pf_dtype dtype, void *x, int64_t MN, int64_t row_len, const double *row,
+                 void *stream);
+
+/* bf_step propagate + weight (filters.py:103-104; lorenz63.py:46-65):
+ * x_out[p] = EM^{n_sub}(x_in[anc[p]]) (anc NULL = identity), logw_out[p] =
+ * log-likelihood of y (device, obs_dim doubles) at observation time t.
+ * z_tape (M, n_sub, N, 3) fp64 or NULL (Philox). */
+int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const void *x_in,
+                               const int32_t *anc, void *x_out, const double *y,
+                               void *logw_out, int64_t M, int64_t N, const uint32_t *keys,
+                               uint32_t t, const double *z_tape, uint32_t *status,
+                               void *stream);
+
+/* One FH-N observation interval: n_sub lattice Euler steps with the particle
+ * resident in shared memory/registers, ancestor gather fused into the load,
+ * electrode log-likelihood fused into the epilogue.
+ * z_tape (M, n_sub, 2, N, rows*cols) fp64 or NULL (Philox). */
+int pf_fhn_interval(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
+                    const int32_t *anc, void *x_out, const double *y, const int32_t *obs_idx,
+                    void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                    const double *z_tape, uint32_t *status, void *stream);
+
+/* normalize_log_weights + multinomial_resample_indices for M segments
+ * (core.py:116-138, resampling.py:21-43, accel.py:175-203):
+ * per-filter max / exp / sum in fp64, w = e/total, fp64 inclusive scan,
+ * sorted uniforms (u_tape (M,N) fp64, or Philox exponential spacings with an
+ * fp64 scan), merge -> anc_out[f*N + j] = f*N + k (int32, non-decreasing).
+ * lnc[f] += m + log(total) - log(N) unless collapsed.  ws may be NULL when
+ * pf_resample_workspace_bytes() returns 0. */
+size_t pf_resample_workspace_bytes(int64_t M, int64_t N);
+int pf_segmented_resample(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
+                          const double *u_tape, const uint32_t *keys, uint32_t t,
+                          int32_t *anc_out, double *lnc, uint8_t *collapsed, uint32_t *status,
+                          void *ws, size_t ws_bytes, void *stream);
+
+/* posterior_mean of the resampled set (core.py:154-156 via filters.py:188):
+ * est[f*dim + d] = (1/N) * sum_j x(anc[f*N+j], d) in a fixed order, fp64,
+ * with element (p, d) at x[p*stride_p + d*stride_d]. */
+int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,
+                       int32_t dim, const int32_t *anc, int64_t M, int64_t N, double *est_out,
+                       void *stream);
+
+/* average_estimates (ensemble.py:68-73): out[t][d] = (e_0 + e_1 + ...) / M,
+ * left to right over filters, fp64.  est is (T, M, dim), out is (T, dim). */
+int pf_ensemble_average(const double *est, int64_t T, int64_t M, int64_t dim, double *out,
+                        void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFBANK_H */

@@ -1,0 +1,230 @@
+"""The GPU filter bank: M independent bootstrap filters of N particles.
+
+This replaces, for the whole bank at once, the reference's per-filter Python
+loop run_filter -> bf_step (filters.py:97-112, 163-193) and the per-filter
+task loop of run_ensemble (ensemble.py:76-111).  One observation interval
+is three stream-ordered launches on device-resident state:
+
+  1. propagate+weight  (pf_lorenz_propagate_weight | pf_fhn_interval):
+     ancestor gather fused into the load, Euler-Maruyama steps in
+     registers/shared memory, Gaussian log-likelihood in the epilogue;
+  2. pf_segmented_resample: per-filter logsumexp, lnc update, collapse flag,
+     fp64 CDF scan, sorted uniforms, merge -> ancestors;
+  3. pf_filter_estimate: per-filter posterior mean of the resampled set.
+
+The resampled particle set is never materialised: the next interval loads
+x[anc[p]] directly (filters.py:111's ``propagated[idx]``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+
+@dataclass
+class DrawTape:
+    """Oracle-mode draws, indexed by GLOBAL filter id (rows).
+
+    prior:    (M, N, 3) standard normals (Lorenz) or None (deterministic prior)
+    noise:    per step k, (M, n_sub, N, 3) [Lorenz] or (M, n_sub, 2, N, nodes)
+              [FH-N] standard normals
+    uniforms: per step k, (M, N) sorted uniforms (rows of collapsed filters
+              are ignored - the reference draws none for them)
+    """
+
+    prior: np.ndarray | None = None
+    noise: list = field(default_factory=list)
+    uniforms: list = field(default_factory=list)
+
+
+def _torch_dtype(dtype):
+    import torch
+
+    if dtype in (None, "float64", "f64", np.float64, torch.float64):
+        return torch.float64
+    if dtype in ("float32", "f32", np.float32, torch.float32):
+        return torch.float32
+    raise ValueError(f"unsupported dtype {dtype!r}")
+
+
+class FilterBank:
+    """M_local filters of one model on the current CUDA device."""
+
+    def __init__(self, model, n_filters: int, n_particles: int, keys, n_steps: int, *,
+                 dtype=None, tape: DrawTape | None = None, filter_offset: int = 0,
+                 estimate: str = "full", est_buffer=None, est_row_offset: int = 0):
+        import torch
+
+        _lib.require_cuda()
+        if n_filters < 1 or n_particles < 1:
+            raise ValueError("n_filters and n_particles must be >= 1")
+        if n_filters * n_particles > 2**31 - 1:
+            raise ValueError("M*N per GPU must fit int32 particle indices")
+        if model.kind not in ("lorenz", "fhn"):
+            raise ValueError(f"model kind {model.kind!r} has no GPU descriptor")
+        self.model = model
+        self.M, self.N = int(n_filters), int(n_particles)
+        self.MN = self.M * self.N
+        self.T = int(n_steps)
+        self.dtype = _torch_dtype(dtype)
+        self.code = _lib.dtype_code(self.dtype)
+        self.tape = tape
+        self.offset = int(filter_offset)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        kw = dict(device=dev)
+
+        if model.kind == "lorenz":
+            self.x = [torch.empty((3, self.MN), dtype=self.dtype, **kw) for _ in range(2)]
+            self.params = model.params()
+            self.est_dim = 3
+            self.est_strides = (1, self.MN)
+        else:
+            self.x = [torch.empty((self.MN, model.dim_x), dtype=self.dtype, **kw)
+                      for _ in range(2)]
+            self.params = model.params()
+            self.obs_idx = torch.from_numpy(model.obs_indices.astype(np.int32)).to(dev)
+            self.est_dim = model.dim_x if estimate == "full" else model.nodes
+            self.est_strides = (model.dim_x, 1)
+        if estimate not in ("full", "projection"):
+            raise ValueError("estimate must be 'full' or 'projection'")
+        self.logw = torch.empty(self.MN, dtype=self.dtype, **kw)
+        self.anc = torch.empty(self.MN, dtype=torch.int32, **kw)
+        self.lnc = torch.zeros(self.M, dtype=torch.float64, **kw)
+        self.collapsed = torch.zeros(self.M, dtype=torch.uint8, **kw)
+        self.status = torch.zeros(self.M, dtype=torch.int32, **kw)
+        k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint32).reshape(self.M, 2))
+        self.keys = torch.from_numpy(k.view(np.int32)).to(dev)
+        ws = _lib.load().pf_resample_workspace_bytes(self.M, self.N)
+        self.ws_bytes = int(ws)
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, **kw)
+        if est_buffer is None:
+            self.est = torch.empty((self.T, self.M, self.est_dim), dtype=torch.float64, **kw)
+            self.est_row = 0
+        else:
+            self.est = est_buffer
+            self.est_row = int(est_row_offset)
+        self.lnc_tr = torch.empty((self.T, self.M), dtype=torch.float64, **kw)
+        self.coll_tr = torch.empty((self.T, self.M), dtype=torch.uint8, **kw)
+        self.obs = None
+        self.cur = 0
+        self.steps_done = 0
+        self.kernel_events = None  # optional (start, end) CUDA events around propagate
+
+    # -- setup ----------------------------------------------------------------
+    def load_observations(self, observations):
+        import torch
+
+        obs = np.atleast_2d(np.asarray(observations, dtype=np.float64))
+        if obs.shape[1] != self.model.dim_y:
+            raise ValueError(f"observations must have {self.model.dim_y} columns")
+        if obs.shape[0] < self.T:
+            raise ValueError("fewer observations than steps")
+        self.obs = torch.from_numpy(np.ascontiguousarray(obs[: self.T])).to(self.device)
+
+    def set_observation_buffer(self, obs_device):
+        """Use a caller-owned (T, dim_y) float64 device tensor (bench/e2e)."""
+        self.obs = obs_device
+
+    def _rows(self):
+        return slice(self.offset, self.offset + self.M)
+
+    def init(self):
+        """bf_init for every filter (filters.py:87-94)."""
+        import torch
+
+        s = _lib.stream_ptr()
+        m = self.model
+        if m.kind == "lorenz":
+            mean, mean_p = _lib.host_f64(m.prior_mean)
+            ztape = None
+            if self.tape is not None:
+                if self.tape.prior is None:
+                    raise ValueError("tape has no prior draws")
+                z = np.ascontiguousarray(self.tape.prior[self._rows()], dtype=np.float64)
+                ztape = torch.from_numpy(z).to(self.device)
+            _lib.call("pf_lorenz_prior", self.code, _lib.ptr(self.x[0]), self.M, self.N, mean_p,
+                      m.prior_sd(), _lib.ptr(self.keys), _lib.ptr(ztape), s)
+        else:
+            row = torch.from_numpy(m.initial_state()).to(self.device)
+            _lib.call("pf_fill_rows", self.code, _lib.ptr(self.x[0]), self.MN, m.dim_x,
+                      _lib.ptr(row), s)
+            self._row_keepalive = row
+        self.lnc.zero_()
+        self.status.zero_()
+        self.cur = 0
+        self.steps_done = 0
+
+    # -- one observation interval --------------------------------------------
+    def step(self, k: int):
+        import torch
+
+        if self.obs is None:
+            raise RuntimeError("load_observations() first")
+        t = k + 1
+        s = _lib.stream_ptr()
+        xin, xout = self.x[self.cur], self.x[1 - self.cur]
+        anc = self.anc if self.steps_done > 0 else None
+        y_ptr = _lib.c_vp(self.obs.data_ptr() + k * self.model.dim_y * 8)
+        noise = uni = None
+        if self.tape is not None:
+            noise = torch.from_numpy(np.ascontiguousarray(
+                self.tape.noise[k][self._rows()], dtype=np.float64)).to(self.device)
+            uni = torch.from_numpy(np.ascontiguousarray(
+                self.tape.uniforms[k][self._rows()], dtype=np.float64)).to(self.device)
+            self._tape_keepalive = (noise, uni)
+        if self.kernel_events is not None:
+            self.kernel_events[0].record()
+        if self.model.kind == "lorenz":
+            _lib.call("pf_lorenz_propagate_weight", self.params, self.code, _lib.ptr(xin),
+                      _lib.ptr(anc), _lib.ptr(xout), y_ptr, _lib.ptr(self.logw), self.M, self.N,
+                      _lib.ptr(self.keys), t, _lib.ptr(noise), _lib.ptr(self.status), s)
+        else:
+            _lib.call("pf_fhn_interval", self.params, self.code, _lib.ptr(xin), _lib.ptr(anc),
+                      _lib.ptr(xout), y_ptr, _lib.ptr(self.obs_idx), _lib.ptr(self.logw),
+                      self.M, self.N, _lib.ptr(self.keys), t, _lib.ptr(noise),
+                      _lib.ptr(self.status), s)
+        if self.kernel_events is not None:
+            self.kernel_events[1].record()
+        _lib.call("pf_segmented_resample", self.code, _lib.ptr(self.logw), self.M, self.N,
+                  _lib.ptr(uni), _lib.ptr(self.keys), t, _lib.ptr(self.anc), _lib.ptr(self.lnc),
+                  _lib.ptr(self.collapsed), _lib.ptr(self.status), _lib.ptr(self.ws),
+                  self.ws_bytes, s)
+        est_ptr = _lib.c_vp(self.est[k].data_ptr() + self.est_row * self.est_dim * 8)
+        sp, sd = self.est_strides
+        _lib.call("pf_filter_estimate", self.code, _lib.ptr(xout), sp, sd, self.est_dim,
+                  _lib.ptr(self.anc), self.M, self.N, est_ptr, s)
+        self.lnc_tr[k].copy_(self.lnc)
+        self.coll_tr[k].copy_(self.collapsed)
+        self.cur = 1 - self.cur
+        self.steps_done += 1
+
+    def run(self, on_step=None):
+        for k in range(self.T):
+            self.step(k)
+            if on_step is not None:
+                on_step(k)
+
+    # -- results ----------------------------------------------------------------
+    def check_status(self):
+        _lib.raise_status(self.status.cpu().numpy())
+
+    def particles(self) -> np.ndarray:
+        """Current (post-resampling) particle set, (M, N, dim_x) float64 host."""
+        import torch
+
+        x = self.x[self.cur]
+        anc = self.anc.long() if self.steps_done > 0 else torch.arange(self.MN, device=x.device)
+        if self.model.kind == "lorenz":
+            g = x[:, anc].t()
+        else:
+            g = x[anc]
+        return g.to(torch.float64).reshape(self.M, self.N, -1).cpu().numpy()
+
+    def collapse_steps(self) -> list[list[int]]:
+        c = self.coll_tr.cpu().numpy()
+        return [[int(k) + 1 for k in np.nonzero(c[:, f])[0]] for f in range(self.M)]

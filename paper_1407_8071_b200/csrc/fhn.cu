@@ -1,0 +1,368 @@
+// FitzHugh-Nagumo lattice kernels.
+//
+//  * pf_fhn_interval       - one observation interval of the bank: n_sub
+//                            lattice Euler steps (accel.py:110-129 per step)
+//                            + Gaussian electrode log-likelihood
+//                            (fhn.py:199-207), ancestor gather fused into
+//                            the load (filters.py:111).
+//  * pf_op_fhn_euler_block - the accel.fhn_euler_block operator (fp64).
+//
+// Design: one CTA owns one particle for the whole interval.
+// The lattice (rows x cols, v and w) lives in registers - each thread owns a
+// vertical strip of R rows of one column - and v is exchanged through a
+// double-buffered shared-memory plane for the 5-point stencil, one barrier
+// per Euler step.  HBM sees the particle once per interval (gathered load +
+// store), i.e. 50x less traffic than streaming every Euler step, which
+// turns the kernel from HBM-bound into issue-bound (RNG dominated).
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace pf {
+
+constexpr int kFhnRows = 6;  // rows per thread (even: Philox pairs rows)
+
+struct FhnConsts {
+  int rows, cols, n_sub, n_obs, nseg, nodes;
+  double dt, coupling, a3, a2, a1, a0, b0, b1, b2, sig_v, sig_w, degree_drive, obs_coef;
+};
+
+// One node update in the reference order (accel.py:121-128) plus w-noise.
+template <typename T>
+__device__ __forceinline__ void fhn_node(T u, T w, T nb, T negdeg, T zv, T zw,
+                                         const FhnConsts &c, T &u_new, T &w_new) {
+  using A = Ar<T>;
+  const T dt = T(c.dt);
+  const T p3 = A::add(A::mul(A::add(A::mul(A::add(A::mul(T(c.a3), u), T(c.a2)), u), T(c.a1)), u),
+                      T(c.a0));
+  const T drive = A::mul(negdeg, u);
+  const T t1 = A::add(u, A::mul(dt, A::sub(p3, w)));
+  const T t2 = A::add(t1, A::mul(dt, A::add(A::mul(T(c.coupling), nb), drive)));
+  u_new = A::add(t2, A::mul(T(c.sig_v), zv));
+  const T wn = A::add(w, A::mul(dt, A::add(A::add(A::mul(T(c.b0), u), A::mul(T(c.b1), w)), T(c.b2))));
+  w_new = A::add(wn, A::mul(T(c.sig_w), zw));
+}
+
+// MODE 0 = Philox, MODE 1 = tape (M, n_sub, 2, N, nodes) fp64.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) fhn_interval_kernel(
+    const T *__restrict__ xin, const int32_t *__restrict__ anc, T *__restrict__ xout,
+    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, T *__restrict__ logw,
+    int64_t MN, int32_t N, FhnConsts c, const uint32_t *__restrict__ keys, uint32_t t,
+    const double *__restrict__ tape, uint32_t *__restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *vs = reinterpret_cast<T *>(smem_raw);  // [2][nodes]
+  __shared__ double red[8];
+  __shared__ int bad;
+
+  const int tid = threadIdx.x;
+  const int seg = tid / c.cols;
+  const int col = tid - seg * c.cols;
+  const bool active = seg < c.nseg;
+  const int row0 = seg * kFhnRows;
+
+  for (int64_t p = blockIdx.x; p < MN; p += gridDim.x) {
+    const int64_t f = p / N;
+    const int32_t j = static_cast<int32_t>(p - f * N);
+    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+    const T *xs = xin + src * 2 * static_cast<int64_t>(c.nodes);
+    if (tid == 0) bad = 0;
+
+    T v[kFhnRows], w[kFhnRows], negdeg[kFhnRows];
+#pragma unroll
+    for (int r = 0; r < kFhnRows; ++r) {
+      const int row = row0 + r;
+      v[r] = T(0);
+      w[r] = T(0);
+      negdeg[r] = T(0);
+      if (active && row < c.rows) {
+        const int node = row * c.cols + col;
+        v[r] = xs[node];
+        w[r] = xs[c.nodes + node];
+        const int deg = (row > 0) + (row < c.rows - 1) + (col > 0) + (col < c.cols - 1);
+        negdeg[r] = T(c.degree_drive * deg);
+        vs[node] = v[r];
+      }
+    }
+    __syncthreads();
+
+    Key2 key{0u, 0u};
+    if (MODE == 0) key = load_key(keys, f);
+    const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
+    int buf = 0;
+    for (int k = 0; k < c.n_sub; ++k) {
+      const T *cur = vs + buf * c.nodes;
+      T *nxt = vs + (buf ^ 1) * c.nodes;
+      if (active) {
+        T zv[kFhnRows], zw[kFhnRows];
+        if (MODE == 0) {
+          // one Philox block = (zv, zw) for a pair of rows of this column
+#pragma unroll
+          for (int q = 0; q < kFhnRows / 2; ++q) {
+            const uint32_t node_pair =
+                static_cast<uint32_t>(((row0 >> 1) + q) * c.cols + col);
+            const uint4 rr = philox10(make_uint4(static_cast<uint32_t>(j), step0 + k, node_pair,
+                                                 kPurposeFhn),
+                                      key);
+            if (sizeof(T) == 4) {
+              const float2 g0 = box_muller_f32(rr.x, rr.y);
+              const float2 g1 = box_muller_f32(rr.z, rr.w);
+              zv[2 * q] = T(g0.x);
+              zw[2 * q] = T(g0.y);
+              zv[2 * q + 1] = T(g1.x);
+              zw[2 * q + 1] = T(g1.y);
+            } else {
+              const double2 g0 = box_muller_f64(rr.x, rr.y, rr.z, rr.w);
+              const uint4 r2 = philox10(make_uint4(static_cast<uint32_t>(j), step0 + k,
+                                                   node_pair | 0x80000000u, kPurposeFhn),
+                                        key);
+              const double2 g1 = box_muller_f64(r2.x, r2.y, r2.z, r2.w);
+              zv[2 * q] = T(g0.x);
+              zw[2 * q] = T(g0.y);
+              zv[2 * q + 1] = T(g1.x);
+              zw[2 * q + 1] = T(g1.y);
+            }
+          }
+        } else {
+          const int64_t base =
+              ((f * c.n_sub + k) * 2 * static_cast<int64_t>(N) + j) * c.nodes;
+          const int64_t wofs = static_cast<int64_t>(N) * c.nodes;
+#pragma unroll
+          for (int r = 0; r < kFhnRows; ++r) {
+            const int row = row0 + r;
+            zv[r] = T(0);
+            zw[r] = T(0);
+            if (row < c.rows) {
+              zv[r] = T(tape[base + row * c.cols + col]);
+              zw[r] = T(tape[base + wofs + row * c.cols + col]);
+            }
+          }
+        }
+        T vn[kFhnRows], wn[kFhnRows];
+#pragma unroll
+        for (int r = 0; r < kFhnRows; ++r) {
+          const int row = row0 + r;
+          vn[r] = v[r];
+          wn[r] = w[r];
+          if (row < c.rows) {
+            // neighbour sum in the reference order: up, down, left, right
+            T nb = T(0);
+            if (row > 0) nb = Ar<T>::add(nb, r > 0 ? v[r - 1] : cur[(row - 1) * c.cols + col]);
+            if (row < c.rows - 1)
+              nb = Ar<T>::add(nb, r < kFhnRows - 1 ? v[r + 1] : cur[(row + 1) * c.cols + col]);
+            if (col > 0) nb = Ar<T>::add(nb, cur[row * c.cols + col - 1]);
+            if (col < c.cols - 1) nb = Ar<T>::add(nb, cur[row * c.cols + col + 1]);
+            fhn_node<T>(v[r], w[r], nb, negdeg[r], zv[r], zw[r], c, vn[r], wn[r]);
+            nxt[row * c.cols + col] = vn[r];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kFhnRows; ++r) {
+          v[r] = vn[r];
+          w[r] = wn[r];
+        }
+      }
+      __syncthreads();
+      buf ^= 1;
+    }
+
+    // ---- epilogue: divergence, store, electrode log-likelihood ----------
+    bool fin = true;
+    T *xd = xout + p * 2 * static_cast<int64_t>(c.nodes);
+#pragma unroll
+    for (int r = 0; r < kFhnRows; ++r) {
+      const int row = row0 + r;
+      if (active && row < c.rows) {
+        const int node = row * c.cols + col;
+        fin = fin && finite_val(v[r]) && finite_val(w[r]);
+        xd[node] = v[r];
+        xd[c.nodes + node] = w[r];
+      }
+    }
+    if (!fin) bad = 1;
+    const T *fin_v = vs + buf * c.nodes;
+    if (tid < 32) {
+      // numpy pairwise order for n <= 128 (8 strided accumulators, then
+      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder) - the
+      // order of np.sum(resid*resid, axis=1) in fhn.py:207.
+      const int n = c.n_obs;
+      const int lane = tid;
+      double acc = 0.0;
+      const int nblk = n - (n % 8);
+      if (n >= 8 && lane < 8) {
+        for (int i = lane; i < nblk; i += 8) {
+          const double rsd = __dsub_rn(y[i], double(fin_v[obs_idx[i]]));
+          const double sq = __dmul_rn(rsd, rsd);
+          acc = (i == lane) ? sq : __dadd_rn(acc, sq);
+        }
+      }
+      // combine ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+      const double o1 = __shfl_down_sync(0xffffffffu, acc, 1);
+      const double s01 = __dadd_rn(acc, o1);  // lanes 0,2,4,6 hold pairs
+      const double o2 = __shfl_down_sync(0xffffffffu, s01, 2);
+      const double s0123 = __dadd_rn(s01, o2);  // lanes 0,4
+      const double o4 = __shfl_down_sync(0xffffffffu, s0123, 4);
+      if (lane == 0) {
+        double res;
+        int i;
+        if (n >= 8) {
+          res = __dadd_rn(s0123, o4);
+          i = nblk;
+        } else {
+          res = 0.0;
+          i = 0;
+        }
+        for (; i < n; ++i) {
+          const double rsd = __dsub_rn(y[i], double(fin_v[obs_idx[i]]));
+          res = __dadd_rn(res, __dmul_rn(rsd, rsd));
+        }
+        red[0] = res;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      logw[p] = T(__dmul_rn(c.obs_coef, red[0]));
+      if (bad) atomicOr(status + f, PF_ST_DIVERGED);
+    }
+    __syncthreads();
+  }
+}
+
+// accel.fhn_euler_block (general form, fp64, per-node drive), one thread per
+// node, reference order.
+__global__ void fhn_block_op_kernel(const double *__restrict__ U, const double *__restrict__ V,
+                                    const double *__restrict__ drive,
+                                    const double *__restrict__ noise, int64_t total, int J1,
+                                    int J2, FhnConsts c, double *__restrict__ un,
+                                    double *__restrict__ vn) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= total) return;
+  const int64_t plane = static_cast<int64_t>(J1) * J2;
+  const int64_t p = g / plane;
+  const int rem = static_cast<int>(g - p * plane);
+  const int i = rem / J2, j = rem - (rem / J2) * J2;
+  const double *Up = U + p * plane;
+  using A = Ar<double>;
+  double nb = 0.0;
+  if (i > 0) nb = A::add(nb, Up[(i - 1) * J2 + j]);
+  if (i < J1 - 1) nb = A::add(nb, Up[(i + 1) * J2 + j]);
+  if (j > 0) nb = A::add(nb, Up[i * J2 + j - 1]);
+  if (j < J2 - 1) nb = A::add(nb, Up[i * J2 + j + 1]);
+  const double u = U[g], v = V[g];
+  const double p3 = A::add(A::mul(A::add(A::mul(A::add(A::mul(c.a3, u), c.a2), u), c.a1), u), c.a0);
+  const double t1 = A::add(u, A::mul(c.dt, A::sub(p3, v)));
+  const double t2 = A::add(t1, A::mul(c.dt, A::add(A::mul(c.coupling, nb), drive[g])));
+  un[g] = A::add(t2, A::mul(c.sig_v, noise[g]));
+  vn[g] = A::add(v, A::mul(c.dt, A::add(A::add(A::mul(c.b0, u), A::mul(c.b1, v)), c.b2)));
+}
+
+static FhnConsts make_consts(const pf_fhn_params *p) {
+  FhnConsts c;
+  c.rows = p->rows;
+  c.cols = p->cols;
+  c.n_sub = p->n_sub;
+  c.n_obs = p->n_obs;
+  c.nseg = (p->rows + kFhnRows - 1) / kFhnRows;
+  c.nodes = p->rows * p->cols;
+  c.dt = p->dt;
+  c.coupling = p->coupling;
+  c.a3 = p->cubic[0];
+  c.a2 = p->cubic[1];
+  c.a1 = p->cubic[2];
+  c.a0 = p->cubic[3];
+  c.b0 = p->beta[0];
+  c.b1 = p->beta[1];
+  c.b2 = p->beta[2];
+  c.sig_v = p->sig_v;
+  c.sig_w = p->sig_w;
+  c.degree_drive = p->degree_drive;
+  c.obs_coef = -0.5 / p->obs_var;  // fhn.py:207: -0.5 / obs_var * sum
+  return c;
+}
+
+template <typename T, int MODE>
+static int launch_fhn(const FhnConsts &c, const void *x_in, const int32_t *anc, void *x_out,
+                      const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
+                      int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
+                      uint32_t *status, cudaStream_t s) {
+  const int threads = ((c.nseg * c.cols + 31) / 32) * 32;
+  const size_t smem = 2 * static_cast<size_t>(c.nodes) * sizeof(T);
+  auto kern = fhn_interval_kernel<T, MODE>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int sms = kSmCount;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(MN, static_cast<int64_t>(sms) * per_sm * 16);
+  kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(
+      static_cast<const T *>(x_in), anc, static_cast<T *>(x_out), y, obs_idx,
+      static_cast<T *>(logw), MN, N, c, keys, t, tape, status);
+  return check_launch("pf_fhn_interval");
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_fhn_interval(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
+                    const int32_t *anc, void *x_out, const double *y, const int32_t *obs_idx,
+                    void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                    const double *z_tape, uint32_t *status, void *stream) {
+  PF_REQUIRE(p && x_in && x_out && y && obs_idx && logw_out && status, "pf_fhn_interval: null");
+  PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_fhn_interval: bad M/N");
+  PF_REQUIRE(p->rows >= 1 && p->cols >= 1 && p->n_sub >= 0, "pf_fhn_interval: bad lattice");
+  PF_REQUIRE(p->n_obs >= 1 && p->n_obs <= 128, "pf_fhn_interval: need 1 <= n_obs <= 128");
+  PF_REQUIRE(t >= 1, "pf_fhn_interval: t is 1-based");
+  PF_REQUIRE(z_tape || keys, "pf_fhn_interval: need keys (Philox) or z_tape");
+  PF_REQUIRE(x_in != x_out, "pf_fhn_interval: x_in and x_out must not alias");
+  const FhnConsts c = make_consts(p);
+  PF_REQUIRE(c.nseg * c.cols <= 256, "pf_fhn_interval: lattice too large for one CTA (%d threads)",
+             c.nseg * c.cols);
+  const int64_t MN = M * N;
+  const int32_t n32 = static_cast<int32_t>(N);
+  const cudaStream_t s = as_stream(stream);
+  if (dtype == PF_F64)
+    return z_tape ? launch_fhn<double, 1>(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32,
+                                          keys, t, z_tape, status, s)
+                  : launch_fhn<double, 0>(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32,
+                                          keys, t, z_tape, status, s);
+  return z_tape ? launch_fhn<float, 1>(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32, keys,
+                                       t, z_tape, status, s)
+                : launch_fhn<float, 0>(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32, keys,
+                                       t, z_tape, status, s);
+}
+
+int pf_op_fhn_euler_block(const double *U, const double *V, const double *drive,
+                          const double *noise, int64_t n, int32_t J1, int32_t J2, double dt,
+                          double coupling, const double *cubic4_host,
+                          const double *beta3_host, double sig_sqdt, double *u_new,
+                          double *v_new, void *stream) {
+  PF_REQUIRE(U && V && drive && noise && u_new && v_new && cubic4_host && beta3_host,
+             "pf_op_fhn_euler_block: null");
+  PF_REQUIRE(n >= 1 && J1 >= 1 && J2 >= 1, "pf_op_fhn_euler_block: bad shape");
+  pf_fhn_params p{};
+  p.rows = J1;
+  p.cols = J2;
+  p.n_sub = 1;
+  p.n_obs = 1;
+  p.dt = dt;
+  p.coupling = coupling;
+  for (int i = 0; i < 4; ++i) p.cubic[i] = cubic4_host[i];
+  for (int i = 0; i < 3; ++i) p.beta[i] = beta3_host[i];
+  p.sig_v = sig_sqdt;
+  p.sig_w = 0.0;
+  p.degree_drive = 0.0;
+  p.obs_var = 1.0;
+  const FhnConsts c = make_consts(&p);
+  const int64_t total = n * J1 * static_cast<int64_t>(J2);
+  fhn_block_op_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
+      U, V, drive, noise, total, J1, J2, c, u_new, v_new);
+  return check_launch("pf_op_fhn_euler_block");
+}
+
+}  // extern "C"

@@ -1,0 +1,295 @@
+// Stochastic Lorenz-63 bank kernels.
+//
+//  * pf_lorenz_prior            - bf_init / Lorenz63Model.sample_prior
+//                                 (filters.py:87-94, lorenz63.py:42-44)
+//  * pf_lorenz_propagate_weight - bf_step propagate + weight
+//                                 (filters.py:103-104, lorenz63.py:46-65,
+//                                 accel.py:60-102), ancestor gather fused
+//                                 into the load (filters.py:111)
+//  * pf_op_lorenz_euler_block   - the accel.lorenz_euler_block operator
+//
+// One thread owns one particle and keeps its 3-vector in registers for all
+// n_sub Euler substeps of an observation interval; the only HBM traffic is
+// the gathered load (3 values), the store (3 values) and the log-weight.
+// Production mode generates the Gaussian increments in-register with
+// Philox4x32-10 + Box-Muller; tape mode reads the reference's exact draws.
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace pf {
+
+struct LorenzConsts {
+  double s, r, b, dt, dts, sq, ns, two_obs_var;
+  int n_sub;
+};
+
+// One Euler-Maruyama substep in the reference's evaluation order
+// (accel.py:73-75).  For double every op rounds once (bit-exact with the
+// numpy/numba twins); for float nvcc contracts to FFMA.
+template <typename T>
+__device__ __forceinline__ void lorenz_substep(T &x1, T &x2, T &x3, T z1, T z2, T z3,
+                                               const LorenzConsts &c) {
+  using A = Ar<T>;
+  const T dt = T(c.dt), dts = T(c.dts), sq = T(c.sq), ns = T(c.ns);
+  const T r = T(c.r), b = T(c.b);
+  const T n1 = A::add(A::sub(x1, A::mul(dts, A::sub(x1, x2))), A::mul(sq, A::mul(ns, z1)));
+  const T n2 = A::add(A::add(x2, A::mul(dt, A::sub(A::sub(A::mul(r, x1), x2), A::mul(x1, x3)))),
+                      A::mul(sq, A::mul(ns, z2)));
+  const T n3 = A::add(A::add(x3, A::mul(dt, A::sub(A::mul(x1, x2), A::mul(b, x3)))),
+                      A::mul(sq, A::mul(ns, z3)));
+  x1 = n1;
+  x2 = n2;
+  x3 = n3;
+}
+
+// fp32 production substep: constants pre-folded (sq*ns), explicit FFMA.
+__device__ __forceinline__ void lorenz_substep_fast(float &x1, float &x2, float &x3, float z1,
+                                                    float z2, float z3, float dt, float ndts,
+                                                    float r, float nb, float cz) {
+  const float n1 = fmaf(cz, z1, fmaf(ndts, x1 - x2, x1));
+  const float t2 = fmaf(-x1, x3, fmaf(r, x1, -x2));
+  const float n2 = fmaf(cz, z2, fmaf(dt, t2, x2));
+  const float t3 = fmaf(nb, x3, x1 * x2);
+  const float n3 = fmaf(cz, z3, fmaf(dt, t3, x3));
+  x1 = n1;
+  x2 = n2;
+  x3 = n3;
+}
+
+// log-likelihood, lorenz63.py:62-65 (obs_dim 1) / SURVEY §8a-A8 (obs_dim 2)
+template <typename T>
+__device__ __forceinline__ T lorenz_loglik(T x1, T x3, const double *y, int obs_dim,
+                                           double two_obs_var) {
+  using A = Ar<T>;
+  if (obs_dim == 1) {
+    const T r0 = A::sub(T(y[0]), x1);
+    return -A::mul(r0, r0) / T(two_obs_var);
+  }
+  const T r0 = A::sub(T(y[0]), x1);
+  const T r1 = A::sub(T(y[1]), x3);
+  return -A::add(A::mul(r0, r0), A::mul(r1, r1)) / T(two_obs_var);
+}
+
+template <typename T>
+__global__ void lorenz_prior_kernel(T *__restrict__ x, int64_t MN, int32_t N, double m0,
+                                    double m1, double m2, double sd,
+                                    const uint32_t *__restrict__ keys,
+                                    const double *__restrict__ tape) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= MN) return;
+  double z0, z1, z2;
+  if (tape) {
+    z0 = tape[p * 3 + 0];
+    z1 = tape[p * 3 + 1];
+    z2 = tape[p * 3 + 2];
+  } else {
+    const int64_t f = p / N;
+    const uint32_t j = static_cast<uint32_t>(p - f * N);
+    const Key2 key = load_key(keys, f);
+    const uint4 a = philox10(make_uint4(j, 0u, 0u, kPurposePrior), key);
+    const uint4 b = philox10(make_uint4(j, 0u, 1u, kPurposePrior), key);
+    const double2 g0 = box_muller_f64(a.x, a.y, a.z, a.w);
+    const double2 g1 = box_muller_f64(b.x, b.y, b.z, b.w);
+    z0 = g0.x;
+    z1 = g0.y;
+    z2 = g1.x;
+  }
+  // mean + sqrt(var) * z  (lorenz63.py:44), one rounding per op
+  x[p] = static_cast<T>(__dadd_rn(m0, __dmul_rn(sd, z0)));
+  x[MN + p] = static_cast<T>(__dadd_rn(m1, __dmul_rn(sd, z1)));
+  x[2 * MN + p] = static_cast<T>(__dadd_rn(m2, __dmul_rn(sd, z2)));
+}
+
+// ---- propagate + weight -------------------------------------------------
+// MODE 0: Philox; MODE 1: tape (M, n_sub, N, 3) fp64.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) lorenz_pw_kernel(
+    const T *__restrict__ xin, const int32_t *__restrict__ anc, T *__restrict__ xout,
+    const double *__restrict__ y, T *__restrict__ logw, int64_t MN, int32_t N, int obs_dim,
+    LorenzConsts c, const uint32_t *__restrict__ keys, uint32_t t,
+    const double *__restrict__ tape, uint32_t *__restrict__ status) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= MN) return;
+  const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+  T x1 = xin[src], x2 = xin[MN + src], x3 = xin[2 * MN + src];
+  const int64_t f = p / N;
+  const int32_t j = static_cast<int32_t>(p - f * N);
+
+  if (MODE == 1) {
+    const double *z = tape + (f * c.n_sub * static_cast<int64_t>(N) + j) * 3;
+    const int64_t kstride = static_cast<int64_t>(N) * 3;
+    for (int k = 0; k < c.n_sub; ++k) {
+      const double *zk = z + k * kstride;
+      lorenz_substep<T>(x1, x2, x3, T(zk[0]), T(zk[1]), T(zk[2]), c);
+    }
+  } else if (sizeof(T) == 4) {
+    // 4 substeps = 12 normals = 3 Philox blocks
+    const Key2 key = load_key(keys, f);
+    const float dt = float(c.dt), ndts = float(-c.dts), r = float(c.r), nb = float(-c.b);
+    const float cz = float(c.sq * c.ns);
+    float a1 = float(x1), a2 = float(x2), a3 = float(x3);
+    for (int k0 = 0; k0 < c.n_sub; k0 += 4) {
+      float z[12];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const uint4 rr = philox10(
+            make_uint4(static_cast<uint32_t>(j), t, static_cast<uint32_t>((k0 >> 2) * 3 + q),
+                       kPurposeLorenz),
+            key);
+        const float2 g0 = box_muller_f32(rr.x, rr.y);
+        const float2 g1 = box_muller_f32(rr.z, rr.w);
+        z[4 * q + 0] = g0.x;
+        z[4 * q + 1] = g0.y;
+        z[4 * q + 2] = g1.x;
+        z[4 * q + 3] = g1.y;
+      }
+      if (k0 + 4 <= c.n_sub) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r, nb,
+                              cz);
+      } else {
+        for (int q = 0; q < c.n_sub - k0; ++q)
+          lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r, nb,
+                              cz);
+      }
+    }
+    x1 = T(a1);
+    x2 = T(a2);
+    x3 = T(a3);
+  } else {
+    // fp64 Philox: 2 substeps = 6 normals = 3 Philox blocks (fp64 Box-Muller)
+    const Key2 key = load_key(keys, f);
+    for (int k0 = 0; k0 < c.n_sub; k0 += 2) {
+      double z[6];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const uint4 rr = philox10(
+            make_uint4(static_cast<uint32_t>(j), t, static_cast<uint32_t>((k0 >> 1) * 3 + q),
+                       kPurposeLorenz),
+            key);
+        const double2 g = box_muller_f64(rr.x, rr.y, rr.z, rr.w);
+        z[2 * q] = g.x;
+        z[2 * q + 1] = g.y;
+      }
+      lorenz_substep<T>(x1, x2, x3, T(z[0]), T(z[1]), T(z[2]), c);
+      if (k0 + 1 < c.n_sub) lorenz_substep<T>(x1, x2, x3, T(z[3]), T(z[4]), T(z[5]), c);
+    }
+  }
+
+  if (!(finite_val(x1) && finite_val(x2) && finite_val(x3)))
+    atomicOr(status + f, PF_ST_DIVERGED);
+  xout[p] = x1;
+  xout[MN + p] = x2;
+  xout[2 * MN + p] = x3;
+  logw[p] = lorenz_loglik<T>(x1, x3, y, obs_dim, c.two_obs_var);
+}
+
+// accel.lorenz_euler_block: states (n,3) row-major, noise (n_sub, n, 3)
+__global__ void lorenz_block_op_kernel(const double *__restrict__ st,
+                                       const double *__restrict__ nz, int64_t n,
+                                       LorenzConsts c, double *__restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  double x1 = st[3 * i], x2 = st[3 * i + 1], x3 = st[3 * i + 2];
+  for (int k = 0; k < c.n_sub; ++k) {
+    const double *z = nz + (k * n + i) * 3;
+    lorenz_substep<double>(x1, x2, x3, z[0], z[1], z[2], c);
+  }
+  out[3 * i] = x1;
+  out[3 * i + 1] = x2;
+  out[3 * i + 2] = x3;
+}
+
+static LorenzConsts make_consts(const pf_lorenz_params *p) {
+  LorenzConsts c;
+  c.s = p->s;
+  c.r = p->r;
+  c.b = p->b;
+  c.dt = p->dt;
+  c.dts = p->dt * p->s;  // (dt * s), accel.py:73
+  c.sq = std::sqrt(p->dt);
+  c.ns = p->noise_scale;
+  c.two_obs_var = 2.0 * p->obs_var;
+  c.n_sub = p->n_sub;
+  return c;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+int pf_lorenz_prior(pf_dtype dtype, void *x, int64_t M, int64_t N, const double *mean3_host,
+                    double prior_sd, const uint32_t *keys, const double *z_tape,
+                    void *stream) {
+  PF_REQUIRE(x && mean3_host && M >= 1 && N >= 1, "pf_lorenz_prior: bad arguments");
+  PF_REQUIRE(z_tape || keys, "pf_lorenz_prior: need keys (Philox) or z_tape");
+  PF_REQUIRE(N <= INT32_MAX && M * N <= INT32_MAX, "pf_lorenz_prior: M*N exceeds int32 range");
+  const int64_t MN = M * N;
+  const cudaStream_t s = as_stream(stream);
+  if (dtype == PF_F64)
+    lorenz_prior_kernel<double><<<grid_for(MN, 256), 256, 0, s>>>(
+        static_cast<double *>(x), MN, static_cast<int32_t>(N), mean3_host[0], mean3_host[1],
+        mean3_host[2], prior_sd, keys, z_tape);
+  else
+    lorenz_prior_kernel<float><<<grid_for(MN, 256), 256, 0, s>>>(
+        static_cast<float *>(x), MN, static_cast<int32_t>(N), mean3_host[0], mean3_host[1],
+        mean3_host[2], prior_sd, keys, z_tape);
+  return check_launch("pf_lorenz_prior");
+}
+
+int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const void *x_in,
+                               const int32_t *anc, void *x_out, const double *y,
+                               void *logw_out, int64_t M, int64_t N, const uint32_t *keys,
+                               uint32_t t, const double *z_tape, uint32_t *status,
+                               void *stream) {
+  PF_REQUIRE(p && x_in && x_out && y && logw_out && status, "pf_lorenz_propagate_weight: null");
+  PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_lorenz_propagate_weight: bad M/N");
+  PF_REQUIRE(p->n_sub >= 0, "substeps must be >= 0");
+  PF_REQUIRE(p->obs_dim == 1 || p->obs_dim == 2, "obs_dim must be 1 or 2");
+  PF_REQUIRE(z_tape || keys, "need keys (Philox) or z_tape");
+  PF_REQUIRE(x_in != x_out, "x_in and x_out must not alias");
+  const LorenzConsts c = make_consts(p);
+  const int64_t MN = M * N;
+  const cudaStream_t s = as_stream(stream);
+  const unsigned grid = grid_for(MN, 256);
+  const int32_t n32 = static_cast<int32_t>(N);
+  if (dtype == PF_F64) {
+    auto *xi = static_cast<const double *>(x_in);
+    auto *xo = static_cast<double *>(x_out);
+    auto *lw = static_cast<double *>(logw_out);
+    if (z_tape)
+      lorenz_pw_kernel<double, 1><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
+                                                       c, keys, t, z_tape, status);
+    else
+      lorenz_pw_kernel<double, 0><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
+                                                       c, keys, t, z_tape, status);
+  } else {
+    auto *xi = static_cast<const float *>(x_in);
+    auto *xo = static_cast<float *>(x_out);
+    auto *lw = static_cast<float *>(logw_out);
+    if (z_tape)
+      lorenz_pw_kernel<float, 1><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
+                                                      c, keys, t, z_tape, status);
+    else
+      lorenz_pw_kernel<float, 0><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
+                                                      c, keys, t, z_tape, status);
+  }
+  return check_launch("pf_lorenz_propagate_weight");
+}
+
+int pf_op_lorenz_euler_block(const double *states, const double *noise, int64_t n,
+                             int64_t n_sub, double dt, double s, double r, double b,
+                             double *out, void *stream) {
+  PF_REQUIRE(states && out && n >= 1 && n_sub >= 0 && (noise || n_sub == 0),
+             "pf_op_lorenz_euler_block: bad arguments");
+  pf_lorenz_params p{s, r, b, dt, 1.0, 1.0, static_cast<int32_t>(n_sub), 1};
+  LorenzConsts c = make_consts(&p);
+  lorenz_block_op_kernel<<<grid_for(n, 128), 128, 0, as_stream(stream)>>>(states, noise, n, c,
+                                                                           out);
+  return check_launch("pf_op_lorenz_euler_block");
+}
+
+}  // extern "C"

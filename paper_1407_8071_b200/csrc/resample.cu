@@ -1,0 +1,490 @@
+// Per-filter logsumexp normalisation + multinomial resampling (segmented).
+//
+// Reference (paths under parpf/):
+//   normalize_log_weights   core.py:116-138   max, exp(lw-m), sum, w=e/total,
+//                                             log_mean_raw = m + log(total) - log(N)
+//   multinomial_resample_*  resampling.py:29-43  cum = cumsum(w) (fp64)
+//   _sorted_uniforms        resampling.py:21-26  c = cumsum(Exp(1) x (N+1)); u = c[:N]/c[N]
+//   resample_indices        accel.py:175-203     smallest k: cum[k] >= u, clamp N-1
+//   bf_step collapse        filters.py:105-109   all -inf -> uniform, lnc unchanged
+//
+// Two paths, same arithmetic:
+//  * bank path (N <= kBankMaxN): one CTA per filter, the filter's cum and u
+//    resident in shared memory; one launch does everything.
+//  * wide path (larger N, e.g. M=1 x N=2^26): tile kernels over HBM with a
+//    per-filter tile-offset pass (max -> sum -> tile scan offsets -> cum ->
+//    merge), workspace from pf_resample_workspace_bytes().
+// Everything is fp64 (the reference upcasts: core.py:126, resampling.py:11);
+// fp32 CDFs lose ~94% of ancestors at N=2^26 (SURVEY §7 hard part 1).
+#include "block_ops.cuh"
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace pf {
+
+constexpr int kBankMaxN = 8192;
+constexpr int kBankThreads = 256;
+constexpr int kTile = 4096;          // wide path elements per tile
+constexpr int kTileThreads = 256;
+
+// E_j for sorted uniforms: Philox block (j>>1, t, 0, RSMP), two fp64
+// exponentials per block.
+__device__ __forceinline__ double spacing_exp(Key2 key, uint32_t t, int64_t j) {
+  const uint4 r = philox10(make_uint4(static_cast<uint32_t>(j >> 1),
+                                      t, static_cast<uint32_t>(j >> 33), kPurposeResample),
+                           key);
+  return (j & 1) ? exp1_f64(r.z, r.w) : exp1_f64(r.x, r.y);
+}
+
+template <typename TW>
+__device__ __forceinline__ double load_lw(const TW *p) {
+  return static_cast<double>(*p);
+}
+
+// ---- bank path: one CTA per filter --------------------------------------
+template <typename TW, int MODE>
+__global__ void __launch_bounds__(kBankThreads) resample_bank_kernel(
+    const TW *__restrict__ logw, int32_t N, const double *__restrict__ u_tape,
+    const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
+    double *__restrict__ lnc, uint8_t *__restrict__ collapsed, uint32_t *__restrict__ status) {
+  extern __shared__ double sm[];
+  double *s_cum = sm;      // N
+  double *s_u = sm + N;    // N
+  __shared__ double scratch[33];
+  const int tid = threadIdx.x;
+  const int64_t f = blockIdx.x;
+  const int64_t base = f * N;
+
+  // 1. load + max (+ NaN detection: np.max propagates NaN, core.py:132)
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int i = tid; i < N; i += blockDim.x) {
+    const double v = load_lw(logw + base + i);
+    s_cum[i] = v;
+    nan |= isnan(v);
+    mx = fmax(mx, v);
+  }
+  nan = __syncthreads_or(nan);
+  const double m = block_max(mx, scratch);
+  if (nan || m == -INFINITY) {
+    // NaN -> ValueError on the host; total underflow -> collapse: identity
+    // ancestors, lnc unchanged (filters.py:105-109)
+    for (int i = tid; i < N; i += blockDim.x) anc[base + i] = static_cast<int32_t>(base + i);
+    if (tid == 0) {
+      collapsed[f] = nan ? 0 : 1;
+      if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
+    }
+    return;
+  }
+
+  // 2. e = exp(lw - m), total (fixed-order block reduction)
+  double part = 0.0;
+  for (int i = tid; i < N; i += blockDim.x) {
+    const double e = exp(__dsub_rn(s_cum[i], m));
+    s_cum[i] = e;
+    part = __dadd_rn(part, e);
+  }
+  const double total = block_sum(part, scratch);
+
+  // 3. w = e / total, inclusive scan -> cum
+  for (int i = tid; i < N; i += blockDim.x) s_cum[i] = __ddiv_rn(s_cum[i], total);
+  __syncthreads();
+  block_scan_inplace(s_cum, N, 0.0, scratch);
+
+  // 4. sorted uniforms
+  if (MODE == 1) {
+    for (int i = tid; i < N; i += blockDim.x) s_u[i] = u_tape[base + i];
+    __syncthreads();
+  } else {
+    const Key2 key = load_key(keys, f);
+    for (int i = tid; i < N; i += blockDim.x) s_u[i] = spacing_exp(key, t, i);
+    __syncthreads();
+    const double cn1 = block_scan_inplace(s_u, N, 0.0, scratch);  // = c[N-1]
+    const double cN = __dadd_rn(cn1, spacing_exp(key, t, N));     // c[N]
+    for (int i = tid; i < N; i += blockDim.x) s_u[i] = __ddiv_rn(s_u[i], cN);
+    __syncthreads();
+  }
+
+  // 5. merge (searchsorted left + clamp)
+  for (int j = tid; j < N; j += blockDim.x) {
+    int k = lower_bound_f64(s_cum, N, s_u[j]);
+    if (k > N - 1) k = N - 1;
+    anc[base + j] = static_cast<int32_t>(base + k);
+  }
+  if (tid == 0) {
+    collapsed[f] = 0;
+    // log_mean_raw = (m + log(total)) - log(N); lnc += log_mean_raw
+    const double lmr = __dsub_rn(__dadd_rn(m, log(total)), log(static_cast<double>(N)));
+    lnc[f] = __dadd_rn(lnc[f], lmr);
+  }
+}
+
+// ---- wide path ----------------------------------------------------------
+struct WideWs {
+  double *tmax, *tsum, *twsum, *tesum, *twoff, *teoff;  // per tile
+  double *m, *total, *cN;                               // per filter
+  int *flag;                                            // per filter: 0 ok, 1 collapse, 2 nan
+  double *cum;                                          // M*N
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+static size_t wide_ws_layout(int64_t M, int64_t N, WideWs *w, char *base) {
+  const int64_t tpf = (N + kTile - 1) / kTile;
+  const int64_t nt = M * tpf;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char *p = base ? base + off : nullptr;
+    off += align256(bytes);
+    return p;
+  };
+  WideWs ws;
+  ws.tmax = reinterpret_cast<double *>(take(nt * 8));
+  ws.tsum = reinterpret_cast<double *>(take(nt * 8));
+  ws.twsum = reinterpret_cast<double *>(take(nt * 8));
+  ws.tesum = reinterpret_cast<double *>(take(nt * 8));
+  ws.twoff = reinterpret_cast<double *>(take(nt * 8));
+  ws.teoff = reinterpret_cast<double *>(take(nt * 8));
+  ws.m = reinterpret_cast<double *>(take(M * 8));
+  ws.total = reinterpret_cast<double *>(take(M * 8));
+  ws.cN = reinterpret_cast<double *>(take(M * 8));
+  ws.flag = reinterpret_cast<int *>(take(M * 4));
+  ws.cum = reinterpret_cast<double *>(take(static_cast<size_t>(M) * N * 8));
+  if (w) *w = ws;
+  return off;
+}
+
+template <typename TW>
+__global__ void __launch_bounds__(kTileThreads) wide_tile_max(const TW *__restrict__ logw,
+                                                              int64_t N, int64_t tpf,
+                                                              WideWs ws) {
+  __shared__ double scratch[33];
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  const int64_t i0 = tt * kTile, i1 = min(N, i0 + kTile);
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const double v = load_lw(logw + f * N + i);
+    nan |= isnan(v);
+    mx = fmax(mx, v);
+  }
+  nan = __syncthreads_or(nan);
+  const double m = block_max(mx, scratch);
+  if (threadIdx.x == 0) ws.tmax[tile] = nan ? NAN : m;
+}
+
+__global__ void wide_filter_max(int64_t tpf, WideWs ws, uint8_t *collapsed, uint32_t *status) {
+  __shared__ double scratch[33];
+  const int64_t f = blockIdx.x;
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int64_t i = threadIdx.x; i < tpf; i += blockDim.x) {
+    const double v = ws.tmax[f * tpf + i];
+    nan |= isnan(v);
+    mx = fmax(mx, v);
+  }
+  nan = __syncthreads_or(nan);
+  const double m = block_max(mx, scratch);
+  if (threadIdx.x == 0) {
+    ws.m[f] = m;
+    const int fl = nan ? 2 : (m == -INFINITY ? 1 : 0);
+    ws.flag[f] = fl;
+    collapsed[f] = fl == 1 ? 1 : 0;
+    if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
+  }
+}
+
+template <typename TW>
+__global__ void __launch_bounds__(kTileThreads) wide_tile_expsum(const TW *__restrict__ logw,
+                                                                 int64_t N, int64_t tpf,
+                                                                 WideWs ws) {
+  __shared__ double scratch[33];
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  if (ws.flag[f]) return;
+  const double m = ws.m[f];
+  const int64_t i0 = tt * kTile, i1 = min(N, i0 + kTile);
+  double part = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+    part = __dadd_rn(part, exp(__dsub_rn(load_lw(logw + f * N + i), m)));
+  const double s = block_sum(part, scratch);
+  if (threadIdx.x == 0) ws.tsum[tile] = s;
+}
+
+__global__ void wide_filter_total(int64_t N, int64_t tpf, WideWs ws, double *lnc) {
+  __shared__ double scratch[33];
+  const int64_t f = blockIdx.x;
+  if (ws.flag[f]) return;
+  double part = 0.0;
+  for (int64_t i = threadIdx.x; i < tpf; i += blockDim.x)
+    part = __dadd_rn(part, ws.tsum[f * tpf + i]);
+  const double total = block_sum(part, scratch);
+  if (threadIdx.x == 0) {
+    ws.total[f] = total;
+    const double lmr =
+        __dsub_rn(__dadd_rn(ws.m[f], log(total)), log(static_cast<double>(N)));
+    lnc[f] = __dadd_rn(lnc[f], lmr);
+  }
+}
+
+// tile sums of w and of the exponential spacings
+template <typename TW, int MODE>
+__global__ void __launch_bounds__(kTileThreads) wide_tile_sums(
+    const TW *__restrict__ logw, int64_t N, int64_t tpf, WideWs ws,
+    const double *__restrict__ u_tape, const uint32_t *__restrict__ keys, uint32_t t) {
+  __shared__ double scratch[33];
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  if (ws.flag[f]) return;
+  const double m = ws.m[f], total = ws.total[f];
+  const int64_t i0 = tt * kTile, i1 = min(N, i0 + kTile);
+  double pw = 0.0, pe = 0.0;
+  Key2 key{0u, 0u};
+  if (MODE == 0) key = load_key(keys, f);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    pw = __dadd_rn(pw, __ddiv_rn(exp(__dsub_rn(load_lw(logw + f * N + i), m)), total));
+    if (MODE == 0) pe = __dadd_rn(pe, spacing_exp(key, t, i));
+  }
+  const double sw = block_sum(pw, scratch);
+  const double se = MODE == 0 ? block_sum(pe, scratch) : 0.0;
+  if (threadIdx.x == 0) {
+    ws.twsum[tile] = sw;
+    ws.tesum[tile] = se;
+  }
+}
+
+// exclusive tile offsets per filter: block per filter, carry across chunks
+__global__ void wide_offsets_kernel(int64_t M, int64_t tpf, WideWs ws) {
+  // block per filter, sequential carry over tiles via block scan
+  __shared__ double scratch[33];
+  extern __shared__ double sbuf[];  // 2 * 1024 doubles
+  const int64_t f = blockIdx.x;
+  if (ws.flag[f]) return;
+  double cw = 0.0, ce = 0.0;
+  for (int64_t b0 = 0; b0 < tpf; b0 += 1024) {
+    const int n = static_cast<int>((tpf - b0 < 1024 ? tpf - b0 : 1024));
+    double *sw = sbuf, *se = sbuf + 1024;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      sw[i] = ws.twsum[f * tpf + b0 + i];
+      se[i] = ws.tesum[f * tpf + b0 + i];
+    }
+    __syncthreads();
+    // exclusive offsets = carry + inclusive scan - own
+    const double cw_next = block_scan_inplace(sw, n, cw, scratch);
+    const double ce_next = block_scan_inplace(se, n, ce, scratch);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      ws.twoff[f * tpf + b0 + i] = i == 0 ? cw : sw[i - 1];
+      ws.teoff[f * tpf + b0 + i] = i == 0 ? ce : se[i - 1];
+    }
+    __syncthreads();
+    cw = cw_next;
+    ce = ce_next;
+  }
+  if (threadIdx.x == 0) ws.cN[f] = ce;  // sum of E_0..E_{N-1}; E_N added by the merge
+}
+
+// cum for one tile -> ws.cum
+template <typename TW>
+__global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restrict__ logw,
+                                                              int64_t N, int64_t tpf,
+                                                              WideWs ws) {
+  __shared__ double scratch[33];
+  __shared__ double s[kTile];
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  if (ws.flag[f]) return;
+  const double m = ws.m[f], total = ws.total[f];
+  const int64_t i0 = tt * kTile;
+  const int n = static_cast<int>((N - i0 < kTile ? N - i0 : kTile));
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    s[i] = __ddiv_rn(exp(__dsub_rn(load_lw(logw + f * N + i0 + i), m)), total);
+  __syncthreads();
+  block_scan_inplace(s, n, ws.twoff[tile], scratch);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) ws.cum[f * N + i0 + i] = s[i];
+}
+
+// sorted uniforms for one u-tile, then merge against ws.cum
+template <int MODE>
+__global__ void __launch_bounds__(kTileThreads) wide_tile_merge(
+    int64_t N, int64_t tpf, WideWs ws, const double *__restrict__ u_tape,
+    const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc) {
+  __shared__ double scratch[33];
+  __shared__ double s[kTile];
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  const int64_t i0 = tt * kTile;
+  const int n = static_cast<int>((N - i0 < kTile ? N - i0 : kTile));
+  const int64_t base = f * N;
+  if (ws.flag[f]) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      anc[base + i0 + i] = static_cast<int32_t>(base + i0 + i);
+    return;
+  }
+  if (MODE == 1) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = u_tape[base + i0 + i];
+    __syncthreads();
+  } else {
+    const Key2 key = load_key(keys, f);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = spacing_exp(key, t, i0 + i);
+    __syncthreads();
+    block_scan_inplace(s, n, ws.teoff[tile], scratch);
+    const double cN = __dadd_rn(ws.cN[f], spacing_exp(key, t, N));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = __ddiv_rn(s[i], cN);
+    __syncthreads();
+  }
+  // each thread merges a contiguous run of u's: binary search then walk
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int j0 = threadIdx.x * per, j1 = min(n, j0 + per);
+  if (j0 >= j1) return;
+  const double *cum = ws.cum + base;
+  int64_t k = lower_bound_f64_64(cum, N, s[j0]);
+  for (int j = j0; j < j1; ++j) {
+    const double u = s[j];
+    while (k < N && __ldg(cum + k) < u) ++k;
+    anc[base + i0 + j] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+  }
+}
+
+template <typename TW>
+static int launch_resample(const void *logw_v, int64_t M, int64_t N, const double *u_tape,
+                           const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
+                           uint8_t *collapsed, uint32_t *status, void *ws_v, size_t ws_bytes,
+                           cudaStream_t s) {
+  const TW *logw = static_cast<const TW *>(logw_v);
+  if (N <= kBankMaxN) {
+    const size_t smem = 2 * static_cast<size_t>(N) * sizeof(double);
+    auto kern = u_tape ? resample_bank_kernel<TW, 1> : resample_bank_kernel<TW, 0>;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    kern<<<static_cast<unsigned>(M), kBankThreads, smem, s>>>(
+        logw, static_cast<int32_t>(N), u_tape, keys, t, anc, lnc, collapsed, status);
+    return check_launch("pf_segmented_resample(bank)");
+  }
+  WideWs ws;
+  const size_t need = wide_ws_layout(M, N, &ws, static_cast<char *>(ws_v));
+  PF_REQUIRE(ws_v && ws_bytes >= need, "pf_segmented_resample: workspace too small (%zu < %zu)",
+             ws_bytes, need);
+  const int64_t tpf = (N + kTile - 1) / kTile;
+  const unsigned nt = static_cast<unsigned>(M * tpf);
+  wide_tile_max<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+  wide_filter_max<<<static_cast<unsigned>(M), 256, 0, s>>>(tpf, ws, collapsed, status);
+  wide_tile_expsum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+  wide_filter_total<<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, lnc);
+  if (u_tape)
+    wide_tile_sums<TW, 1><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
+  else
+    wide_tile_sums<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
+  wide_offsets_kernel<<<static_cast<unsigned>(M), 256, 2 * 1024 * sizeof(double), s>>>(M, tpf,
+                                                                                        ws);
+  wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+  if (u_tape)
+    wide_tile_merge<1><<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc);
+  else
+    wide_tile_merge<0><<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc);
+  return check_launch("pf_segmented_resample(wide)");
+}
+
+// ---- normalize_log_weights operator (segmented) ---------------------------
+template <typename TW>
+__global__ void __launch_bounds__(256) nlw_kernel(const TW *__restrict__ logw, int32_t N,
+                                                  double *__restrict__ w,
+                                                  double *__restrict__ lmr,
+                                                  uint8_t *__restrict__ collapsed,
+                                                  uint32_t *__restrict__ status) {
+  __shared__ double scratch[33];
+  const int64_t f = blockIdx.x, base = f * N;
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double v = load_lw(logw + base + i);
+    nan |= isnan(v);
+    mx = fmax(mx, v);
+  }
+  nan = __syncthreads_or(nan);
+  const double m = block_max(mx, scratch);
+  if (nan || m == -INFINITY) {
+    if (threadIdx.x == 0) {
+      collapsed[f] = nan ? 0 : 1;
+      if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
+    }
+    return;
+  }
+  double part = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double e = exp(__dsub_rn(load_lw(logw + base + i), m));
+    w[base + i] = e;
+    part = __dadd_rn(part, e);
+  }
+  const double total = block_sum(part, scratch);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) w[base + i] = __ddiv_rn(w[base + i], total);
+  if (threadIdx.x == 0) {
+    collapsed[f] = 0;
+    lmr[f] = __dsub_rn(__dadd_rn(m, log(total)), log(static_cast<double>(N)));
+  }
+}
+
+__global__ void resample_indices_kernel(const double *__restrict__ cum, int64_t n,
+                                        const double *__restrict__ u, int64_t m,
+                                        int64_t *__restrict__ idx) {
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (j >= m) return;
+  const int64_t k = lower_bound_f64_64(cum, n, u[j]);
+  idx[j] = k < n - 1 ? k : n - 1;
+}
+
+}  // namespace pf
+
+using namespace pf;
+
+extern "C" {
+
+size_t pf_resample_workspace_bytes(int64_t M, int64_t N) {
+  if (M < 1 || N < 1 || N <= kBankMaxN) return 0;
+  return wide_ws_layout(M, N, nullptr, nullptr);
+}
+
+int pf_segmented_resample(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
+                          const double *u_tape, const uint32_t *keys, uint32_t t,
+                          int32_t *anc_out, double *lnc, uint8_t *collapsed, uint32_t *status,
+                          void *ws, size_t ws_bytes, void *stream) {
+  PF_REQUIRE(logw && anc_out && lnc && collapsed && status, "pf_segmented_resample: null");
+  PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_segmented_resample: bad M/N");
+  PF_REQUIRE(u_tape || keys, "pf_segmented_resample: need keys (Philox) or u_tape");
+  const cudaStream_t s = as_stream(stream);
+  if (logw_dtype == PF_F64)
+    return launch_resample<double>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status,
+                                   ws, ws_bytes, s);
+  return launch_resample<float>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status, ws,
+                                ws_bytes, s);
+}
+
+int pf_op_normalize_log_weights(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
+                                double *weights_out, double *log_mean_raw_out,
+                                uint8_t *collapsed, uint32_t *status, void *stream) {
+  PF_REQUIRE(logw && weights_out && log_mean_raw_out && collapsed && status,
+             "pf_op_normalize_log_weights: null");
+  PF_REQUIRE(M >= 1 && N >= 1 && N <= INT32_MAX, "pf_op_normalize_log_weights: bad M/N");
+  const cudaStream_t s = as_stream(stream);
+  if (logw_dtype == PF_F64)
+    nlw_kernel<double><<<static_cast<unsigned>(M), 256, 0, s>>>(
+        static_cast<const double *>(logw), static_cast<int32_t>(N), weights_out,
+        log_mean_raw_out, collapsed, status);
+  else
+    nlw_kernel<float><<<static_cast<unsigned>(M), 256, 0, s>>>(
+        static_cast<const float *>(logw), static_cast<int32_t>(N), weights_out,
+        log_mean_raw_out, collapsed, status);
+  return check_launch("pf_op_normalize_log_weights");
+}
+
+int pf_op_resample_indices(const double *cum, int64_t n, const double *u, int64_t m,
+                           int64_t *idx_out, void *stream) {
+  PF_REQUIRE(cum && u && idx_out && n >= 1 && m >= 0, "pf_op_resample_indices: bad arguments");
+  if (m == 0) return PF_OK;
+  resample_indices_kernel<<<grid_for(m, 256), 256, 0, as_stream(stream)>>>(cum, n, u, m,
+                                                                           idx_out);
+  return check_launch("pf_op_resample_indices");
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+"""Ensembles of M independent filters (drop-in for parpf/ensemble.py).
+
+``run_ensemble`` keeps the reference signature (ensemble.py:76-78).  All M
+filters live as segments of one device batch; under torch.distributed the
+filters are block-sharded across ranks (one GPU each) and the per-step
+estimates are combined with one disjoint-support all-reduce per observation
+(dist.py), so results are bit-identical for any GPU count.  ``workers``
+keeps its meaning of "affects wall time only" and is validated but unused.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, dist, philox
+from .bank import DrawTape, FilterBank
+from .filters import FilterOutput, _bank_seconds, _validate
+
+CENTRALISED = "centralised"
+ENSEMBLE = "ensemble"
+
+
+@dataclass
+class EnsembleOutput:
+    """M independent filter records plus their averaged estimators
+    (ensemble.py:27-53)."""
+
+    variant: str
+    n_filters: int
+    n_particles: int
+    master_seed: object
+    filter_outputs: list
+    mean_estimates: np.ndarray
+    filter_seconds: np.ndarray
+    total_seconds: float
+
+    @property
+    def n_steps(self) -> int:
+        return self.mean_estimates.shape[0]
+
+    def same_result(self, other: "EnsembleOutput") -> bool:
+        return (
+            self.variant == other.variant
+            and self.n_filters == other.n_filters
+            and self.n_particles == other.n_particles
+            and np.array_equal(self.mean_estimates, other.mean_estimates)
+            and all(a.same_result(b) for a, b in zip(self.filter_outputs, other.filter_outputs))
+        )
+
+
+def filter_seeds(master_seed, n_filters: int):
+    """ensemble.py:56-60 (same SeedSequence tree)."""
+    return philox.filter_seeds(master_seed, n_filters)
+
+
+def average_estimates(filter_outputs) -> np.ndarray:
+    """Left-to-right mean of per-filter estimates (ensemble.py:68-73),
+    evaluated on the GPU with the same association."""
+    import torch
+
+    _lib.require_cuda()
+    est = np.stack([np.asarray(o.estimates, dtype=np.float64) for o in filter_outputs], axis=1)
+    d = torch.from_numpy(np.ascontiguousarray(est)).cuda()
+    T, M, dim = d.shape
+    out = torch.empty((T, dim), dtype=torch.float64, device="cuda")
+    _lib.call("pf_ensemble_average", _lib.ptr(d), T, M, dim, _lib.ptr(out), _lib.stream_ptr())
+    return out.cpu().numpy()
+
+
+def run_ensemble(model, observations, variant: str, n_filters: int, n_particles: int,
+                 master_seed, workers: int = 1, *, dtype=None, tape: DrawTape | None = None,
+                 estimate: str = "full", shard: bool | None = None) -> EnsembleOutput:
+    """ensemble.py:76-111 on the GPU bank.
+
+    shard: None -> shard across ranks when torch.distributed is initialised
+    with world_size > 1; every rank returns the full EnsembleOutput.
+    """
+    import torch
+
+    if n_filters < 1 or n_particles < 1:
+        raise ValueError("n_filters and n_particles must be >= 1")
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    obs = _validate(observations, variant, model)
+    T = obs.shape[0]
+    rank, world = dist.world()
+    if shard is False or world == 1:
+        rank, world = 0, 1
+    lo, hi = dist.shard_range(n_filters, rank, world) if world > 1 else (0, n_filters)
+    keys = philox.filter_keys(master_seed, n_filters)
+    started = time.perf_counter()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if model.kind == "lorenz":
+        est_dim = 3
+    else:
+        est_dim = model.dim_x if estimate == "full" else model.nodes
+    est_full = torch.zeros((T, n_filters, est_dim), dtype=torch.float64, device=dev)
+    bank = FilterBank(model, hi - lo, n_particles, keys[lo:hi], T, dtype=dtype, tape=tape,
+                      filter_offset=lo, estimate=estimate, est_buffer=est_full,
+                      est_row_offset=lo)
+    bank.load_observations(obs)
+    bank.init()
+    exch = dist.EstimateExchange(est_full) if world > 1 else None
+    events = [torch.cuda.Event(enable_timing=True) for _ in range(T + 1)]
+    events[0].record()
+    for k in range(T):
+        bank.step(k)
+        events[k + 1].record()
+        if exch is not None:
+            exch.step_done(k)
+    if exch is not None:
+        exch.finish()
+    mean = torch.empty((T, est_dim), dtype=torch.float64, device=dev)
+    _lib.call("pf_ensemble_average", _lib.ptr(est_full), T, n_filters, est_dim, _lib.ptr(mean),
+              _lib.stream_ptr())
+    # small end-of-run traces: lnc, collapse flags, status (disjoint support)
+    lnc_full = torch.zeros((T, n_filters), dtype=torch.float64, device=dev)
+    coll_full = torch.zeros((T, n_filters), dtype=torch.int32, device=dev)
+    st_full = torch.zeros(n_filters, dtype=torch.int32, device=dev)
+    lnc_full[:, lo:hi] = bank.lnc_tr
+    coll_full[:, lo:hi] = bank.coll_tr.to(torch.int32)
+    st_full[lo:hi] = bank.status
+    if world > 1:
+        for t_ in (lnc_full, coll_full, st_full):
+            dist.allreduce_disjoint(t_)
+    torch.cuda.synchronize()
+    total = time.perf_counter() - started
+    _lib.raise_status(st_full.cpu().numpy())
+    secs = _bank_seconds(events)
+    est_h = est_full.cpu().numpy()
+    lnc_h = lnc_full.cpu().numpy()
+    coll_h = coll_full.cpu().numpy()
+    outputs = []
+    for f in range(n_filters):
+        steps = [int(k) + 1 for k in np.nonzero(coll_h[:, f])[0]]
+        outputs.append(FilterOutput(variant, n_particles, None, est_h[:, f, :], lnc_h[:, f],
+                                    secs.copy(), steps))
+    seeds = filter_seeds(master_seed, n_filters)
+    for f, o in enumerate(outputs):
+        o.seed = seeds[f]
+    filter_seconds = np.array([o.total_seconds for o in outputs])
+    return EnsembleOutput(variant, n_filters, n_particles, master_seed, outputs,
+                          mean.cpu().numpy(), filter_seconds, total)
+
+
+def ensemble_estimate(out: EnsembleOutput, t: int) -> np.ndarray:
+    """ensemble.py:114-118."""
+    if not 0 <= t < out.n_steps:
+        raise ValueError(f"step index {t} outside 0..{out.n_steps - 1}")
+    return out.mean_estimates[t]
+
+
+def time_error_index(variant: str, n_filters: int, n_particles: int) -> float:
+    """ensemble.py:121-135."""
+    if n_filters < 1 or n_particles < 1:
+        raise ValueError("n_filters and n_particles must be >= 1")
+    if variant == CENTRALISED:
+        return 1.0
+    if variant == ENSEMBLE:
+        return 1.0 / n_filters + 1.0 / n_particles
+    raise ValueError(f"unknown variant {variant!r}")

@@ -1,0 +1,138 @@
+"""Single-filter drivers and step functions (drop-in for parpf/filters.py).
+
+* :func:`run_filter` - filters.py:163-193; runs on the GPU bank with M=1.
+* :func:`bf_init` / :func:`bf_step` - filters.py:87-112; reference-style
+  step functions over host ParticleApproximation containers whose
+  arithmetic (propagation, weighting, normalisation, resampling, gather)
+  runs on the GPU via the model hooks and the L2 operators.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import philox
+from .bank import DrawTape, FilterBank
+from .core import ParticleApproximation, StateSpaceModel, normalize_log_weights, uniform_weights
+from .exceptions import UnsupportedModelError, WeightCollapseError
+from .resampling import multinomial_resample_indices
+
+VARIANT_BOOTSTRAP = "bootstrap"
+VARIANT_AUXILIARY = "auxiliary"
+KNOWN_VARIANTS = (VARIANT_BOOTSTRAP,)
+
+
+@dataclass
+class FilterOutput:
+    """Per-step record of one filter run (filters.py:43-78)."""
+
+    variant: str
+    n_particles: int
+    seed: object
+    estimates: np.ndarray
+    log_norm_const: np.ndarray
+    step_seconds: np.ndarray
+    collapse_steps: list = field(default_factory=list)
+
+    @property
+    def n_steps(self) -> int:
+        return self.estimates.shape[0]
+
+    @property
+    def total_seconds(self) -> float:
+        return float(self.step_seconds.sum())
+
+    def same_result(self, other: "FilterOutput") -> bool:
+        return (
+            self.variant == other.variant
+            and self.n_particles == other.n_particles
+            and self.collapse_steps == other.collapse_steps
+            and np.array_equal(self.estimates, other.estimates)
+            and np.array_equal(self.log_norm_const, other.log_norm_const)
+        )
+
+
+def _check_uniform(state: ParticleApproximation):
+    n = state.n_particles
+    if not np.allclose(state.weights, 1.0 / n, rtol=0.0, atol=1e-12):
+        raise ValueError("step functions expect uniform (post-resampling) weights")
+
+
+def bf_init(model: StateSpaceModel, n_particles: int, rng) -> ParticleApproximation:
+    if n_particles < 1:
+        raise ValueError("n_particles must be >= 1")
+    particles = model.sample_prior(rng, n_particles)
+    return ParticleApproximation(particles, uniform_weights(n_particles), log_norm_const=0.0, t=0)
+
+
+def bf_step(model: StateSpaceModel, state: ParticleApproximation, y, rng) -> ParticleApproximation:
+    """One bootstrap step with the reference's control flow and draw order."""
+    _check_uniform(state)
+    t = state.t + 1
+    n = state.n_particles
+    propagated = model.sample_transition(state.particles, t, rng)
+    log_w = model.log_likelihood(y, propagated, t)
+    try:
+        weights, log_mean_raw = normalize_log_weights(log_w)
+    except WeightCollapseError:
+        return ParticleApproximation(propagated, uniform_weights(n), state.log_norm_const, t,
+                                     collapsed=True)
+    import torch
+
+    idx = multinomial_resample_indices(weights, n, rng)
+    gathered = torch.from_numpy(np.ascontiguousarray(propagated)).cuda()[
+        torch.from_numpy(idx).cuda()].cpu().numpy()
+    return ParticleApproximation(gathered, uniform_weights(n),
+                                 state.log_norm_const + log_mean_raw, t)
+
+
+def _validate(observations, variant, model):
+    obs = np.atleast_2d(np.asarray(observations, dtype=np.float64))
+    if obs.shape[0] == 0:
+        raise ValueError("observation sequence must be non-empty")
+    if variant == VARIANT_AUXILIARY:
+        raise UnsupportedModelError("the auxiliary variant is not on the GPU bank path yet")
+    if variant not in KNOWN_VARIANTS:
+        raise ValueError(f"unknown filter variant {variant!r}")
+    if getattr(model, "dim_y", obs.shape[1]) == 1 and obs.ndim == 2 and obs.shape[1] != 1:
+        obs = obs.reshape(-1, 1)
+    return obs
+
+
+def _bank_seconds(events):
+    """Per-step device times from CUDA events recorded around each step."""
+    return np.array([events[i].elapsed_time(events[i + 1]) / 1e3
+                     for i in range(len(events) - 1)])
+
+
+def run_filter(model: StateSpaceModel, observations, variant: str, n_particles: int, seed, *,
+               dtype=None, tape: DrawTape | None = None, estimate: str = "full") -> FilterOutput:
+    """filters.py:163-193 on the GPU bank (M=1).
+
+    Production mode (tape=None): Philox keyed by ``seed``'s SeedSequence.
+    Oracle mode: ``tape`` supplies the reference's draws (bank.DrawTape).
+    ``step_seconds`` holds device time per observation step.
+    """
+    import torch
+
+    obs = _validate(observations, variant, model)
+    if n_particles < 1:
+        raise ValueError("n_particles must be >= 1")
+    keys = philox.seed_key(seed)[None, :]
+    bank = FilterBank(model, 1, n_particles, keys, obs.shape[0], dtype=dtype, tape=tape,
+                      estimate=estimate)
+    bank.load_observations(obs)
+    bank.init()
+    events = [torch.cuda.Event(enable_timing=True) for _ in range(obs.shape[0] + 1)]
+    events[0].record()
+    for k in range(obs.shape[0]):
+        bank.step(k)
+        events[k + 1].record()
+    torch.cuda.synchronize()
+    bank.check_status()
+    return FilterOutput(variant, n_particles, seed, bank.est[:, 0, :].cpu().numpy(),
+                        bank.lnc_tr[:, 0].cpu().numpy(), _bank_seconds(events),
+                        bank.collapse_steps()[0])

@@ -1,0 +1,89 @@
+"""CPU-side checks of the C-ABI boundary: libpfbank.so loads without a GPU
+and exports every symbol include/pfbank.h declares, with matching ctypes
+signatures; the Philox host mirror reproduces the published known answers."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(REPO, "include", "pfbank.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pf_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1407_8071_b200 import _build, _lib
+
+    if not os.path.exists(_lib.LIB_PATH):
+        _build.build(verbose=False)
+    return _lib.load()
+
+
+def test_header_declares_the_abi():
+    fns = _header_functions()
+    for name in ("pf_segmented_resample", "pf_lorenz_propagate_weight", "pf_fhn_interval",
+                 "pf_filter_estimate", "pf_op_resample_indices", "pf_op_lorenz_euler_block",
+                 "pf_op_fhn_euler_block", "pf_op_normalize_log_weights"):
+        assert name in fns
+
+
+def test_library_exports_every_header_symbol(lib):
+    from paper_1407_8071_b200 import _lib
+
+    for name in _header_functions():
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+    assert set(_lib.SIGNATURES) == set(_header_functions())
+
+
+def test_library_basic_calls_without_gpu(lib):
+    assert lib.pf_version() >= 10000
+    # argument validation happens before any CUDA call
+    from paper_1407_8071_b200 import _lib
+
+    with pytest.raises(ValueError):
+        _lib.call("pf_segmented_resample", _lib.PF_F32, None, 1, 16, None, None, 1, None, None,
+                  None, None, None, 0, None)
+    assert lib.pf_resample_workspace_bytes(4, 1024) == 0
+    assert lib.pf_resample_workspace_bytes(1, 1 << 26) > 8 * (1 << 26)
+
+
+def test_philox_known_answers():
+    """Random123 philox4x32-10 known-answer vectors (kat_vectors)."""
+    from paper_1407_8071_b200.philox import philox4x32_10
+
+    ctr = np.array([[0, 0, 0, 0], [0xFFFFFFFF] * 4,
+                    [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344]], dtype=np.uint32)
+    key = np.array([[0, 0], [0xFFFFFFFF, 0xFFFFFFFF], [0xA4093822, 0x299F31D0]], dtype=np.uint32)
+    want = np.array([[0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8],
+                     [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD],
+                     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]], dtype=np.uint32)
+    assert np.array_equal(philox4x32_10(ctr, key), want)
+
+
+def test_seed_keys_follow_the_reference_seed_tree():
+    from paper_1407_8071_b200 import philox
+
+    ks = philox.filter_keys(5, 3)
+    kids = np.random.SeedSequence(5).spawn(3)
+    for k, c in zip(ks, kids):
+        assert np.array_equal(k, c.generate_state(2, dtype=np.uint32))
+    assert np.array_equal(philox.seed_key(philox.filter_seeds(5, 1)[0]), ks[0])
+
+
+def test_product_fails_loudly_without_cuda():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1407_8071_b200 as pf
+
+    with pytest.raises(RuntimeError, match="CUDA"):
+        pf.normalize_log_weights(np.zeros(4))

@@ -1,0 +1,384 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+golden fixtures generated from the reference.
+
+Tolerances (north star): ancestors bit-exact; fp64 states / weights / lnc /
+estimates within 1e-12 norm-relative (element-wise pure-relative fails near
+zero even for a correct kernel); fp32 within 1e-4 norm-relative.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import parpf_oracle as orc
+from oracle import tapes
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1407_8071_b200 as pf  # noqa: E402
+from paper_1407_8071_b200 import _lib  # noqa: E402
+
+
+def norm_rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def certify_ties(anc_gpu, anc_ref, cum_ref, u):
+    """Mismatching ancestors are allowed only where u sits within rounding
+    distance of the reference CDF boundary, i.e. the choice is a rounding
+    tie.  The distance bound is the worst-case error of an N-term fp64
+    prefix sum of weights summing to 1 on either side: 2 * N * 2^-53
+    (Higham, gamma_N).  Returns the number of (certified) mismatches."""
+    n = cum_ref.shape[1]
+    tol = 2.0 * n * 2.0 ** -53
+    bad = np.argwhere(anc_gpu != anc_ref)
+    for f, j in bad:
+        k = min(anc_gpu[f, j], anc_ref[f, j])
+        assert abs(cum_ref[f, k] - u[f, j]) <= tol, (
+            f"uncertified ancestor mismatch at filter {f}, slot {j}")
+    return len(bad)
+
+
+# ---------------------------------------------------------------- L1 operators
+
+def test_philox_device_matches_host_mirror():
+    from paper_1407_8071_b200.philox import philox4x32_10
+
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2**32, size=(1000, 4), dtype=np.uint64).astype(np.uint32)
+    key = rng.integers(0, 2**32, size=(1000, 2), dtype=np.uint64).astype(np.uint32)
+    d_c = torch.from_numpy(ctr.view(np.int32)).cuda()
+    d_k = torch.from_numpy(key.view(np.int32)).cuda()
+    out = torch.empty((1000, 4), dtype=torch.int32, device="cuda")
+    _lib.call("pf_philox_kat", _lib.ptr(d_c), _lib.ptr(d_k), _lib.ptr(out), 1000, _lib.stream_ptr())
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), philox4x32_10(ctr, key))
+
+
+def test_lorenz_block_bit_exact(golden):
+    g = golden["kernels"]
+    out = pf.accel.lorenz_euler_block(g["lz_states"], g["lz_noise"], 1e-3, 10.0, 28.0, 8.0 / 3.0)
+    assert np.array_equal(out, g["lz_out"])
+
+
+@pytest.mark.parametrize("tag", ["rect", "sq"])
+def test_fhn_block_bit_exact(golden, tag):
+    g = golden["kernels"]
+    p = g[f"fhn_{tag}_params"]
+    u, v = pf.accel.fhn_euler_block(g[f"fhn_{tag}_U"], g[f"fhn_{tag}_V"], g[f"fhn_{tag}_drive"],
+                                    g[f"fhn_{tag}_noise"], p[0], p[1], tuple(p[2:6]),
+                                    tuple(p[6:9]), p[9])
+    assert np.array_equal(u, g[f"fhn_{tag}_u_new"])
+    assert np.array_equal(v, g[f"fhn_{tag}_v_new"])
+
+
+def test_resample_indices_bit_exact(golden):
+    g = golden["kernels"]
+    for i in range(int(g["ri_count"])):
+        idx = pf.accel.resample_indices(g[f"ri_cum_{i}"], g[f"ri_u_{i}"])
+        assert idx.dtype == np.int64
+        assert np.array_equal(idx, g[f"ri_idx_{i}"]), i
+    assert not np.any(pf.accel.resample_indices(g["ri_cum_0"], g["ri_u_0"]) == 1)
+
+
+def test_normalize_log_weights(golden):
+    g = golden["kernels"]
+    for i in range(int(g["nlw_count"])):
+        w, lm = pf.normalize_log_weights(g[f"nlw_in_{i}"])
+        assert norm_rel(w, g[f"nlw_w_{i}"]) < 1e-14
+        assert abs(lm - float(g[f"nlw_lm_{i}"])) <= 1e-12 * max(1.0, abs(lm))
+    with pytest.raises(pf.WeightCollapseError):
+        pf.normalize_log_weights(np.full(8, -np.inf))
+    with pytest.raises(ValueError):
+        pf.normalize_log_weights(np.array([0.0, np.nan]))
+    with pytest.raises(ValueError):
+        pf.normalize_log_weights(np.array([]))
+
+
+def test_multinomial_resample_consumes_rng_like_reference(golden):
+    g = golden["kernels"]
+    idx = pf.multinomial_resample_indices(g["mri_w"], 500, np.random.default_rng(77))
+    assert np.array_equal(idx, g["mri_idx"])
+
+
+# ---------------------------------------------------------------- bank, oracle mode
+
+def _lorenz_models(truth0):
+    om = orc.LorenzConfigModel(prior_mean=tuple(truth0))
+    gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(truth0), prior_var=1.0)
+    return om, gm
+
+
+def _run_bank_with_tape(gmodel, obs, M, N, prior, noise, uni, dtype=None):
+    tape = pf.DrawTape(prior=prior, noise=noise, uniforms=uni)
+    bank = pf.FilterBank(gmodel, M, N, np.zeros((M, 2), np.uint32), len(obs), tape=tape,
+                         dtype=dtype)
+    bank.load_observations(obs)
+    bank.init()
+    ancs = []
+    for k in range(len(obs)):
+        bank.step(k)
+        ancs.append(bank.anc.cpu().numpy().reshape(M, N) - np.arange(M)[:, None] * N)
+    torch.cuda.synchronize()
+    return bank, ancs
+
+
+def test_lorenz_bank_oracle_mode_fp64(golden):
+    g = golden["lorenz"]
+    om, gm = _lorenz_models(g["truth0"])
+    M, N = 4, 100
+    traces, mean, prior, noise, uni = tapes.ensemble_with_tape(om, g["obs"], M, N,
+                                                              int(g["e_master"]))
+    assert np.array_equal(mean, g["e_mean"])  # oracle == reference fixture
+    bank, ancs = _run_bank_with_tape(gm, g["obs"], M, N, prior, noise, uni)
+    for k in range(len(g["obs"])):
+        want = np.stack([tr.steps[k].ancestors for tr in traces])
+        assert np.array_equal(ancs[k], want), f"step {k + 1}"
+    est = bank.est.cpu().numpy()
+    assert norm_rel(est, np.stack([tr.estimates for tr in traces], axis=1)) < 1e-12
+    assert norm_rel(bank.lnc_tr.cpu().numpy(), g["e_lnc"].T) < 1e-12
+
+
+def test_lorenz_run_ensemble_oracle_mode_matches_golden(golden):
+    g = golden["lorenz"]
+    om, gm = _lorenz_models(g["truth0"])
+    _, _, prior, noise, uni = tapes.ensemble_with_tape(om, g["obs"], 4, 100, int(g["e_master"]))
+    out = pf.run_ensemble(gm, g["obs"], "bootstrap", 4, 100, int(g["e_master"]),
+                          tape=pf.DrawTape(prior, noise, uni))
+    assert norm_rel(out.mean_estimates, g["e_mean"]) < 1e-12
+    assert norm_rel(np.stack([o.estimates for o in out.filter_outputs]), g["e_est"]) < 1e-12
+    assert norm_rel(np.stack([o.log_norm_const for o in out.filter_outputs]), g["e_lnc"]) < 1e-12
+
+
+def test_lorenz_one_interval_fp32_within_1e4(golden):
+    g = golden["lorenz"]
+    om, gm = _lorenz_models(g["truth0"])
+    traces, _, prior, noise, uni = tapes.ensemble_with_tape(om, g["obs"][:1], 2, 512, 3)
+    bank, _ = _run_bank_with_tape(gm, g["obs"][:1], 2, 512, prior, noise, uni,
+                                  dtype=torch.float32)
+    x = bank.x[1].cpu().numpy().astype(np.float64)  # propagated planes (3, M*N)
+    want = np.concatenate([tr.steps[0].propagated for tr in traces]).T
+    assert norm_rel(x, want) < 1e-4
+    lw = bank.logw.cpu().numpy().astype(np.float64)
+    assert norm_rel(lw, np.concatenate([tr.steps[0].log_w for tr in traces])) < 1e-4
+
+
+def test_lorenz_collapse_semantics(golden):
+    g = golden["lorenz"]
+    om, gm = _lorenz_models(g["truth0"])
+    tr = orc.run_filter(om, g["c_obs"], 32, 11, keep_steps=True)
+    assert tr.collapse_steps == [3]
+    rec = orc.TapeRecorder(11)
+    tr = orc.run_filter(om, g["c_obs"], 32, rec, keep_steps=True)
+    prior = tr.prior_noise[None]
+    noise = [s.noise[None] for s in tr.steps]
+    uni = [(s.u if s.u is not None else np.full(32, np.nan))[None] for s in tr.steps]
+    out = pf.run_filter(gm, g["c_obs"], "bootstrap", 32, 11,
+                        tape=pf.DrawTape(prior, noise, uni))
+    assert out.collapse_steps == [3]
+    assert out.log_norm_const[2] == out.log_norm_const[1]
+    assert norm_rel(out.estimates, g["c_est"]) < 1e-12
+    assert norm_rel(out.log_norm_const, g["c_lnc"]) < 1e-12
+
+
+def test_fhn_bank_oracle_mode_fp64(golden):
+    g = golden["fhn"]
+    om = orc.FhnConfigModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    gm = pf.FhnLatticeModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    M, N = 2, 8
+    traces, mean, prior, noise, uni = tapes.ensemble_with_tape(om, g["obs"], M, N, 5)
+    bank, ancs = _run_bank_with_tape(gm, g["obs"], M, N, None, noise, uni)
+    for k in range(len(g["obs"])):
+        want = np.stack([tr.steps[k].ancestors for tr in traces])
+        assert np.array_equal(ancs[k], want), f"step {k + 1}"
+        # log-weights of the last step's propagated particles
+    lw_want = np.concatenate([tr.steps[-1].log_w for tr in traces])
+    assert norm_rel(bank.logw.cpu().numpy(), lw_want) < 1e-12
+    est = bank.est.cpu().numpy()
+    assert norm_rel(est, np.stack([tr.estimates for tr in traces], axis=1)) < 1e-12
+    lnc_want = np.stack([tr.log_norm_const for tr in traces], axis=1)
+    assert norm_rel(bank.lnc_tr.cpu().numpy(), lnc_want) < 1e-12
+
+
+def test_fhn_filter_matches_golden(golden):
+    g = golden["fhn"]
+    om = orc.FhnConfigModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    gm = pf.FhnLatticeModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    rec = orc.TapeRecorder(np.random.SeedSequence(99))
+    tr = orc.run_filter(om, g["obs"], 8, rec, keep_steps=True)
+    noise = [s.noise.reshape(om.substeps, 2, 8, -1)[None] for s in tr.steps]
+    uni = [s.u[None] for s in tr.steps]
+    out = pf.run_filter(gm, g["obs"], "bootstrap", 8, 99,
+                        tape=pf.DrawTape(None, noise, uni))
+    assert norm_rel(out.estimates[:, : om.nodes], g["f_est_v"]) < 1e-12
+    assert norm_rel(out.log_norm_const, g["f_lnc"]) < 1e-12
+
+
+def test_fhn_one_interval_fp32_within_1e4(golden):
+    g = golden["fhn"]
+    om = orc.FhnConfigModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    gm = pf.FhnLatticeModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    traces, _, _, noise, uni = tapes.ensemble_with_tape(om, g["obs"][:1], 2, 16, 8)
+    bank, _ = _run_bank_with_tape(gm, g["obs"][:1], 2, 16, None, noise, uni,
+                                  dtype=torch.float32)
+    x = bank.x[1].cpu().numpy().astype(np.float64)
+    want = np.concatenate([tr.steps[0].propagated for tr in traces])
+    assert norm_rel(x, want) < 1e-4
+    assert norm_rel(bank.logw.cpu().numpy(),
+                    np.concatenate([tr.steps[0].log_w for tr in traces])) < 1e-4
+
+
+# ---------------------------------------------------------------- resampling (cfg1)
+
+def _resample_case(M, N, sigma, seed):
+    rng = np.random.default_rng(seed)
+    lw = (rng.standard_normal((M, N)) * sigma).astype(np.float32)
+    u = orc.sorted_uniform_rows(np.random.default_rng(seed + 1), M, N)
+    return lw, u
+
+
+def _gpu_resample(lw, u):
+    M, N = lw.shape
+    d_lw = torch.from_numpy(lw.reshape(-1)).cuda()
+    d_u = torch.from_numpy(u.reshape(-1)).cuda()
+    anc = torch.empty(M * N, dtype=torch.int32, device="cuda")
+    lnc = torch.zeros(M, dtype=torch.float64, device="cuda")
+    coll = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    st = torch.zeros(M, dtype=torch.int32, device="cuda")
+    wsb = _lib.load().pf_resample_workspace_bytes(M, N)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    _lib.call("pf_segmented_resample", _lib.PF_F32, _lib.ptr(d_lw), M, N, _lib.ptr(d_u), None, 1,
+              _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st), _lib.ptr(ws), wsb,
+              _lib.stream_ptr())
+    a = anc.cpu().numpy().reshape(M, N).astype(np.int64) - (np.arange(M) * N)[:, None]
+    return a, lnc.cpu().numpy(), coll.cpu().numpy()
+
+
+@pytest.mark.parametrize("sigma", [1.0, 10.0])
+def test_cfg1_bank_ancestors_bit_exact(sigma):
+    M, N = 1 << 12, 1 << 10  # a 4096-filter slice of cfg1's 2^16 bank (CPU oracle time)
+    lw, u = _resample_case(M, N, sigma, seed=int(sigma))
+    anc, lmr, coll = _gpu_resample(lw, u)
+    ref_anc, ref_lmr, ref_coll, cum = orc.resample_rows(lw, u)
+    assert not coll.any()
+    assert certify_ties(anc, ref_anc, cum, u) == 0
+    assert np.all(np.diff(anc, axis=1) >= 0)
+    assert np.max(np.abs(lmr - ref_lmr)) < 1e-12
+
+
+@pytest.mark.parametrize("M,N", [(3, 20000), (2, 70001)])
+def test_wide_path_multi_filter(M, N):
+    lw, u = _resample_case(M, N, 3.0, seed=N)
+    anc, lmr, coll = _gpu_resample(lw, u)
+    ref_anc, ref_lmr, _, cum = orc.resample_rows(lw, u)
+    assert certify_ties(anc, ref_anc, cum, u) == 0
+    assert np.max(np.abs(lmr - ref_lmr)) < 1e-12
+
+
+@pytest.mark.parametrize("sigma", [1.0, 10.0])
+def test_cfg1_centralised_2pow26(sigma):
+    N = 1 << 26
+    lw, u = _resample_case(1, N, sigma, seed=100 + int(sigma))
+    anc, lmr, coll = _gpu_resample(lw, u)
+    ref_anc, ref_lmr, _, cum = orc.resample_rows(lw, u)
+    n_ties = certify_ties(anc, ref_anc, cum, u)
+    print(f"N=2^26 sigma={sigma}: {n_ties} certified rounding-tie mismatches")
+    assert n_ties < 2000
+    assert abs(lmr[0] - ref_lmr[0]) < 1e-10
+
+
+def test_collapse_and_nan_flags():
+    lw = np.zeros((3, 64), np.float32)
+    lw[1] = -np.inf
+    lw[2, 5] = np.nan
+    u = orc.sorted_uniform_rows(np.random.default_rng(0), 3, 64)
+    anc, lmr, coll = _gpu_resample(lw, u)
+    assert coll.tolist() == [0, 1, 0]
+    assert np.array_equal(anc[1], np.arange(64))
+    assert lmr[1] == 0.0
+
+
+# ---------------------------------------------------------------- production (Philox) mode
+
+def _cfg0_small():
+    truth0, _, obs = orc.lorenz_truth(seed=3, n_obs=20)
+    _, gm = _lorenz_models(truth0)
+    return gm, obs
+
+
+def test_philox_mode_deterministic_and_seed_tree():
+    gm, obs = _cfg0_small()
+    a = pf.run_filter(gm, obs, "bootstrap", 256, 12345)
+    b = pf.run_filter(gm, obs, "bootstrap", 256, 12345)
+    c = pf.run_filter(gm, obs, "bootstrap", 256, 54321)
+    assert a.same_result(b) and not a.same_result(c)
+    ens = pf.run_ensemble(gm, obs, "bootstrap", 1, 256, 5)
+    single = pf.run_filter(gm, obs, "bootstrap", 256, pf.filter_seeds(5, 1)[0])
+    assert np.array_equal(ens.mean_estimates, single.estimates)
+
+
+def test_sharding_does_not_change_filters():
+    """Filters computed as two half-banks (as two ranks would) equal the
+    full bank bit for bit (GPU-count invariance)."""
+    gm, obs = _cfg0_small()
+    keys = pf.philox.filter_keys(9, 4)
+    outs = []
+    for lo, hi in ((0, 4), (0, 2), (2, 4)):
+        b = pf.FilterBank(gm, hi - lo, 128, keys[lo:hi], len(obs), dtype=torch.float32)
+        b.load_observations(obs)
+        b.init()
+        b.run()
+        outs.append((b.est.cpu().numpy(), b.lnc_tr.cpu().numpy()))
+    full_est, full_lnc = outs[0]
+    assert np.array_equal(full_est[:, :2], outs[1][0]) and np.array_equal(full_est[:, 2:], outs[2][0])
+    assert np.array_equal(full_lnc[:, :2], outs[1][1]) and np.array_equal(full_lnc[:, 2:], outs[2][1])
+
+
+def test_left_to_right_average():
+    gm, obs = _cfg0_small()
+    out = pf.run_ensemble(gm, obs, "bootstrap", 5, 64, 11)
+    acc = out.filter_outputs[0].estimates.copy()
+    for fo in out.filter_outputs[1:]:
+        acc += fo.estimates
+    assert np.array_equal(out.mean_estimates, acc / 5.0)
+
+
+def test_divergence_raises():
+    gm = pf.Lorenz63Model(substeps=40, prior_mean=(1e200, 1e200, 1e200), prior_var=1.0)
+    with pytest.raises(pf.NumericalDivergenceError):
+        pf.run_filter(gm, np.zeros((2, 1)), "bootstrap", 16, 0)
+
+
+def test_nan_observation_raises_value_error():
+    gm, obs = _cfg0_small()
+    obs = obs.copy()
+    obs[1, 0] = np.nan
+    with pytest.raises(ValueError):
+        pf.run_filter(gm, obs, "bootstrap", 16, 0)
+
+
+def test_invalid_arguments():
+    gm, obs = _cfg0_small()
+    with pytest.raises(ValueError):
+        pf.run_ensemble(gm, obs, "bootstrap", 0, 10, 0)
+    with pytest.raises(ValueError):
+        pf.run_ensemble(gm, obs, "bootstrap", 2, 10, 0, workers=0)
+    with pytest.raises(ValueError):
+        pf.run_filter(gm, obs, "smooth", 10, 0)
+    with pytest.raises(ValueError):
+        pf.run_filter(gm, np.zeros((0, 2)), "bootstrap", 10, 0)
+
+
+def test_philox_filter_tracks_truth():
+    """Production-mode sanity: the cfg0 bank tracks the truth about as well
+    as the CPU oracle does (statistical parity proper: test_gpu_stats.py)."""
+    truth0, states, obs = orc.lorenz_truth(seed=4, n_obs=60)
+    _, gm = _lorenz_models(truth0)
+    out = pf.run_ensemble(gm, obs, "bootstrap", 4, 1000, 1)
+    mse = np.mean((out.mean_estimates - states) ** 2)
+    assert mse < 2.0, mse

@@ -143,3 +143,41 @@ def test_tape_recorder_reproduces_seeded_run(golden):
     assert np.array_equal(tr.estimates, g["f_est"])
     kinds = [k for k, _ in rec.log]
     assert kinds[0] == "normal" and kinds[1] == "normal" and kinds[2] == "exponential"
+
+
+# ---- the oracle's C kernels (CPU baseline) are bit-identical too ----------
+
+def _ck():
+    from oracle import ckernels
+
+    try:
+        ckernels.load()
+    except FileNotFoundError:
+        import subprocess
+
+        subprocess.run(["make", "-s", "-C", "oracle"], check=True)
+    return ckernels
+
+
+def test_ckernels_lorenz_golden(golden):
+    g = golden["kernels"]
+    out = _ck().lorenz_euler_block(g["lz_states"], g["lz_noise"], 1e-3, 10.0, 28.0, 8.0 / 3.0)
+    assert np.array_equal(out, g["lz_out"])
+
+
+@pytest.mark.parametrize("tag", ["rect", "sq"])
+def test_ckernels_fhn_golden(golden, tag):
+    g = golden["kernels"]
+    p = g[f"fhn_{tag}_params"]
+    u, v = _ck().fhn_euler_block(g[f"fhn_{tag}_U"], g[f"fhn_{tag}_V"], g[f"fhn_{tag}_drive"],
+                                 g[f"fhn_{tag}_noise"], p[0], p[1], tuple(p[2:6]),
+                                 tuple(p[6:9]), p[9])
+    assert np.array_equal(u, g[f"fhn_{tag}_u_new"])
+    assert np.array_equal(v, g[f"fhn_{tag}_v_new"])
+
+
+def test_ckernels_resample_golden(golden):
+    g = golden["kernels"]
+    for i in range(int(g["ri_count"])):
+        assert np.array_equal(_ck().resample_indices(g[f"ri_cum_{i}"], g[f"ri_u_{i}"]),
+                              g[f"ri_idx_{i}"])
