@@ -315,6 +315,10 @@ def run_ours(args, cfg):
     roof["traffic"] = _ncu_traffic(args.config)
 
     # e2e through the public API (host observations in, host results out)
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"profile_run": args.config, "value": value, "kernel_ms": kern_ms}))
+        return 0
     _barrier(world)
     e2e_obs = obs[: args.steps]
     t0 = time.perf_counter()
@@ -372,6 +376,8 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="timed steps only (no e2e / CPU baseline): for ncu captures")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

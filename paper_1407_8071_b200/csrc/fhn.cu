@@ -227,6 +227,167 @@ __global__ void __launch_bounds__(256) fhn_interval_kernel(
   }
 }
 
+// ---- fp32 production kernel (Philox, Neumann Laplacian) --------------------
+// Same dynamics, restated for throughput (tolerance-checked, not bit-exact):
+//  * shared plane padded with a ghost ring holding the mirrored boundary
+//    value ("ghost = self"), so the 5-point stencil has no boundary
+//    predicates: coupling*nb - deg*u == coupling*(sum of 4 padded nbrs - 4u)
+//    when degree_drive == -coupling (BASELINE cfg3/cfg4);
+//  * constants pre-folded into FFMA form; MUFU-approx Box-Muller;
+//  * register budget for 4 resident CTAs/SM (32 warps) to hide the
+//    dependent Philox/MUFU latencies.
+struct FhnFast {
+  int rows, cols, n_sub, n_obs, nseg, nodes;
+  float a3, a2, a1, a0;       // cubic
+  float dt, dtc, dtc4;        // dt, dt*coupling, 4*dt*coupling
+  float wc, uc, c0;           // w' = wc*w + uc*u + c0  (1+dt*b1, dt*b0, dt*b2)
+  float sig_v, sig_w;
+  double obs_coef;
+};
+
+// Lattice geometry is compile-time (ROWS x COLS, R rows per thread) so every
+// shared-memory access is base register + immediate.  TAPE=true reads the
+// standard normals from an fp64 tape (parity tests of this exact kernel).
+template <int ROWS, int COLS, int R, bool TAPE>
+__global__ void __launch_bounds__(256, 4) fhn_fast_kernel(
+    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
+    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
+    int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
+    const double *__restrict__ tape, uint32_t *__restrict__ status) {
+  constexpr int W = COLS + 2;
+  constexpr int P = (ROWS + 2) * W;
+  constexpr int NSEG = (ROWS + R - 1) / R;
+  constexpr int NODES = ROWS * COLS;
+  static_assert(R % 2 == 0, "rows per thread must be even (Philox row pairs)");
+  extern __shared__ __align__(16) float vsp[];  // [2][P]
+  __shared__ double red[1];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  const int seg = tid / COLS;
+  const int col = tid - seg * COLS;
+  const bool active = seg < NSEG;
+  const int row0 = seg * R;
+  // horizontal ghost target: the mirrored cell for edge columns, else self
+  const int hg = col == 0 ? -1 : (col == COLS - 1 ? 1 : 0);
+  const int base = (row0 + 1) * W + col + 1;  // this thread's first cell
+
+  for (int64_t p = blockIdx.x; p < MN; p += gridDim.x) {
+    const int64_t f = p / N;
+    const uint32_t j = static_cast<uint32_t>(p - f * N);
+    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+    const float *xs = xin + src * 2 * static_cast<int64_t>(NODES);
+    if (tid == 0) bad = 0;
+    float v[R], w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      v[r] = 0.f;
+      w[r] = 0.f;
+      if (active && row0 + r < ROWS) {
+        const int node = (row0 + r) * COLS + col;
+        v[r] = __ldg(xs + node);
+        w[r] = __ldg(xs + NODES + node);
+        float *cell = vsp + base + r * W;
+        cell[0] = v[r];
+        cell[hg] = v[r];
+        if (r == 0 && row0 == 0) cell[-W] = v[r];
+        if (row0 + r == ROWS - 1) cell[W] = v[r];
+      }
+    }
+    __syncthreads();
+
+    Key2 key{0u, 0u};
+    if (!TAPE) key = load_key(keys, f);
+    const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
+    for (int k = 0; k < c.n_sub; ++k) {
+      const float *cur = vsp + (k & 1) * P + base;
+      float *nxt = vsp + ((k & 1) ^ 1) * P + base;
+      if (active) {
+        float up = cur[-W];  // old value of the row above this strip
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q) {
+          float zv0, zw0, zv1, zw1;
+          if (TAPE) {
+            const int64_t b0 = ((f * c.n_sub + k) * 2 * static_cast<int64_t>(N) + j) * NODES +
+                               (row0 + 2 * q) * COLS + col;
+            const int64_t wo = static_cast<int64_t>(N) * NODES;
+            const bool ok1 = row0 + 2 * q + 1 < ROWS;
+            zv0 = float(tape[b0]);
+            zw0 = float(tape[b0 + wo]);
+            zv1 = ok1 ? float(tape[b0 + COLS]) : 0.f;
+            zw1 = ok1 ? float(tape[b0 + wo + COLS]) : 0.f;
+          } else {
+            const uint32_t node_pair = static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col);
+            const uint4 rr = philox10(make_uint4(j, step0 + k, node_pair, kPurposeFhn), key);
+            const float2 g0 = box_muller_fast(rr.x, rr.y);
+            const float2 g1 = box_muller_fast(rr.z, rr.w);
+            zv0 = g0.x;
+            zw0 = g0.y;
+            zv1 = g1.x;
+            zw1 = g1.y;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 2 * q + h;
+            if (row0 + r < ROWS) {
+              const float *cell = cur + r * W;
+              const float u = v[r];
+              const float dn = (r < R - 1 && row0 + r + 1 < ROWS) ? v[r + 1] : cell[W];
+              const float nb = ((up + dn) + cell[-1]) + cell[1];
+              const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
+              // u + dt(p3 - w) + dt*coupling*(nb - 4u) + sig_v*zv
+              float un = fmaf(c.dt, p3 - w[r], u);
+              un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
+              un = fmaf(c.sig_v, h ? zv1 : zv0, un);
+              w[r] = fmaf(c.sig_w, h ? zw1 : zw0, fmaf(c.wc, w[r], fmaf(c.uc, u, c.c0)));
+              float *dst = nxt + r * W;
+              dst[0] = un;
+              dst[hg] = un;
+              if (r == 0 && row0 == 0) dst[-W] = un;
+              if (row0 + r == ROWS - 1) dst[W] = un;
+              up = u;
+              v[r] = un;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    // epilogue: divergence flag, store, electrode log-likelihood
+    bool fin = true;
+    float *xd = xout + p * 2 * static_cast<int64_t>(NODES);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (active && row0 + r < ROWS) {
+        const int node = (row0 + r) * COLS + col;
+        fin = fin && isfinite(v[r]) && isfinite(w[r]);
+        xd[node] = v[r];
+        xd[NODES + node] = w[r];
+      }
+    }
+    if (!fin) bad = 1;
+    if (tid < 32) {
+      const float *fv = vsp + (c.n_sub & 1) * P;
+      double acc = 0.0;
+      for (int i = tid; i < c.n_obs; i += 32) {
+        const int n = __ldg(obs_idx + i);
+        const int rr = n / COLS;
+        const double rsd = __ldg(y + i) - static_cast<double>(fv[(rr + 1) * W + (n - rr * COLS) + 1]);
+        acc = fma(rsd, rsd, acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+      if (tid == 0) red[0] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      logw[p] = static_cast<float>(c.obs_coef * red[0]);
+      if (bad) atomicOr(status + f, PF_ST_DIVERGED);
+    }
+    __syncthreads();
+  }
+}
+
 // accel.fhn_euler_block (general form, fp64, per-node drive), one thread per
 // node, reference order.
 __global__ void fhn_block_op_kernel(const double *__restrict__ U, const double *__restrict__ V,
@@ -303,6 +464,68 @@ static int launch_fhn(const FhnConsts &c, const void *x_in, const int32_t *anc, 
   return check_launch("pf_fhn_interval");
 }
 
+template <int ROWS, int COLS, bool TAPE>
+static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
+                             const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
+                             int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
+                             uint32_t *status, cudaStream_t s) {
+  constexpr int R = kFhnRows;
+  constexpr int threads = (((ROWS + R - 1) / R * COLS) + 31) / 32 * 32;
+  static_assert(threads <= 256, "lattice too large for the fast kernel");
+  const size_t smem = 2 * static_cast<size_t>((ROWS + 2) * (COLS + 2)) * sizeof(float);
+  auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int sms = kSmCount, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(MN, static_cast<int64_t>(sms) * per_sm);
+  kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(
+      static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
+      static_cast<float *>(logw), MN, N, fc, keys, t, tape, status);
+  return check_launch("pf_fhn_interval(fast)");
+}
+
+// The fp32 fast path covers lattices with a compiled geometry; others use
+// the generic kernel.
+static bool fhn_fast_supported(const pf_fhn_params *p) {
+  return p->rows == 30 && p->cols == 50 && p->degree_drive == -p->coupling;
+}
+
+static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *anc, void *x_out,
+                           const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
+                           int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
+                           uint32_t *status, cudaStream_t s) {
+  FhnFast fc;
+  fc.rows = c.rows;
+  fc.cols = c.cols;
+  fc.n_sub = c.n_sub;
+  fc.n_obs = c.n_obs;
+  fc.nseg = c.nseg;
+  fc.nodes = c.nodes;
+  fc.a3 = float(c.a3);
+  fc.a2 = float(c.a2);
+  fc.a1 = float(c.a1);
+  fc.a0 = float(c.a0);
+  fc.dt = float(c.dt);
+  fc.dtc = float(c.dt * c.coupling);
+  fc.dtc4 = float(4.0 * c.dt * c.coupling);
+  fc.wc = float(1.0 + c.dt * c.b1);
+  fc.uc = float(c.dt * c.b0);
+  fc.c0 = float(c.dt * c.b2);
+  fc.sig_v = float(c.sig_v);
+  fc.sig_w = float(c.sig_w);
+  fc.obs_coef = c.obs_coef;
+  if (tape)
+    return launch_fhn_fast_t<30, 50, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
+                                           t, tape, status, s);
+  return launch_fhn_fast_t<30, 50, false>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t,
+                                          tape, status, s);
+}
+
 }  // namespace pf
 
 using namespace pf;
@@ -326,6 +549,9 @@ int pf_fhn_interval(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
   const int64_t MN = M * N;
   const int32_t n32 = static_cast<int32_t>(N);
   const cudaStream_t s = as_stream(stream);
+  if (dtype == PF_F32 && fhn_fast_supported(p))
+    return launch_fhn_fast(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32, keys, t, z_tape,
+                           status, s);
   if (dtype == PF_F64)
     return z_tape ? launch_fhn<double, 1>(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32,
                                           keys, t, z_tape, status, s)

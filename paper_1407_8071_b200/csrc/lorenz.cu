@@ -136,23 +136,19 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
             make_uint4(static_cast<uint32_t>(j), t, static_cast<uint32_t>((k0 >> 2) * 3 + q),
                        kPurposeLorenz),
             key);
-        const float2 g0 = box_muller_f32(rr.x, rr.y);
-        const float2 g1 = box_muller_f32(rr.z, rr.w);
+        const float2 g0 = box_muller_fast(rr.x, rr.y);
+        const float2 g1 = box_muller_fast(rr.z, rr.w);
         z[4 * q + 0] = g0.x;
         z[4 * q + 1] = g0.y;
         z[4 * q + 2] = g1.x;
         z[4 * q + 3] = g1.y;
       }
-      if (k0 + 4 <= c.n_sub) {
+      // fully unrolled with predication: z[] stays in registers
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q)
+        if (k0 + q < c.n_sub)
           lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r, nb,
                               cz);
-      } else {
-        for (int q = 0; q < c.n_sub - k0; ++q)
-          lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r, nb,
-                              cz);
-      }
     }
     x1 = T(a1);
     x2 = T(a2);

@@ -48,6 +48,39 @@ __device__ __forceinline__ float2 box_muller_f32(uint32_t a, uint32_t b) {
   return make_float2(r * c, r * s);
 }
 
+// ---- fast fp32 Box-Muller on the MUFU approximations -----------------------
+// lg2/sqrt/sin/cos .approx.ftz: ~2^-21 relative error, no denormal or
+// special-case branches (the precise sqrtf/logf paths cost ~2x the issue
+// slots).  The angle is centred on [-pi, pi) where sin/cos.approx are most
+// accurate; the resulting sign flip is immaterial for a symmetric law.
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sin_approx(float x) {
+  float y;
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float cos_approx(float x) {
+  float y;
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float2 box_muller_fast(uint32_t a, uint32_t b) {
+  const float u = fmaf(static_cast<float>(a), 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  const float r = sqrt_approx(-1.3862943611198906f * lg2_approx(u));
+  const float ang = fmaf(static_cast<float>(b >> 8), 3.7450702829239286e-07f, -3.14159265358979f);
+  return make_float2(r * cos_approx(ang), r * sin_approx(ang));
+}
+
 // ---- fp64 transforms (53-bit uniforms) ------------------------------------
 __device__ __forceinline__ double u53_open0(uint32_t hi, uint32_t lo) {
   // (v + 1) * 2^-53 in (0, 1] with v a 53-bit integer
