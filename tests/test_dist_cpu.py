@@ -1,0 +1,84 @@
+"""Multi-process (gloo, world size 2, CPU) tests of the sharding and the
+disjoint-support estimate exchange used by run_ensemble on N GPUs."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1407_8071_b200 import dist as pdist
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_range_partitions_filters():
+    for m in (1, 2, 7, 64, 4096):
+        for w in (1, 2, 3, 8):
+            if m < w:
+                continue
+            spans = [pdist.shard_range(m, r, w) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == m
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        pdist.shard_range(4, 2, 2)
+
+
+def _worker(rank, world, port, T, M, dim, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(0)
+        full = rng.standard_normal((T, M, dim))  # every filter's estimate trace
+        lo, hi = pdist.shard_range(M, rank, world)
+        buf = torch.zeros((T, M, dim), dtype=torch.float64)
+        ex = pdist.EstimateExchange(buf)
+        for k in range(T):
+            buf[k, lo:hi] = torch.from_numpy(full[k, lo:hi])  # this rank's kernel output
+            ex.step_done(k)
+        ex.finish()
+        # every rank now holds every filter's exact estimate
+        assert np.array_equal(buf.numpy(), full)
+        # fixed left-to-right average == the reference's average_estimates order
+        acc = buf[:, 0].clone()
+        for m in range(1, M):
+            acc += buf[:, m]
+        mean = (acc / M).numpy()
+        ref = full[:, 0].copy()
+        for m in range(1, M):
+            ref += full[:, m]
+        ref /= float(M)
+        assert mean.tobytes() == ref.tobytes()
+        st = torch.zeros(M, dtype=torch.int32)
+        st[lo:hi] = rank + 1
+        pdist.allreduce_disjoint(st)
+        hi0 = pdist.shard_range(M, 0, world)[1]
+        assert st.tolist() == [1 if f < hi0 else 2 for f in range(M)]
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - surfaced through the queue
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_disjoint_allreduce_two_ranks_bit_identical():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 5, 7, 4, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
