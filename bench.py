@@ -44,6 +44,12 @@ CONFIGS = {
                  desc="Lorenz-63, M=4096 x N=1024 (M*N=2^22), 40 Euler steps/obs, fp32"),
     "cfg2m256": dict(kind="lorenz", M=256, N=16384, dtype="float32",
                      desc="Lorenz-63, M=256 x N=16384 (M*N=2^22), 40 Euler steps/obs, fp32"),
+    "cfg1b": dict(kind="resample", M=1 << 16, N=1 << 10, dtype="float32",
+                  desc="resampling microbench: bank M=2^16 x N=2^10, fp32 logw ~ N(0, sigma^2), "
+                       "logsumexp + multinomial + 3-float ancestor gather"),
+    "cfg1c": dict(kind="resample", M=1, N=1 << 26, dtype="float32",
+                  desc="resampling microbench: centralised M=1 x N=2^26, fp32 logw ~ "
+                       "N(0, sigma^2), logsumexp + multinomial + 3-float ancestor gather"),
     "cfg0": dict(kind="lorenz", M=4, N=1000, dtype="float64",
                  desc="Lorenz-63, M=4 x N=1000, 40 Euler steps/obs, fp64"),
 }
@@ -230,6 +236,124 @@ def run_reference_arm(args, cfg):
     return 0
 
 
+# ----------------------------------------------------------------- cfg1: resampling
+
+RESAMPLE_BYTES_PER_PARTICLE = 32.0  # logw 4 + ancestor 4 + gather read 12 + write 12
+
+
+def cpu_resample_baseline(cfg, sigma, budget_s=10.0):
+    """Reference CPU path for cfg1 on one core (the reference has no
+    intra-filter parallelism): normalize_log_weights + multinomial_resample
+    (numpy cumsum + exponential spacings + C merge) + gather, fp64."""
+    from oracle import ckernels
+    from oracle import parpf_oracle as orc
+
+    ckernels.install()
+    rng = np.random.default_rng(0)
+    n = min(cfg["N"], 1 << 22)
+    m_per = max(1, (1 << 20) // n)
+    lw = (rng.standard_normal((m_per, n)) * sigma).astype(np.float32)
+    x = rng.standard_normal((m_per * n, 3)).astype(np.float32)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        for f in range(m_per):
+            w, _ = orc.normalize_log_weights(lw[f])
+            idx = orc.multinomial_resample_indices(w, n, rng)
+            _ = x[f * n + idx]
+        done += m_per * n
+    wall = time.perf_counter() - t0
+    return {"value": done / wall, "unit": "particles/s", "cores": 1, "kind": "port",
+            "sample": f"{m_per} filter(s) x N={n}, repeated for {wall:.1f} s on 1 core, fp64 "
+                      f"(numpy + C merge)"}
+
+
+def run_resample(args, cfg):
+    import torch
+
+    from paper_1407_8071_b200 import _lib, philox
+
+    rank, world, local = _dist_setup()
+    M, N = cfg["M"], cfg["N"]
+    lo, hi = (0, M)
+    if world > 1:
+        from paper_1407_8071_b200 import dist as pdist
+
+        if M % world:
+            raise SystemExit(f"M={M} does not shard over {world} GPUs (replicas only)")
+        lo, hi = pdist.shard_range(M, rank, world)
+    Ml = hi - lo
+    MN = Ml * N
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    logw = (torch.randn(MN, device="cuda", generator=g) * args.sigma).float()
+    x_in = torch.randn((3, MN), device="cuda", generator=g)
+    x_out = torch.empty_like(x_in)
+    anc = torch.empty(MN, dtype=torch.int32, device="cuda")
+    lnc = torch.zeros(Ml, dtype=torch.float64, device="cuda")
+    coll = torch.zeros(Ml, dtype=torch.uint8, device="cuda")
+    st = torch.zeros(Ml, dtype=torch.int32, device="cuda")
+    keys = torch.from_numpy(philox.filter_keys(7, M)[lo:hi].view(np.int32)).cuda()
+    wsb = _lib.load().pf_resample_workspace_bytes(Ml, N)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    s = _lib.stream_ptr()
+
+    def step(k):
+        _lib.call("pf_segmented_resample", _lib.PF_F32, _lib.ptr(logw), Ml, N, None,
+                  _lib.ptr(keys), k + 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll),
+                  _lib.ptr(st), _lib.ptr(ws), wsb, s)
+        _lib.call("pf_gather_planes", _lib.PF_F32, _lib.ptr(x_in), _lib.ptr(anc), MN, 3,
+                  _lib.ptr(x_out), s)
+
+    for k in range(args.warmup):
+        step(k)
+    _barrier(world)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record()
+        for i in range(args.steps):
+            step(args.warmup + i)
+        end.record()
+        torch.cuda.synchronize()
+    _barrier(world)
+    local_s = start.elapsed_time(end) / 1e3
+    elapsed = _max_over_ranks(local_s, world)
+    value = M * N * args.steps / elapsed
+    per = local_s / args.steps
+    peaks, peak_src = _peaks()
+    achieved = MN * RESAMPLE_BYTES_PER_PARTICLE / per / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
+            "kernel": "pf_segmented_resample + pf_gather_planes (one step)",
+            "algorithmic": f"{RESAMPLE_BYTES_PER_PARTICLE:.0f} B/particle x {MN} particles",
+            "traffic": _ncu_traffic(args.config)}
+    # e2e: host logw in (pinned), host ancestors out, through the C ABI
+    h_lw = logw.cpu().pin_memory()
+    h_anc = torch.empty(MN, dtype=torch.int32).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        logw.copy_(h_lw, non_blocking=True)
+        step(i)
+        h_anc.copy_(anc, non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = _max_over_ranks(time.perf_counter() - t0, world)
+    if rank == 0:
+        cb = None if (world > 1 or args.no_cpu_baseline) else cpu_resample_baseline(cfg, args.sigma)
+        line = {"metric": "particles/s (logsumexp + multinomial resampling + gather)",
+                "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+                "higher_is_better": True, "scaling": "weak" if M > 1 else "replicas",
+                "vs_baseline": None, "dtype": "f32 logw / f64 CDF", "data": "synthetic",
+                "config": {"workload": args.config, "desc": cfg["desc"], "sigma": args.sigma,
+                           "M": M, "N": N},
+                "roofline": roof, "cpu_baseline": cb,
+                "e2e": {"value": M * N * args.steps / e2e_s, "unit": "particles/s",
+                        "h2d_bytes_per_step": MN * 4, "d2h_bytes_per_step": MN * 4},
+                "gpu_launches": (2 if N <= 8192 else 10) * args.steps,
+                "clocks": clocks.summary()}
+        print(json.dumps(line))
+    return 0
+
+
 # ----------------------------------------------------------------- our arm
 
 def run_ours(args, cfg):
@@ -376,12 +500,15 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sigma", type=float, default=1.0, help="cfg1 log-weight std")
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no e2e / CPU baseline): for ncu captures")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
+    if cfg["kind"] == "resample":
+        return run_resample(args, cfg)
     return run_ours(args, cfg)
 
 

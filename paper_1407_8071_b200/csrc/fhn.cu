@@ -17,6 +17,8 @@
 #include "common.cuh"
 #include "philox.cuh"
 
+#include <cstdlib>
+
 namespace pf {
 
 constexpr int kFhnRows = 6;  // rows per thread (even: Philox pairs rows)
@@ -248,8 +250,8 @@ struct FhnFast {
 // Lattice geometry is compile-time (ROWS x COLS, R rows per thread) so every
 // shared-memory access is base register + immediate.  TAPE=true reads the
 // standard normals from an fp64 tape (parity tests of this exact kernel).
-template <int ROWS, int COLS, int R, bool TAPE>
-__global__ void __launch_bounds__(256, 4) fhn_fast_kernel(
+template <int ROWS, int COLS, int R, bool TAPE, int MINB>
+__global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
     const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
     int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
@@ -297,6 +299,9 @@ __global__ void __launch_bounds__(256, 4) fhn_fast_kernel(
 
     Key2 key{0u, 0u};
     if (!TAPE) key = load_key(keys, f);
+    // Philox normals come out of box_muller_fast_unscaled: fold sqrt(2 ln 2)
+    const float sv = TAPE ? c.sig_v : c.sig_v * kSqrt2Ln2;
+    const float sw = TAPE ? c.sig_w : c.sig_w * kSqrt2Ln2;
     const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
     for (int k = 0; k < c.n_sub; ++k) {
       const float *cur = vsp + (k & 1) * P + base;
@@ -318,8 +323,8 @@ __global__ void __launch_bounds__(256, 4) fhn_fast_kernel(
           } else {
             const uint32_t node_pair = static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col);
             const uint4 rr = philox10(make_uint4(j, step0 + k, node_pair, kPurposeFhn), key);
-            const float2 g0 = box_muller_fast(rr.x, rr.y);
-            const float2 g1 = box_muller_fast(rr.z, rr.w);
+            const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
+            const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
             zv0 = g0.x;
             zw0 = g0.y;
             zv1 = g1.x;
@@ -337,8 +342,8 @@ __global__ void __launch_bounds__(256, 4) fhn_fast_kernel(
               // u + dt(p3 - w) + dt*coupling*(nb - 4u) + sig_v*zv
               float un = fmaf(c.dt, p3 - w[r], u);
               un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
-              un = fmaf(c.sig_v, h ? zv1 : zv0, un);
-              w[r] = fmaf(c.sig_w, h ? zw1 : zw0, fmaf(c.wc, w[r], fmaf(c.uc, u, c.c0)));
+              un = fmaf(sv, h ? zv1 : zv0, un);
+              w[r] = fmaf(sw, h ? zw1 : zw0, fmaf(c.wc, w[r], fmaf(c.uc, u, c.c0)));
               float *dst = nxt + r * W;
               dst[0] = un;
               dst[hg] = un;
@@ -464,7 +469,7 @@ static int launch_fhn(const FhnConsts &c, const void *x_in, const int32_t *anc, 
   return check_launch("pf_fhn_interval");
 }
 
-template <int ROWS, int COLS, bool TAPE>
+template <int ROWS, int COLS, bool TAPE, int MINB>
 static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
                              const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                              int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
@@ -473,7 +478,7 @@ static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t 
   constexpr int threads = (((ROWS + R - 1) / R * COLS) + 31) / 32 * 32;
   static_assert(threads <= 256, "lattice too large for the fast kernel");
   const size_t smem = 2 * static_cast<size_t>((ROWS + 2) * (COLS + 2)) * sizeof(float);
-  auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE>;
+  auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE, MINB>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int per_sm = 0;
@@ -489,10 +494,153 @@ static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t 
   return check_launch("pf_fhn_interval(fast)");
 }
 
+// ---- warp-per-particle variant ------------------------------------------
+// One warp owns one particle for the whole interval: lane r holds lattice
+// row r (ROWS <= 32) in registers (v[COLS], w[COLS]).  Left/right
+// neighbours are the lane's own registers, up/down come from
+// __shfl_sync with a clamped source lane (which *is* the ghost = self
+// Neumann boundary), so there is no shared memory traffic and no CTA
+// barrier inside the time loop; 25 independent column pairs per lane give
+// the scheduler instruction-level parallelism instead of thread-level.
+template <int ROWS, int COLS, bool TAPE>
+__global__ void __launch_bounds__(64, 5) fhn_warp_kernel(
+    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
+    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
+    int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
+    const double *__restrict__ tape, uint32_t *__restrict__ status) {
+  static_assert(ROWS <= 32 && COLS % 2 == 0, "warp kernel: ROWS <= 32, even COLS");
+  constexpr int NODES = ROWS * COLS;
+  constexpr int WPB = 2;  // warps per block
+  extern __shared__ __align__(16) float wsm[];  // [WPB][NODES], epilogue only
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float *vs = wsm + wib * NODES;
+  const int row = lane < ROWS ? lane : ROWS - 1;  // spare lanes shadow the last row
+  const int src_up = row > 0 ? row - 1 : 0;        // clamp = ghost = self
+  const int src_dn = row < ROWS - 1 ? row + 1 : ROWS - 1;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * WPB;
+
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * WPB + wib; p < MN; p += nwarps) {
+    const int64_t f = p / N;
+    const uint32_t j = static_cast<uint32_t>(p - f * N);
+    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+    const float2 *xs = reinterpret_cast<const float2 *>(xin + src * 2 * static_cast<int64_t>(NODES) +
+                                                        row * COLS);
+    float v[COLS], w[COLS];
+#pragma unroll
+    for (int q = 0; q < COLS / 2; ++q) {
+      const float2 a = __ldg(xs + q);
+      const float2 b = __ldg(xs + NODES / 2 + q);
+      v[2 * q] = a.x;
+      v[2 * q + 1] = a.y;
+      w[2 * q] = b.x;
+      w[2 * q + 1] = b.y;
+    }
+    Key2 key{0u, 0u};
+    if (!TAPE) key = load_key(keys, f);
+    const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
+    for (int k = 0; k < c.n_sub; ++k) {
+      float prev = v[0];  // left ghost of column 0 = itself
+#pragma unroll
+      for (int q = 0; q < COLS / 2; ++q) {
+        float z[4];
+        if (TAPE) {
+          const int64_t b0 = ((f * c.n_sub + k) * 2 * static_cast<int64_t>(N) + j) * NODES +
+                             row * COLS + 2 * q;
+          const int64_t wo = static_cast<int64_t>(N) * NODES;
+          z[0] = float(tape[b0]);
+          z[1] = float(tape[b0 + wo]);
+          z[2] = float(tape[b0 + 1]);
+          z[3] = float(tape[b0 + wo + 1]);
+        } else {
+          const uint4 rr = philox10(
+              make_uint4(j, step0 + k, static_cast<uint32_t>(row * (COLS / 2) + q), kPurposeFhn),
+              key);
+          const float2 g0 = box_muller_fast(rr.x, rr.y);
+          const float2 g1 = box_muller_fast(rr.z, rr.w);
+          z[0] = g0.x;
+          z[1] = g0.y;
+          z[2] = g1.x;
+          z[3] = g1.y;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = 2 * q + h;
+          const float u = v[cc];
+          const float up = __shfl_sync(0xffffffffu, u, src_up);
+          const float dn = __shfl_sync(0xffffffffu, u, src_dn);
+          const float rt = cc < COLS - 1 ? v[cc + 1] : u;
+          const float nb = ((up + dn) + prev) + rt;
+          const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
+          float un = fmaf(c.dt, p3 - w[cc], u);
+          un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
+          w[cc] = fmaf(c.sig_w, z[2 * h + 1], fmaf(c.wc, w[cc], fmaf(c.uc, u, c.c0)));
+          v[cc] = fmaf(c.sig_v, z[2 * h], un);
+          prev = u;
+        }
+      }
+    }
+
+    // epilogue: store, divergence flag, electrode log-likelihood
+    bool fin = true;
+#pragma unroll
+    for (int cc = 0; cc < COLS; ++cc) fin = fin && isfinite(v[cc]) && isfinite(w[cc]);
+    if (lane < ROWS) {
+      float2 *xd = reinterpret_cast<float2 *>(xout + p * 2 * static_cast<int64_t>(NODES) +
+                                              row * COLS);
+#pragma unroll
+      for (int q = 0; q < COLS / 2; ++q) {
+        xd[q] = make_float2(v[2 * q], v[2 * q + 1]);
+        xd[NODES / 2 + q] = make_float2(w[2 * q], w[2 * q + 1]);
+        reinterpret_cast<float2 *>(vs + row * COLS)[q] = make_float2(v[2 * q], v[2 * q + 1]);
+      }
+    }
+    const bool any_bad = __any_sync(0xffffffffu, lane < ROWS && !fin);
+    __syncwarp();
+    double acc = 0.0;
+    for (int i = lane; i < c.n_obs; i += 32) {
+      const double rsd = __ldg(y + i) - static_cast<double>(vs[__ldg(obs_idx + i)]);
+      acc = fma(rsd, rsd, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      logw[p] = static_cast<float>(c.obs_coef * acc);
+      if (any_bad) atomicOr(status + f, PF_ST_DIVERGED);
+    }
+    __syncwarp();
+  }
+}
+
+template <int ROWS, int COLS, bool TAPE>
+static int launch_fhn_warp_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
+                             const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
+                             int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
+                             uint32_t *status, cudaStream_t s) {
+  constexpr int threads = 64;
+  const size_t smem = 2 * static_cast<size_t>(ROWS * COLS) * sizeof(float);
+  auto kern = fhn_warp_kernel<ROWS, COLS, TAPE>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int sms = kSmCount, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>((MN + 1) / 2, static_cast<int64_t>(sms) * per_sm);
+  kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(
+      static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
+      static_cast<float *>(logw), MN, N, fc, keys, t, tape, status);
+  return check_launch("pf_fhn_interval(warp)");
+}
+
 // The fp32 fast path covers lattices with a compiled geometry; others use
 // the generic kernel.
 static bool fhn_fast_supported(const pf_fhn_params *p) {
   return p->rows == 30 && p->cols == 50 && p->degree_drive == -p->coupling;
+}
+
+static bool use_warp_kernel() {
+  const char *e = getenv("PF_FHN_KERNEL");
+  return e && e[0] == 'w';  // "warp" selects the warp-per-particle kernel
 }
 
 static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *anc, void *x_out,
@@ -519,11 +667,26 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   fc.sig_v = float(c.sig_v);
   fc.sig_w = float(c.sig_w);
   fc.obs_coef = c.obs_coef;
+  if (use_warp_kernel()) {
+    if (tape)
+      return launch_fhn_warp_t<30, 50, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
+                                             t, tape, status, s);
+    return launch_fhn_warp_t<30, 50, false>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
+                                            t, tape, status, s);
+  }
   if (tape)
-    return launch_fhn_fast_t<30, 50, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
-                                           t, tape, status, s);
-  return launch_fhn_fast_t<30, 50, false>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t,
-                                          tape, status, s);
+    return launch_fhn_fast_t<30, 50, true, 4>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
+                                              t, tape, status, s);
+  const char *mb = getenv("PF_FHN_MINB");
+  const int minb = mb ? atoi(mb) : 5;
+  if (minb == 4)
+    return launch_fhn_fast_t<30, 50, false, 4>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                               keys, t, tape, status, s);
+  if (minb == 6)
+    return launch_fhn_fast_t<30, 50, false, 6>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                               keys, t, tape, status, s);
+  return launch_fhn_fast_t<30, 50, false, 5>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
+                                             t, tape, status, s);
 }
 
 }  // namespace pf

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
     // 4 substeps = 12 normals = 3 Philox blocks
     const Key2 key = load_key(keys, f);
     const float dt = float(c.dt), ndts = float(-c.dts), r = float(c.r), nb = float(-c.b);
-    const float cz = float(c.sq * c.ns);
+    const float cz = float(c.sq * c.ns) * kSqrt2Ln2;  // normals are box_muller_fast_unscaled
     float a1 = float(x1), a2 = float(x2), a3 = float(x3);
     for (int k0 = 0; k0 < c.n_sub; k0 += 4) {
       float z[12];
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
             make_uint4(static_cast<uint32_t>(j), t, static_cast<uint32_t>((k0 >> 2) * 3 + q),
                        kPurposeLorenz),
             key);
-        const float2 g0 = box_muller_fast(rr.x, rr.y);
-        const float2 g1 = box_muller_fast(rr.z, rr.w);
+        const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
+        const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
         z[4 * q + 0] = g0.x;
         z[4 * q + 1] = g0.y;
         z[4 * q + 2] = g1.x;

@@ -77,7 +77,21 @@ __device__ __forceinline__ float cos_approx(float x) {
 __device__ __forceinline__ float2 box_muller_fast(uint32_t a, uint32_t b) {
   const float u = fmaf(static_cast<float>(a), 2.3283064365386963e-10f, 1.1641532182693481e-10f);
   const float r = sqrt_approx(-1.3862943611198906f * lg2_approx(u));
-  const float ang = fmaf(static_cast<float>(b >> 8), 3.7450702829239286e-07f, -3.14159265358979f);
+  // angle from 23 random mantissa bits without an int->float conversion:
+  // x in [2, 4) -> pi*x - 3*pi in [-pi, pi)
+  const float x = __uint_as_float((b & 0x007fffffu) | 0x40000000u);
+  const float ang = fmaf(x, 3.14159265358979f, -9.42477796076938f);
+  return make_float2(r * cos_approx(ang), r * sin_approx(ang));
+}
+
+// Same draw with the constant sqrt(2 ln 2) left out of the radius (callers
+// fold it into their noise scale): r' = sqrt(-log2 u), z = sqrt(2 ln 2) r'.
+constexpr float kSqrt2Ln2 = 1.1774100225154747f;
+__device__ __forceinline__ float2 box_muller_fast_unscaled(uint32_t a, uint32_t b) {
+  const float u = fmaf(static_cast<float>(a), 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  const float r = sqrt_approx(-lg2_approx(u));
+  const float x = __uint_as_float((b & 0x007fffffu) | 0x40000000u);
+  const float ang = fmaf(x, 3.14159265358979f, -9.42477796076938f);
   return make_float2(r * cos_approx(ang), r * sin_approx(ang));
 }
 

@@ -18,6 +18,8 @@ known-answer tests.
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 
 M0, M1 = 0xD2511F53, 0xCD9E8D57
@@ -46,7 +48,15 @@ def filter_seeds(master_seed, n_filters):
 
 
 def filter_keys(master_seed, n_filters) -> np.ndarray:
-    """(n_filters, 2) uint32 keys for the bank."""
+    """(n_filters, 2) uint32 keys for the bank (cached for int seeds: the
+    SeedSequence tree is deterministic and spawning is ~15 us per filter)."""
+    if isinstance(master_seed, (int, np.integer)) and not isinstance(master_seed, bool):
+        return _filter_keys_cached(int(master_seed), int(n_filters)).copy()
+    return np.stack([seed_key(s) for s in filter_seeds(master_seed, n_filters)]).astype(np.uint32)
+
+
+@functools.lru_cache(maxsize=32)
+def _filter_keys_cached(master_seed: int, n_filters: int) -> np.ndarray:
     return np.stack([seed_key(s) for s in filter_seeds(master_seed, n_filters)]).astype(np.uint32)
 
 

@@ -1,0 +1,123 @@
+"""Production (Philox) mode statistical parity with the reference algorithm.
+
+North star: over >= 64 seeds the GPU bank's MSE must reproduce the CPU
+reference's (within 5 %), and the ensemble estimator must show the paper's
+decomposition: variance ~ 1/(M N) and bias ~ 1/N (Corollary 2,
+PAPER.md:568-586).  The checks mirror parpf/verify.py:160-260
+(check_ensemble_variance_rate, check_bias_rate) with the Lorenz-63 cfg0
+model; independent replicates are simply more filters in one GPU bank.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import parpf_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1407_8071_b200 as pf  # noqa: E402
+
+
+def _cfg0(n_obs, seed=11):
+    truth0, states, obs = orc.lorenz_truth(seed=seed, n_obs=n_obs)
+    gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(truth0), prior_var=1.0)
+    om = orc.LorenzConfigModel(prior_mean=tuple(truth0))
+    return gm, om, states, obs
+
+
+def _bank_estimates(model, obs, n_filters, n_particles, master, dtype=torch.float64):
+    keys = pf.philox.filter_keys(master, n_filters)
+    bank = pf.FilterBank(model, n_filters, n_particles, keys, len(obs), dtype=dtype)
+    bank.load_observations(obs)
+    bank.init()
+    bank.run()
+    torch.cuda.synchronize()
+    bank.check_status()
+    return bank.est.cpu().numpy()  # (T, M, 3)
+
+
+def loglog_slope(x, y):
+    """metrics.loglog_slope (parpf/metrics.py:70-79): least-squares slope."""
+    return float(np.polyfit(np.log(x), np.log(y), 1)[0])
+
+
+def test_mse_matches_cpu_reference_over_64_seeds():
+    gm, om, states, obs = _cfg0(n_obs=40)
+    seeds = 64
+    M, N = 4, 1000
+    # GPU: 64 independent run_ensemble calls == one bank of 64*M filters
+    # grouped into ensembles of M (filters never interact).
+    est = _bank_estimates(gm, obs, seeds * M, N, 2024)          # (T, 64*M, 3)
+    ens = est.reshape(len(obs), seeds, M, 3).mean(axis=2)         # (T, 64, 3)
+    mse_gpu = ((ens - states[:, None, :]) ** 2).mean(axis=(0, 2))  # per seed
+    # CPU reference algorithm (oracle port, fp64), 64 seeds
+    from oracle import ckernels
+
+    ckernels.install()
+    mse_cpu = np.empty(seeds)
+    for s in range(seeds):
+        _, mean = orc.run_ensemble(om, obs, M, N, 5000 + s, workers=orc.cpu_cores())
+        mse_cpu[s] = ((mean - states) ** 2).mean()
+    d = mse_gpu.mean() - mse_cpu.mean()
+    se = np.sqrt(mse_gpu.var(ddof=1) / seeds + mse_cpu.var(ddof=1) / seeds)
+    print(f"MSE gpu {mse_gpu.mean():.5f} cpu {mse_cpu.mean():.5f} diff {d:+.5f} se {se:.5f}")
+    assert abs(d) <= 0.05 * mse_cpu.mean()
+    assert abs(d) <= 3.5 * se + 1e-12
+
+
+def test_ensemble_variance_decays_like_one_over_M():
+    """verify.check_ensemble_variance_rate analogue: slope in [-1.25, -0.75]."""
+    gm, _, _, obs = _cfg0(n_obs=10, seed=3)
+    reps, N = 500, 64
+    variances = []
+    Ms = (1, 2, 4, 8, 16)
+    for i, M in enumerate(Ms):
+        est = _bank_estimates(gm, obs, reps * M, N, 900 + i)
+        ens = est[-1].reshape(reps, M, 3).mean(axis=1)[:, 0]
+        variances.append(ens.var(ddof=1))
+    slope = loglog_slope(np.array(Ms, float), np.array(variances))
+    print("variance slope", slope, variances)
+    assert -1.25 <= slope <= -0.75
+
+
+def test_total_particle_variance_decays_like_one_over_MN():
+    """Variance depends on the total budget M*N (Corollary 2 first term)."""
+    gm, _, _, obs = _cfg0(n_obs=10, seed=4)
+    reps = 400
+    budget = []
+    variances = []
+    for i, (M, N) in enumerate(((2, 64), (4, 128), (8, 256), (16, 512))):
+        est = _bank_estimates(gm, obs, reps * M, N, 700 + i)
+        ens = est[-1].reshape(reps, M, 3).mean(axis=1)[:, 0]
+        budget.append(M * N)
+        variances.append(ens.var(ddof=1))
+    slope = loglog_slope(np.array(budget, float), np.array(variances))
+    print("MN slope", slope, variances)
+    assert -1.25 <= slope <= -0.75
+
+
+def test_bias_decays_like_one_over_N():
+    """verify.check_bias_rate analogue on one observation of a sharply
+    observed Lorenz state, against a 16 x 2^20-particle GPU proxy;
+    |bias| slope in [-1.35, -0.65]."""
+    truth0, _, obs = orc.lorenz_truth(seed=21, n_obs=1)
+    gm = pf.Lorenz63Model(substeps=40, obs_var=0.05, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(truth0), prior_var=4.0)
+    proxy = _bank_estimates(gm, obs, 16, 1 << 20, 1)[-1, :, 0].mean()
+    reps = 200_000
+    Ns = (8, 16, 32, 64, 128)
+    biases, ses = [], []
+    for i, N in enumerate(Ns):
+        est = _bank_estimates(gm, obs, reps, N, 300 + i)[-1, :, 0]
+        err = est - proxy
+        biases.append(abs(err.mean()))
+        ses.append(err.std(ddof=1) / np.sqrt(reps))
+    slope = loglog_slope(np.array(Ns, float), np.array(biases))
+    print("bias slope", slope, biases, ses)
+    assert biases[0] > 5 * ses[0]
+    assert -1.35 <= slope <= -0.65
