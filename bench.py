@@ -213,24 +213,33 @@ def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    resample = cfg["kind"] == "resample"
+
+    def sample(budget):
+        if resample:
+            return cpu_resample_baseline(cfg, args.sigma, budget_s=budget)
+        return cpu_baseline(cfg, budget_s=budget, steps=1)
+
     for _ in range(args.warmup):
-        cpu_baseline(cfg, budget_s=2.0, steps=1)
+        sample(2.0)
     vals = []
     t0 = time.perf_counter()
     cb = None
     for _ in range(args.steps):
-        cb = cpu_baseline(cfg, budget_s=max(3.0, 60.0 / max(args.steps, 1)), steps=1)
+        cb = sample(max(3.0, 60.0 / max(args.steps, 1)))
         vals.append(cb["value"])
     wall = time.perf_counter() - t0
     value = float(np.median(vals))
     cb["value"] = value
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "particle-steps/s",
+    unit = "particles/s" if resample else "particle-steps/s"
+    metric = "particles/s (logsumexp + multinomial resampling + gather)" if resample else METRIC
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"]},
             "cpu_baseline": cb,
-            "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0

@@ -20,6 +20,8 @@
 #include "common.cuh"
 #include "philox.cuh"
 
+#include <type_traits>
+
 namespace pf {
 
 constexpr int kBankMaxN = 8192;
@@ -27,42 +29,86 @@ constexpr int kBankThreads = 256;
 constexpr int kTile = 4096;          // wide path elements per tile
 constexpr int kTileThreads = 256;
 
-// E_j for sorted uniforms: Philox block (j>>1, t, 0, RSMP), two fp64
-// exponentials per block.
-__device__ __forceinline__ double spacing_exp(Key2 key, uint32_t t, int64_t j) {
-  const uint4 r = philox10(make_uint4(static_cast<uint32_t>(j >> 1),
-                                      t, static_cast<uint32_t>(j >> 33), kPurposeResample),
-                           key);
-  return (j & 1) ? exp1_f64(r.z, r.w) : exp1_f64(r.x, r.y);
-}
-
 template <typename TW>
 __device__ __forceinline__ double load_lw(const TW *p) {
   return static_cast<double>(*p);
 }
 
+// Production-mode exponential spacing E_j = -ln(U_j), one 32-bit Philox
+// word per draw (4 draws per Philox block), MUFU log2: ~2^-22 relative
+// accuracy, far below Monte Carlo noise; the order statistics are then formed
+// by an fp64 scan exactly as in resampling.py:24-26.
+__device__ __forceinline__ double spacing_exp_fast_word(uint32_t a) {
+  const float u = fmaf(static_cast<float>(a), 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  return static_cast<double>(-0.6931471805599453f * lg2_approx(u));
+}
+__device__ __forceinline__ double spacing_exp_fast(Key2 key, uint32_t t, int64_t j) {
+  const uint4 r = philox10(make_uint4(static_cast<uint32_t>(j >> 2), t,
+                                      static_cast<uint32_t>(j >> 34), kPurposeResample),
+                           key);
+  const uint32_t w = (j & 3) == 0 ? r.x : (j & 3) == 1 ? r.y : (j & 3) == 2 ? r.z : r.w;
+  return spacing_exp_fast_word(w);
+}
+
+// Exclusive block scan of one fp64 value per thread; returns the exclusive
+// prefix and writes the block total to *total.  scratch >= 33 doubles.
+__device__ __forceinline__ double block_exclusive_scan(double v, double *scratch, double *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = __dadd_rn(x, y);
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    double wv = lane < nw ? scratch[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, wv, o);
+      if (lane >= o) wv = __dadd_rn(wv, y);
+    }
+    scratch[lane] = wv;  // inclusive warp-total prefix
+  }
+  __syncthreads();
+  const double woff = warp > 0 ? scratch[warp - 1] : 0.0;
+  *total = scratch[nw - 1];
+  const double prev = __shfl_up_sync(0xffffffffu, x, 1);
+  const double excl = lane > 0 ? prev : 0.0;  // sum of lower lanes in this warp
+  __syncthreads();
+  return warp > 0 ? __dadd_rn(woff, excl) : excl;
+}
+
 // ---- bank path: one CTA per filter --------------------------------------
-template <typename TW, int MODE>
+// Thread t owns the IPT consecutive particles [t*IPT, t*IPT+IPT): weights,
+// CDF and sorted uniforms live in registers, the per-thread sums are
+// combined with one block scan, and only the CDF goes to shared memory for
+// the merge (binary search for the thread's first uniform, then a forward
+// walk over its sorted run).
+template <typename TW, int MODE, int IPT>
 __global__ void __launch_bounds__(kBankThreads) resample_bank_kernel(
     const TW *__restrict__ logw, int32_t N, const double *__restrict__ u_tape,
     const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
     double *__restrict__ lnc, uint8_t *__restrict__ collapsed, uint32_t *__restrict__ status) {
-  extern __shared__ double sm[];
-  double *s_cum = sm;      // N
-  double *s_u = sm + N;    // N
+  extern __shared__ double s_cum[];  // N
   __shared__ double scratch[33];
   const int tid = threadIdx.x;
   const int64_t f = blockIdx.x;
   const int64_t base = f * N;
+  const int i0 = tid * IPT;
 
-  // 1. load + max (+ NaN detection: np.max propagates NaN, core.py:132)
+  // 1. load + max (NaN detection: np.max propagates NaN, core.py:132)
+  double lw[IPT];
   double mx = -INFINITY;
   int nan = 0;
-  for (int i = tid; i < N; i += blockDim.x) {
-    const double v = load_lw(logw + base + i);
-    s_cum[i] = v;
-    nan |= isnan(v);
-    mx = fmax(mx, v);
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const int i = i0 + q;
+    lw[q] = i < N ? static_cast<double>(logw[base + i]) : -INFINITY;
+    nan |= isnan(lw[q]);
+    mx = fmax(mx, lw[q]);
   }
   nan = __syncthreads_or(nan);
   const double m = block_max(mx, scratch);
@@ -77,39 +123,61 @@ __global__ void __launch_bounds__(kBankThreads) resample_bank_kernel(
     return;
   }
 
-  // 2. e = exp(lw - m), total (fixed-order block reduction)
+  // 2. e = exp(lw - m) and the total (core.py:134-135)
   double part = 0.0;
-  for (int i = tid; i < N; i += blockDim.x) {
-    const double e = exp(__dsub_rn(s_cum[i], m));
-    s_cum[i] = e;
-    part = __dadd_rn(part, e);
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    lw[q] = i0 + q < N ? exp(__dsub_rn(lw[q], m)) : 0.0;
+    part = __dadd_rn(part, lw[q]);
   }
   const double total = block_sum(part, scratch);
 
-  // 3. w = e / total, inclusive scan -> cum
-  for (int i = tid; i < N; i += blockDim.x) s_cum[i] = __ddiv_rn(s_cum[i], total);
-  __syncthreads();
-  block_scan_inplace(s_cum, N, 0.0, scratch);
+  // 3. w = e / total, CDF = thread offset + running local sum
+  double run = 0.0;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    lw[q] = __ddiv_rn(lw[q], total);
+    run = __dadd_rn(run, lw[q]);
+    lw[q] = run;  // local inclusive prefix
+  }
+  double wtot;
+  const double off = block_exclusive_scan(run, scratch, &wtot);
+#pragma unroll
+  for (int q = 0; q < IPT; ++q)
+    if (i0 + q < N) s_cum[i0 + q] = __dadd_rn(off, lw[q]);
 
-  // 4. sorted uniforms
+  // 4. this thread's sorted uniforms (resampling.py:21-26)
+  double u[IPT];
   if (MODE == 1) {
-    for (int i = tid; i < N; i += blockDim.x) s_u[i] = u_tape[base + i];
-    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? u_tape[base + i0 + q] : 2.0;
   } else {
     const Key2 key = load_key(keys, f);
-    for (int i = tid; i < N; i += blockDim.x) s_u[i] = spacing_exp(key, t, i);
-    __syncthreads();
-    const double cn1 = block_scan_inplace(s_u, N, 0.0, scratch);  // = c[N-1]
-    const double cN = __dadd_rn(cn1, spacing_exp(key, t, N));     // c[N]
-    for (int i = tid; i < N; i += blockDim.x) s_u[i] = __ddiv_rn(s_u[i], cN);
-    __syncthreads();
+    double erun = 0.0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      u[q] = i0 + q < N ? spacing_exp_fast(key, t, i0 + q) : 0.0;
+      erun = __dadd_rn(erun, u[q]);
+      u[q] = erun;
+    }
+    double etot;
+    const double eoff = block_exclusive_scan(erun, scratch, &etot);
+    const double cN = __dadd_rn(etot, spacing_exp_fast(key, t, N));  // c[N]
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __ddiv_rn(__dadd_rn(eoff, u[q]), cN) : 2.0;
   }
+  __syncthreads();  // s_cum complete
 
-  // 5. merge (searchsorted left + clamp)
-  for (int j = tid; j < N; j += blockDim.x) {
-    int k = lower_bound_f64(s_cum, N, s_u[j]);
-    if (k > N - 1) k = N - 1;
-    anc[base + j] = static_cast<int32_t>(base + k);
+  // 5. merge: searchsorted(cum, u, 'left') clamped to N-1 (accel.py:175-197)
+  if (i0 < N) {
+    int k = lower_bound_f64(s_cum, N, u[0]);
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      if (i0 + q < N) {
+        while (k < N && s_cum[k] < u[q]) ++k;
+        anc[base + i0 + q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+      }
+    }
   }
   if (tid == 0) {
     collapsed[f] = 0;
@@ -244,7 +312,7 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_sums(
   if (MODE == 0) key = load_key(keys, f);
   for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     pw = __dadd_rn(pw, __ddiv_rn(exp(__dsub_rn(load_lw(logw + f * N + i), m)), total));
-    if (MODE == 0) pe = __dadd_rn(pe, spacing_exp(key, t, i));
+    if (MODE == 0) pe = __dadd_rn(pe, spacing_exp_fast(key, t, i));
   }
   const double sw = block_sum(pw, scratch);
   const double se = MODE == 0 ? block_sum(pe, scratch) : 0.0;
@@ -326,10 +394,10 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_merge(
     __syncthreads();
   } else {
     const Key2 key = load_key(keys, f);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = spacing_exp(key, t, i0 + i);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = spacing_exp_fast(key, t, i0 + i);
     __syncthreads();
     block_scan_inplace(s, n, ws.teoff[tile], scratch);
-    const double cN = __dadd_rn(ws.cN[f], spacing_exp(key, t, N));
+    const double cN = __dadd_rn(ws.cN[f], spacing_exp_fast(key, t, N));
     for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = __ddiv_rn(s[i], cN);
     __syncthreads();
   }
@@ -353,8 +421,20 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
                            cudaStream_t s) {
   const TW *logw = static_cast<const TW *>(logw_v);
   if (N <= kBankMaxN) {
-    const size_t smem = 2 * static_cast<size_t>(N) * sizeof(double);
-    auto kern = u_tape ? resample_bank_kernel<TW, 1> : resample_bank_kernel<TW, 0>;
+    const size_t smem = static_cast<size_t>(N) * sizeof(double);
+    const int ipt = N <= 256 ? 1 : N <= 512 ? 2 : N <= 1024 ? 4 : N <= 2048 ? 8 : N <= 4096 ? 16 : 32;
+    auto pick = [&](auto tag) {
+      constexpr int I = decltype(tag)::value;
+      return u_tape ? resample_bank_kernel<TW, 1, I> : resample_bank_kernel<TW, 0, I>;
+    };
+    void (*kern)(const TW *, int32_t, const double *, const uint32_t *, uint32_t, int32_t *,
+                 double *, uint8_t *, uint32_t *) =
+        ipt == 1 ? pick(std::integral_constant<int, 1>{})
+        : ipt == 2 ? pick(std::integral_constant<int, 2>{})
+        : ipt == 4 ? pick(std::integral_constant<int, 4>{})
+        : ipt == 8 ? pick(std::integral_constant<int, 8>{})
+        : ipt == 16 ? pick(std::integral_constant<int, 16>{})
+                    : pick(std::integral_constant<int, 32>{});
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
