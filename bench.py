@@ -306,11 +306,9 @@ def run_resample(args, cfg):
     s = _lib.stream_ptr()
 
     def step(k):
-        _lib.call("pf_segmented_resample", _lib.PF_F32, _lib.ptr(logw), Ml, N, None,
+        _lib.call("pf_segmented_resample_gather", _lib.PF_F32, _lib.ptr(logw), Ml, N, None,
                   _lib.ptr(keys), k + 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll),
-                  _lib.ptr(st), _lib.ptr(ws), wsb, s)
-        _lib.call("pf_gather_planes", _lib.PF_F32, _lib.ptr(x_in), _lib.ptr(anc), MN, 3,
-                  _lib.ptr(x_out), s)
+                  _lib.ptr(st), _lib.ptr(ws), wsb, _lib.ptr(x_in), _lib.ptr(x_out), 3, s)
 
     for k in range(args.warmup):
         step(k)
@@ -331,7 +329,7 @@ def run_resample(args, cfg):
     achieved = MN * RESAMPLE_BYTES_PER_PARTICLE / per / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
-            "kernel": "pf_segmented_resample + pf_gather_planes (one step)",
+            "kernel": "pf_segmented_resample_gather (resample_bank_kernel with fused gather)",
             "algorithmic": f"{RESAMPLE_BYTES_PER_PARTICLE:.0f} B/particle x {MN} particles",
             "traffic": _ncu_traffic(args.config)}
     # e2e: host logw in (pinned), host ancestors out, through the C ABI
@@ -357,7 +355,7 @@ def run_resample(args, cfg):
                 "roofline": roof, "cpu_baseline": cb,
                 "e2e": {"value": M * N * args.steps / e2e_s, "unit": "particles/s",
                         "h2d_bytes_per_step": MN * 4, "d2h_bytes_per_step": MN * 4},
-                "gpu_launches": (2 if N <= 8192 else 10) * args.steps,
+                "gpu_launches": (1 if N <= 8192 else 10) * args.steps,
                 "clocks": clocks.summary()}
         print(json.dumps(line))
     return 0

@@ -70,6 +70,9 @@ SIGNATURES = {
     "pf_resample_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "pf_segmented_resample": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_u32,
                                              c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "pf_segmented_resample_gather": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
+                                                    c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
+                                                    c_vp, c_vp, c_i32, c_vp]),
     "pf_filter_estimate": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64,
                                           c_i64, c_vp, c_vp]),
     "pf_ensemble_average": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),

@@ -83,16 +83,37 @@ __device__ __forceinline__ double block_exclusive_scan(double v, double *scratch
 
 // ---- bank path: one CTA per filter --------------------------------------
 // Thread t owns the IPT consecutive particles [t*IPT, t*IPT+IPT): weights,
-// CDF and sorted uniforms live in registers, the per-thread sums are
-// combined with one block scan, and only the CDF goes to shared memory for
-// the merge (binary search for the thread's first uniform, then a forward
-// walk over its sorted run).
-template <typename TW, int MODE, int IPT>
-__global__ void __launch_bounds__(kBankThreads) resample_bank_kernel(
+// CDF and sorted uniforms live in registers, per-thread sums are combined
+// with one block scan, and only the CDF goes to shared memory for the merge
+// (binary search for the thread's first uniform, then a forward walk over
+// its sorted run).  Shared CDF layout is "thread-major" (element i at
+// (i % IPT) * THREADS + i / IPT) so the per-thread stores are conflict-free.
+// GATHER fuses the ancestor gather of a fp32 planar state (cfg1).
+template <int THREADS, int IPT>
+__device__ __forceinline__ int cdf_slot(int i) {
+  return (i % IPT) * THREADS + i / IPT;
+}
+
+template <int THREADS, int IPT>
+__device__ __forceinline__ int lower_bound_tm(const double *c, int n, double x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (c[cdf_slot<THREADS, IPT>(mid)] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <typename TW, int MODE, int THREADS, int IPT, bool GATHER>
+__global__ void __launch_bounds__(THREADS) resample_bank_kernel(
     const TW *__restrict__ logw, int32_t N, const double *__restrict__ u_tape,
     const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
-    double *__restrict__ lnc, uint8_t *__restrict__ collapsed, uint32_t *__restrict__ status) {
-  extern __shared__ double s_cum[];  // N
+    double *__restrict__ lnc, uint8_t *__restrict__ collapsed, uint32_t *__restrict__ status,
+    const float *__restrict__ gx_in, float *__restrict__ gx_out, int gdims, int64_t gMN) {
+  extern __shared__ double s_cum[];  // THREADS * IPT slots, thread-major
   __shared__ double scratch[33];
   const int tid = threadIdx.x;
   const int64_t f = blockIdx.x;
@@ -103,10 +124,28 @@ __global__ void __launch_bounds__(kBankThreads) resample_bank_kernel(
   double lw[IPT];
   double mx = -INFINITY;
   int nan = 0;
+  // VEC: whole runs in range and 16-byte aligned -> vector loads/stores
+  // (fully coalesced: consecutive lanes own consecutive runs)
+  const bool vec = (IPT % 4 == 0) && (N % IPT == 0) && sizeof(TW) == 4 && ((base & 3) == 0);
+  if (vec && i0 < N) {
+#pragma unroll
+    for (int q = 0; q < IPT; q += 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(logw + base + i0 + q));
+      lw[q] = v.x;
+      lw[q + 1] = v.y;
+      lw[q + 2] = v.z;
+      lw[q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      const int i = i0 + q;
+      lw[q] = i < N ? static_cast<double>(__ldg(logw + base + i)) : -INFINITY;
+    }
+  }
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
-    const int i = i0 + q;
-    lw[q] = i < N ? static_cast<double>(logw[base + i]) : -INFINITY;
+    if (i0 + q >= N) lw[q] = -INFINITY;
     nan |= isnan(lw[q]);
     mx = fmax(mx, lw[q]);
   }
@@ -115,7 +154,11 @@ __global__ void __launch_bounds__(kBankThreads) resample_bank_kernel(
   if (nan || m == -INFINITY) {
     // NaN -> ValueError on the host; total underflow -> collapse: identity
     // ancestors, lnc unchanged (filters.py:105-109)
-    for (int i = tid; i < N; i += blockDim.x) anc[base + i] = static_cast<int32_t>(base + i);
+    for (int i = tid; i < N; i += blockDim.x) {
+      anc[base + i] = static_cast<int32_t>(base + i);
+      if (GATHER)
+        for (int d = 0; d < gdims; ++d) gx_out[d * gMN + base + i] = gx_in[d * gMN + base + i];
+    }
     if (tid == 0) {
       collapsed[f] = nan ? 0 : 1;
       if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
@@ -132,50 +175,87 @@ __global__ void __launch_bounds__(kBankThreads) resample_bank_kernel(
   }
   const double total = block_sum(part, scratch);
 
-  // 3. w = e / total, CDF = thread offset + running local sum
+  // 3. w = e / total (IEEE division, core.py:136), CDF = offset + local run
   double run = 0.0;
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
-    lw[q] = __ddiv_rn(lw[q], total);
-    run = __dadd_rn(run, lw[q]);
+    run = __dadd_rn(run, __ddiv_rn(lw[q], total));
     lw[q] = run;  // local inclusive prefix
   }
   double wtot;
   const double off = block_exclusive_scan(run, scratch, &wtot);
 #pragma unroll
   for (int q = 0; q < IPT; ++q)
-    if (i0 + q < N) s_cum[i0 + q] = __dadd_rn(off, lw[q]);
+    if (i0 + q < N) s_cum[q * THREADS + tid] = __dadd_rn(off, lw[q]);
 
   // 4. this thread's sorted uniforms (resampling.py:21-26)
   double u[IPT];
   if (MODE == 1) {
 #pragma unroll
-    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? u_tape[base + i0 + q] : 2.0;
+    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __ldg(u_tape + base + i0 + q) : 2.0;
   } else {
     const Key2 key = load_key(keys, f);
     double erun = 0.0;
 #pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-      u[q] = i0 + q < N ? spacing_exp_fast(key, t, i0 + q) : 0.0;
-      erun = __dadd_rn(erun, u[q]);
-      u[q] = erun;
+    for (int q = 0; q < IPT; q += 4) {
+      const uint4 r = philox10(make_uint4(static_cast<uint32_t>((i0 + q) >> 2), t, 0u,
+                                          kPurposeResample),
+                               key);
+      const uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int h = 0; h < 4 && q + h < IPT; ++h) {
+        const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
+        erun = __dadd_rn(erun, e);
+        u[q + h] = erun;
+      }
     }
     double etot;
     const double eoff = block_exclusive_scan(erun, scratch, &etot);
     const double cN = __dadd_rn(etot, spacing_exp_fast(key, t, N));  // c[N]
+    const double inv = 1.0 / cN;  // production draws: reciprocal multiply
 #pragma unroll
-    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __ddiv_rn(__dadd_rn(eoff, u[q]), cN) : 2.0;
+    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __dadd_rn(eoff, u[q]) * inv : 2.0;
   }
   __syncthreads();  // s_cum complete
 
   // 5. merge: searchsorted(cum, u, 'left') clamped to N-1 (accel.py:175-197)
   if (i0 < N) {
-    int k = lower_bound_f64(s_cum, N, u[0]);
+    int k = lower_bound_tm<THREADS, IPT>(s_cum, N, u[0]);
+    int32_t av[IPT];
 #pragma unroll
     for (int q = 0; q < IPT; ++q) {
       if (i0 + q < N) {
-        while (k < N && s_cum[k] < u[q]) ++k;
-        anc[base + i0 + q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+        while (k < N && s_cum[cdf_slot<THREADS, IPT>(k)] < u[q]) ++k;
+        av[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+      } else {
+        av[q] = 0;
+      }
+    }
+    if (vec) {
+#pragma unroll
+      for (int q = 0; q < IPT; q += 4)
+        *reinterpret_cast<int4 *>(anc + base + i0 + q) =
+            make_int4(av[q], av[q + 1], av[q + 2], av[q + 3]);
+      if (GATHER) {
+        for (int d = 0; d < gdims; ++d) {
+          const float *src = gx_in + d * gMN;
+          float *dst = gx_out + d * gMN + base + i0;
+#pragma unroll
+          for (int q = 0; q < IPT; q += 4)
+            *reinterpret_cast<float4 *>(dst + q) =
+                make_float4(__ldg(src + av[q]), __ldg(src + av[q + 1]), __ldg(src + av[q + 2]),
+                            __ldg(src + av[q + 3]));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < IPT; ++q) {
+        if (i0 + q < N) {
+          anc[base + i0 + q] = av[q];
+          if (GATHER)
+            for (int d = 0; d < gdims; ++d)
+              gx_out[d * gMN + base + i0 + q] = __ldg(gx_in + d * gMN + av[q]);
+        }
       }
     }
   }
@@ -414,32 +494,51 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_merge(
   }
 }
 
+__global__ void wide_gather_kernel(const float *__restrict__ xin, const int32_t *__restrict__ anc,
+                                   int64_t MN, int dims, float *__restrict__ xout) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= MN) return;
+  const int64_t a = __ldg(anc + p);
+  for (int d = 0; d < dims; ++d) xout[d * MN + p] = __ldg(xin + d * MN + a);
+}
+
 template <typename TW>
 static int launch_resample(const void *logw_v, int64_t M, int64_t N, const double *u_tape,
                            const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
                            uint8_t *collapsed, uint32_t *status, void *ws_v, size_t ws_bytes,
-                           cudaStream_t s) {
+                           cudaStream_t s, const float *gx_in = nullptr,
+                           float *gx_out = nullptr, int gdims = 0) {
   const TW *logw = static_cast<const TW *>(logw_v);
   if (N <= kBankMaxN) {
-    const size_t smem = static_cast<size_t>(N) * sizeof(double);
-    const int ipt = N <= 256 ? 1 : N <= 512 ? 2 : N <= 1024 ? 4 : N <= 2048 ? 8 : N <= 4096 ? 16 : 32;
-    auto pick = [&](auto tag) {
-      constexpr int I = decltype(tag)::value;
-      return u_tape ? resample_bank_kernel<TW, 1, I> : resample_bank_kernel<TW, 0, I>;
-    };
-    void (*kern)(const TW *, int32_t, const double *, const uint32_t *, uint32_t, int32_t *,
-                 double *, uint8_t *, uint32_t *) =
-        ipt == 1 ? pick(std::integral_constant<int, 1>{})
-        : ipt == 2 ? pick(std::integral_constant<int, 2>{})
-        : ipt == 4 ? pick(std::integral_constant<int, 4>{})
-        : ipt == 8 ? pick(std::integral_constant<int, 8>{})
-        : ipt == 16 ? pick(std::integral_constant<int, 16>{})
-                    : pick(std::integral_constant<int, 32>{});
+    using K = void (*)(const TW *, int32_t, const double *, const uint32_t *, uint32_t, int32_t *,
+                       double *, uint8_t *, uint32_t *, const float *, float *, int, int64_t);
+    K kern;
+    int threads;
+    const bool g = gx_in != nullptr;
+#define PF_PICK(TH, I)                                                                        \
+  {                                                                                           \
+    threads = TH;                                                                             \
+    kern = u_tape ? (g ? resample_bank_kernel<TW, 1, TH, I, true>                             \
+                       : resample_bank_kernel<TW, 1, TH, I, false>)                           \
+                  : (g ? resample_bank_kernel<TW, 0, TH, I, true>                             \
+                       : resample_bank_kernel<TW, 0, TH, I, false>);                          \
+  }
+    if (N <= 256) PF_PICK(128, 2)
+    else if (N <= 512) PF_PICK(128, 4)
+    else if (N <= 1024) PF_PICK(128, 8)
+    else if (N <= 2048) PF_PICK(256, 8)
+    else if (N <= 4096) PF_PICK(256, 16)
+    else PF_PICK(512, 16)
+#undef PF_PICK
+    // thread-major CDF slots: THREADS * IPT doubles (>= N)
+    const int ipt = N <= 256 ? 2 : N <= 512 ? 4 : N <= 1024 ? 8 : N <= 2048 ? 8 : 16;
+    const size_t smem = static_cast<size_t>(threads) * ipt * sizeof(double);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-    kern<<<static_cast<unsigned>(M), kBankThreads, smem, s>>>(
-        logw, static_cast<int32_t>(N), u_tape, keys, t, anc, lnc, collapsed, status);
+    kern<<<static_cast<unsigned>(M), threads, smem, s>>>(logw, static_cast<int32_t>(N), u_tape,
+                                                         keys, t, anc, lnc, collapsed, status,
+                                                         gx_in, gx_out, gdims, M * N);
     return check_launch("pf_segmented_resample(bank)");
   }
   WideWs ws;
@@ -463,6 +562,8 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
     wide_tile_merge<1><<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc);
   else
     wide_tile_merge<0><<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc);
+  if (gx_in)
+    wide_gather_kernel<<<grid_for(M * N, 256), 256, 0, s>>>(gx_in, anc, M * N, gdims, gx_out);
   return check_launch("pf_segmented_resample(wide)");
 }
 
@@ -538,6 +639,24 @@ int pf_segmented_resample(pf_dtype logw_dtype, const void *logw, int64_t M, int6
                                    ws, ws_bytes, s);
   return launch_resample<float>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status, ws,
                                 ws_bytes, s);
+}
+
+int pf_segmented_resample_gather(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
+                                 const double *u_tape, const uint32_t *keys, uint32_t t,
+                                 int32_t *anc_out, double *lnc, uint8_t *collapsed,
+                                 uint32_t *status, void *ws, size_t ws_bytes,
+                                 const float *x_in, float *x_out, int32_t dims, void *stream) {
+  PF_REQUIRE(logw && anc_out && lnc && collapsed && status && x_in && x_out && dims >= 1,
+             "pf_segmented_resample_gather: null / bad arguments");
+  PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_segmented_resample_gather: bad M/N");
+  PF_REQUIRE(u_tape || keys, "pf_segmented_resample_gather: need keys (Philox) or u_tape");
+  PF_REQUIRE(x_in != x_out, "pf_segmented_resample_gather: x_in and x_out must not alias");
+  const cudaStream_t s = as_stream(stream);
+  if (logw_dtype == PF_F64)
+    return launch_resample<double>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status,
+                                   ws, ws_bytes, s, x_in, x_out, dims);
+  return launch_resample<float>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status, ws,
+                                ws_bytes, s, x_in, x_out, dims);
 }
 
 int pf_op_normalize_log_weights(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,

@@ -382,3 +382,25 @@ def test_philox_filter_tracks_truth():
     out = pf.run_ensemble(gm, obs, "bootstrap", 4, 1000, 1)
     mse = np.mean((out.mean_estimates - states) ** 2)
     assert mse < 2.0, mse
+
+
+@pytest.mark.parametrize("M,N", [(64, 1024), (2, 20000)])
+def test_resample_gather_fused_matches_unfused(M, N):
+    lw, u = _resample_case(M, N, 1.0, seed=5)
+    anc_ref, _, _ = _gpu_resample(lw, u)
+    d_lw = torch.from_numpy(lw.reshape(-1)).cuda()
+    d_u = torch.from_numpy(u.reshape(-1)).cuda()
+    x = torch.randn((3, M * N), device="cuda")
+    xo = torch.empty_like(x)
+    anc = torch.empty(M * N, dtype=torch.int32, device="cuda")
+    lnc = torch.zeros(M, dtype=torch.float64, device="cuda")
+    coll = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    st = torch.zeros(M, dtype=torch.int32, device="cuda")
+    wsb = _lib.load().pf_resample_workspace_bytes(M, N)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    _lib.call("pf_segmented_resample_gather", _lib.PF_F32, _lib.ptr(d_lw), M, N, _lib.ptr(d_u),
+              None, 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st), _lib.ptr(ws),
+              wsb, _lib.ptr(x), _lib.ptr(xo), 3, _lib.stream_ptr())
+    a = anc.cpu().numpy().astype(np.int64)
+    assert np.array_equal(a.reshape(M, N) - (np.arange(M) * N)[:, None], anc_ref)
+    assert torch.equal(xo, x[:, anc.long()])
