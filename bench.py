@@ -306,9 +306,9 @@ def run_resample(args, cfg):
     s = _lib.stream_ptr()
 
     def step(k):
-        _lib.call("pf_segmented_resample_gather", _lib.PF_F32, _lib.ptr(logw), Ml, N, None,
+        _lib.call("pf_segmented_resample_ex", _lib.PF_F32, _lib.ptr(logw), Ml, N, None,
                   _lib.ptr(keys), k + 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll),
-                  _lib.ptr(st), _lib.ptr(ws), wsb, _lib.ptr(x_in), _lib.ptr(x_out), 3, s)
+                  _lib.ptr(st), _lib.ptr(ws), wsb, _lib.ptr(x_in), _lib.ptr(x_out), 3, 0, s)
 
     for k in range(args.warmup):
         step(k)
@@ -329,7 +329,7 @@ def run_resample(args, cfg):
     achieved = MN * RESAMPLE_BYTES_PER_PARTICLE / per / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
-            "kernel": "pf_segmented_resample_gather (resample_bank_kernel with fused gather)",
+            "kernel": "pf_segmented_resample_ex (resample_bank_kernel with fused gather)",
             "algorithmic": f"{RESAMPLE_BYTES_PER_PARTICLE:.0f} B/particle x {MN} particles",
             "traffic": _ncu_traffic(args.config)}
     # e2e: host logw in (pinned), host ancestors out, through the C ABI

@@ -165,14 +165,19 @@ int pf_segmented_resample(pf_dtype logw_dtype, const void *logw, int64_t M, int6
                           int32_t *anc_out, double *lnc, uint8_t *collapsed, uint32_t *status,
                           void *ws, size_t ws_bytes, void *stream);
 
-/* pf_segmented_resample with the ancestor gather of a planar fp32 state
- * fused in (filters.py:111 / BASELINE cfg1): x_out[d][p] = x_in[d][anc[p]],
- * d < dims, planes of M*N floats. */
-int pf_segmented_resample_gather(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
-                                 const double *u_tape, const uint32_t *keys, uint32_t t,
-                                 int32_t *anc_out, double *lnc, uint8_t *collapsed,
-                                 uint32_t *status, void *ws, size_t ws_bytes,
-                                 const float *x_in, float *x_out, int32_t dims, void *stream);
+/* pf_segmented_resample with options (filters.py:111, resampling.py:29-43):
+ *  - x_in/x_out/dims (nullable): fused ancestor gather of a planar fp32 state,
+ *    x_out[d][p] = x_in[d][anc[p]] (BASELINE cfg1);
+ *  - flags & PF_RS_REFERENCE_ORDER: build the CDF in the reference's exact
+ *    floating-point order (numpy pairwise sum for the total, IEEE division,
+ *    strictly sequential cumsum) so ancestors are bit-identical to the
+ *    reference's for identical uniforms (oracle mode; slower). */
+#define PF_RS_REFERENCE_ORDER 1u
+int pf_segmented_resample_ex(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
+                             const double *u_tape, const uint32_t *keys, uint32_t t,
+                             int32_t *anc_out, double *lnc, uint8_t *collapsed, uint32_t *status,
+                             void *ws, size_t ws_bytes, const float *x_in, float *x_out,
+                             int32_t dims, uint32_t flags, void *stream);
 
 /* posterior_mean of the resampled set (core.py:154-156 via filters.py:188):
  * est[f*dim + d] = (1/N) * sum_j x(anc[f*N+j], d) in a fixed order, fp64,

@@ -24,6 +24,7 @@ PF_EINVAL = -22
 PF_ECUDA = -5
 PF_ST_DIVERGED = 1
 PF_ST_NAN_WEIGHT = 2
+PF_RS_REFERENCE_ORDER = 1
 PF_F32 = 0
 PF_F64 = 1
 
@@ -70,9 +71,9 @@ SIGNATURES = {
     "pf_resample_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "pf_segmented_resample": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_u32,
                                              c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
-    "pf_segmented_resample_gather": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
-                                                    c_u32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
-                                                    c_vp, c_vp, c_i32, c_vp]),
+    "pf_segmented_resample_ex": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_u32,
+                                                c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp,
+                                                c_i32, c_u32, c_vp]),
     "pf_filter_estimate": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64,
                                           c_i64, c_vp, c_vp]),
     "pf_ensemble_average": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),

@@ -56,7 +56,8 @@ class FilterBank:
 
     def __init__(self, model, n_filters: int, n_particles: int, keys, n_steps: int, *,
                  dtype=None, tape: DrawTape | None = None, filter_offset: int = 0,
-                 estimate: str = "full", est_buffer=None, est_row_offset: int = 0):
+                 estimate: str = "full", est_buffer=None, est_row_offset: int = 0,
+                 reference_order: bool = True):
         import torch
 
         _lib.require_cuda()
@@ -114,6 +115,9 @@ class FilterBank:
         self.cur = 0
         self.steps_done = 0
         self.kernel_events = None  # optional (start, end) CUDA events around propagate
+        # oracle mode builds the CDF in the reference's exact order (bit-exact
+        # ancestors); production mode uses the parallel scan
+        self.rs_flags = _lib.PF_RS_REFERENCE_ORDER if (tape is not None and reference_order) else 0
 
     # -- setup ----------------------------------------------------------------
     def load_observations(self, observations):
@@ -190,10 +194,10 @@ class FilterBank:
                       _lib.ptr(self.status), s)
         if self.kernel_events is not None:
             self.kernel_events[1].record()
-        _lib.call("pf_segmented_resample", self.code, _lib.ptr(self.logw), self.M, self.N,
+        _lib.call("pf_segmented_resample_ex", self.code, _lib.ptr(self.logw), self.M, self.N,
                   _lib.ptr(uni), _lib.ptr(self.keys), t, _lib.ptr(self.anc), _lib.ptr(self.lnc),
                   _lib.ptr(self.collapsed), _lib.ptr(self.status), _lib.ptr(self.ws),
-                  self.ws_bytes, s)
+                  self.ws_bytes, None, None, 0, self.rs_flags, s)
         est_ptr = _lib.c_vp(self.est[k].data_ptr() + self.est_row * self.est_dim * 8)
         sp, sd = self.est_strides
         _lib.call("pf_filter_estimate", self.code, _lib.ptr(xout), sp, sd, self.est_dim,

@@ -250,7 +250,10 @@ struct FhnFast {
 // Lattice geometry is compile-time (ROWS x COLS, R rows per thread) so every
 // shared-memory access is base register + immediate.  TAPE=true reads the
 // standard normals from an fp64 tape (parity tests of this exact kernel).
-template <int ROWS, int COLS, int R, bool TAPE, int MINB>
+// PP particles are advanced together by the same threads (independent
+// dependency chains -> more ILP per warp, one barrier per Euler step for
+// all PP particles).
+template <int ROWS, int COLS, int R, bool TAPE, int MINB, int PP>
 __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
     const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
@@ -261,9 +264,9 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
   constexpr int NSEG = (ROWS + R - 1) / R;
   constexpr int NODES = ROWS * COLS;
   static_assert(R % 2 == 0, "rows per thread must be even (Philox row pairs)");
-  extern __shared__ __align__(16) float vsp[];  // [2][P]
-  __shared__ double red[1];
-  __shared__ int bad;
+  extern __shared__ __align__(16) float vsp[];  // [PP][2][P]
+  __shared__ double red[PP];
+  __shared__ int bad[PP];
   const int tid = threadIdx.x;
   const int seg = tid / COLS;
   const int col = tid - seg * COLS;
@@ -273,84 +276,97 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
   const int hg = col == 0 ? -1 : (col == COLS - 1 ? 1 : 0);
   const int base = (row0 + 1) * W + col + 1;  // this thread's first cell
 
-  for (int64_t p = blockIdx.x; p < MN; p += gridDim.x) {
-    const int64_t f = p / N;
-    const uint32_t j = static_cast<uint32_t>(p - f * N);
-    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
-    const float *xs = xin + src * 2 * static_cast<int64_t>(NODES);
-    if (tid == 0) bad = 0;
-    float v[R], w[R];
+  for (int64_t pb = static_cast<int64_t>(blockIdx.x) * PP; pb < MN;
+       pb += static_cast<int64_t>(gridDim.x) * PP) {
+    float v[PP][R], w[PP][R];
+    int64_t fe[PP];
+    uint32_t je[PP];
+    Key2 key[PP];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      v[r] = 0.f;
-      w[r] = 0.f;
-      if (active && row0 + r < ROWS) {
-        const int node = (row0 + r) * COLS + col;
-        v[r] = __ldg(xs + node);
-        w[r] = __ldg(xs + NODES + node);
-        float *cell = vsp + base + r * W;
-        cell[0] = v[r];
-        cell[hg] = v[r];
-        if (r == 0 && row0 == 0) cell[-W] = v[r];
-        if (row0 + r == ROWS - 1) cell[W] = v[r];
+    for (int e = 0; e < PP; ++e) {
+      const int64_t p = pb + e < MN ? pb + e : MN - 1;  // tail: recompute the last (no store)
+      fe[e] = p / N;
+      je[e] = static_cast<uint32_t>(p - fe[e] * N);
+      const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+      const float *xs = xin + src * 2 * static_cast<int64_t>(NODES);
+      if (tid == 0) bad[e] = 0;
+      key[e] = Key2{0u, 0u};
+      if (!TAPE) key[e] = load_key(keys, fe[e]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        v[e][r] = 0.f;
+        w[e][r] = 0.f;
+        if (active && row0 + r < ROWS) {
+          const int node = (row0 + r) * COLS + col;
+          v[e][r] = __ldg(xs + node);
+          w[e][r] = __ldg(xs + NODES + node);
+          float *cell = vsp + e * 2 * P + base + r * W;
+          cell[0] = v[e][r];
+          cell[hg] = v[e][r];
+          if (r == 0 && row0 == 0) cell[-W] = v[e][r];
+          if (row0 + r == ROWS - 1) cell[W] = v[e][r];
+        }
       }
     }
     __syncthreads();
 
-    Key2 key{0u, 0u};
-    if (!TAPE) key = load_key(keys, f);
     // Philox normals come out of box_muller_fast_unscaled: fold sqrt(2 ln 2)
     const float sv = TAPE ? c.sig_v : c.sig_v * kSqrt2Ln2;
     const float sw = TAPE ? c.sig_w : c.sig_w * kSqrt2Ln2;
     const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
     for (int k = 0; k < c.n_sub; ++k) {
-      const float *cur = vsp + (k & 1) * P + base;
-      float *nxt = vsp + ((k & 1) ^ 1) * P + base;
       if (active) {
-        float up = cur[-W];  // old value of the row above this strip
 #pragma unroll
-        for (int q = 0; q < R / 2; ++q) {
-          float zv0, zw0, zv1, zw1;
-          if (TAPE) {
-            const int64_t b0 = ((f * c.n_sub + k) * 2 * static_cast<int64_t>(N) + j) * NODES +
-                               (row0 + 2 * q) * COLS + col;
-            const int64_t wo = static_cast<int64_t>(N) * NODES;
-            const bool ok1 = row0 + 2 * q + 1 < ROWS;
-            zv0 = float(tape[b0]);
-            zw0 = float(tape[b0 + wo]);
-            zv1 = ok1 ? float(tape[b0 + COLS]) : 0.f;
-            zw1 = ok1 ? float(tape[b0 + wo + COLS]) : 0.f;
-          } else {
-            const uint32_t node_pair = static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col);
-            const uint4 rr = philox10(make_uint4(j, step0 + k, node_pair, kPurposeFhn), key);
-            const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
-            const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
-            zv0 = g0.x;
-            zw0 = g0.y;
-            zv1 = g1.x;
-            zw1 = g1.y;
-          }
+        for (int e = 0; e < PP; ++e) {
+          const float *cur = vsp + e * 2 * P + (k & 1) * P + base;
+          float *nxt = vsp + e * 2 * P + ((k & 1) ^ 1) * P + base;
+          float up = cur[-W];  // old value of the row above this strip
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = 2 * q + h;
-            if (row0 + r < ROWS) {
-              const float *cell = cur + r * W;
-              const float u = v[r];
-              const float dn = (r < R - 1 && row0 + r + 1 < ROWS) ? v[r + 1] : cell[W];
-              const float nb = ((up + dn) + cell[-1]) + cell[1];
-              const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
-              // u + dt(p3 - w) + dt*coupling*(nb - 4u) + sig_v*zv
-              float un = fmaf(c.dt, p3 - w[r], u);
-              un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
-              un = fmaf(sv, h ? zv1 : zv0, un);
-              w[r] = fmaf(sw, h ? zw1 : zw0, fmaf(c.wc, w[r], fmaf(c.uc, u, c.c0)));
-              float *dst = nxt + r * W;
-              dst[0] = un;
-              dst[hg] = un;
-              if (r == 0 && row0 == 0) dst[-W] = un;
-              if (row0 + r == ROWS - 1) dst[W] = un;
-              up = u;
-              v[r] = un;
+          for (int q = 0; q < R / 2; ++q) {
+            float zv0, zw0, zv1, zw1;
+            if (TAPE) {
+              const int64_t b0 =
+                  ((fe[e] * c.n_sub + k) * 2 * static_cast<int64_t>(N) + je[e]) * NODES +
+                  (row0 + 2 * q) * COLS + col;
+              const int64_t wo = static_cast<int64_t>(N) * NODES;
+              const bool ok1 = row0 + 2 * q + 1 < ROWS;
+              zv0 = float(tape[b0]);
+              zw0 = float(tape[b0 + wo]);
+              zv1 = ok1 ? float(tape[b0 + COLS]) : 0.f;
+              zw1 = ok1 ? float(tape[b0 + wo + COLS]) : 0.f;
+            } else {
+              const uint32_t node_pair = static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col);
+              const uint4 rr =
+                  philox10(make_uint4(je[e], step0 + k, node_pair, kPurposeFhn), key[e]);
+              const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
+              const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
+              zv0 = g0.x;
+              zw0 = g0.y;
+              zv1 = g1.x;
+              zw1 = g1.y;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int r = 2 * q + h;
+              if (row0 + r < ROWS) {
+                const float *cell = cur + r * W;
+                const float u = v[e][r];
+                const float dn = (r < R - 1 && row0 + r + 1 < ROWS) ? v[e][r + 1] : cell[W];
+                const float nb = ((up + dn) + cell[-1]) + cell[1];
+                const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
+                // u + dt(p3 - w) + dt*coupling*(nb - 4u) + sig_v*zv
+                float un = fmaf(c.dt, p3 - w[e][r], u);
+                un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
+                un = fmaf(sv, h ? zv1 : zv0, un);
+                w[e][r] = fmaf(sw, h ? zw1 : zw0, fmaf(c.wc, w[e][r], fmaf(c.uc, u, c.c0)));
+                float *dst = nxt + r * W;
+                dst[0] = un;
+                dst[hg] = un;
+                if (r == 0 && row0 == 0) dst[-W] = un;
+                if (row0 + r == ROWS - 1) dst[W] = un;
+                up = u;
+                v[e][r] = un;
+              }
             }
           }
         }
@@ -359,22 +375,28 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
     }
 
     // epilogue: divergence flag, store, electrode log-likelihood
-    bool fin = true;
-    float *xd = xout + p * 2 * static_cast<int64_t>(NODES);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (active && row0 + r < ROWS) {
-        const int node = (row0 + r) * COLS + col;
-        fin = fin && isfinite(v[r]) && isfinite(w[r]);
-        xd[node] = v[r];
-        xd[NODES + node] = w[r];
+    for (int e = 0; e < PP; ++e) {
+      if (pb + e >= MN) continue;
+      const int64_t p = pb + e;
+      bool fin = true;
+      float *xd = xout + p * 2 * static_cast<int64_t>(NODES);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (active && row0 + r < ROWS) {
+          const int node = (row0 + r) * COLS + col;
+          fin = fin && isfinite(v[e][r]) && isfinite(w[e][r]);
+          xd[node] = v[e][r];
+          xd[NODES + node] = w[e][r];
+        }
       }
+      if (!fin) bad[e] = 1;
     }
-    if (!fin) bad = 1;
-    if (tid < 32) {
-      const float *fv = vsp + (c.n_sub & 1) * P;
+    if (tid < 32 * PP) {
+      const int e = tid >> 5, lane = tid & 31;
+      const float *fv = vsp + e * 2 * P + (c.n_sub & 1) * P;
       double acc = 0.0;
-      for (int i = tid; i < c.n_obs; i += 32) {
+      for (int i = lane; i < c.n_obs; i += 32) {
         const int n = __ldg(obs_idx + i);
         const int rr = n / COLS;
         const double rsd = __ldg(y + i) - static_cast<double>(fv[(rr + 1) * W + (n - rr * COLS) + 1]);
@@ -382,12 +404,12 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-      if (tid == 0) red[0] = acc;
+      if (lane == 0) red[e] = acc;
     }
     __syncthreads();
-    if (tid == 0) {
-      logw[p] = static_cast<float>(c.obs_coef * red[0]);
-      if (bad) atomicOr(status + f, PF_ST_DIVERGED);
+    if (tid < PP && pb + tid < MN) {
+      logw[pb + tid] = static_cast<float>(c.obs_coef * red[tid]);
+      if (bad[tid]) atomicOr(status + fe[tid], PF_ST_DIVERGED);
     }
     __syncthreads();
   }
@@ -469,7 +491,7 @@ static int launch_fhn(const FhnConsts &c, const void *x_in, const int32_t *anc, 
   return check_launch("pf_fhn_interval");
 }
 
-template <int ROWS, int COLS, bool TAPE, int MINB>
+template <int ROWS, int COLS, bool TAPE, int MINB, int PP>
 static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
                              const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                              int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
@@ -477,8 +499,8 @@ static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t 
   constexpr int R = kFhnRows;
   constexpr int threads = (((ROWS + R - 1) / R * COLS) + 31) / 32 * 32;
   static_assert(threads <= 256, "lattice too large for the fast kernel");
-  const size_t smem = 2 * static_cast<size_t>((ROWS + 2) * (COLS + 2)) * sizeof(float);
-  auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE, MINB>;
+  const size_t smem = PP * 2 * static_cast<size_t>((ROWS + 2) * (COLS + 2)) * sizeof(float);
+  auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE, MINB, PP>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int per_sm = 0;
@@ -487,7 +509,8 @@ static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t 
   int sms = kSmCount, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t grid = std::min<int64_t>(MN, static_cast<int64_t>(sms) * per_sm);
+  const int64_t grid =
+      std::min<int64_t>((MN + PP - 1) / PP, static_cast<int64_t>(sms) * per_sm);
   kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(
       static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
       static_cast<float *>(logw), MN, N, fc, keys, t, tape, status);
@@ -632,6 +655,159 @@ static int launch_fhn_warp_t(const FhnFast &fc, const void *x_in, const int32_t 
   return check_launch("pf_fhn_interval(warp)");
 }
 
+// ---- warp-pair-per-particle variant ---------------------------------------
+// Two warps own one particle: lane r of warp h holds row r, columns
+// [h*HC, h*HC+HC) in registers.  Vertical neighbours come from __shfl_sync
+// with clamped source lanes (= the ghost = self Neumann boundary),
+// horizontal ones from the lane's own registers; only the two columns at the
+// half boundary cross warps, through a double-buffered shared slot and one
+// 64-thread named barrier per Euler step.  No shared-memory stencil, no
+// CTA-wide barrier.
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int ROWS, int COLS, bool TAPE>
+__global__ void __launch_bounds__(128, 4) fhn_pair_kernel(
+    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
+    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
+    int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
+    const double *__restrict__ tape, uint32_t *__restrict__ status) {
+  static_assert(ROWS <= 32 && COLS % 2 == 0, "pair kernel: ROWS <= 32, even COLS");
+  constexpr int HC = COLS / 2;          // columns per warp
+  constexpr int NQ = (HC + 1) / 2;      // Philox blocks per lane per step
+  constexpr int NODES = ROWS * COLS;
+  constexpr int PPB = 2;                // particles per block (4 warps)
+  __shared__ float bnd[PPB][2][2][32];  // [pair][buffer][half][lane]
+  __shared__ __align__(16) float plane[PPB][NODES];
+  __shared__ int bad[PPB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pr = warp >> 1, half = warp & 1;
+  const int row = lane < ROWS ? lane : ROWS - 1;  // spare lanes shadow the last row
+  const int src_up = row > 0 ? row - 1 : 0;        // clamp = ghost = self
+  const int src_dn = row < ROWS - 1 ? row + 1 : ROWS - 1;
+  const int c0 = half * HC;
+  const int bar_id = 1 + pr;
+  const int64_t npairs = static_cast<int64_t>(gridDim.x) * PPB;
+
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * PPB + pr; p < MN; p += npairs) {
+    const int64_t f = p / N;
+    const uint32_t j = static_cast<uint32_t>(p - f * N);
+    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+    const float *xs = xin + src * 2 * static_cast<int64_t>(NODES) + row * COLS + c0;
+    float v[HC], w[HC];
+#pragma unroll
+    for (int q = 0; q < HC; ++q) {
+      v[q] = __ldg(xs + q);
+      w[q] = __ldg(xs + NODES + q);
+    }
+    Key2 key{0u, 0u};
+    if (!TAPE) key = load_key(keys, f);
+    const float sv = TAPE ? c.sig_v : c.sig_v * kSqrt2Ln2;
+    const float sw = TAPE ? c.sig_w : c.sig_w * kSqrt2Ln2;
+    const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
+    for (int k = 0; k < c.n_sub; ++k) {
+      // exchange the half-boundary column (old values)
+      bnd[pr][k & 1][half][lane] = half == 0 ? v[HC - 1] : v[0];
+      named_bar_sync(bar_id, 64);
+      const float ob = bnd[pr][k & 1][half ^ 1][lane];
+      float prev = half == 0 ? v[0] : ob;             // left neighbour of column 0
+      const float last_rt = half == 0 ? ob : v[HC - 1];  // right neighbour of the last column
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        float z[4];
+        if (TAPE) {
+          const int64_t b0 = ((f * c.n_sub + k) * 2 * static_cast<int64_t>(N) + j) * NODES +
+                             row * COLS + c0 + 2 * q;
+          const int64_t wo = static_cast<int64_t>(N) * NODES;
+          z[0] = float(tape[b0]);
+          z[1] = float(tape[b0 + wo]);
+          z[2] = 2 * q + 1 < HC ? float(tape[b0 + 1]) : 0.f;
+          z[3] = 2 * q + 1 < HC ? float(tape[b0 + wo + 1]) : 0.f;
+        } else {
+          const uint4 rr = philox10(
+              make_uint4(j, step0 + k, static_cast<uint32_t>((row * 2 + half) * NQ + q),
+                         kPurposeFhn),
+              key);
+          const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
+          const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
+          z[0] = g0.x;
+          z[1] = g0.y;
+          z[2] = g1.x;
+          z[3] = g1.y;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = 2 * q + h;
+          if (cc < HC) {
+            const float u = v[cc];
+            const float up = __shfl_sync(0xffffffffu, u, src_up);
+            const float dn = __shfl_sync(0xffffffffu, u, src_dn);
+            const float rt = cc < HC - 1 ? v[cc + 1] : last_rt;
+            const float nb = ((up + dn) + prev) + rt;
+            const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
+            float un = fmaf(c.dt, p3 - w[cc], u);
+            un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
+            w[cc] = fmaf(sw, z[2 * h + 1], fmaf(c.wc, w[cc], fmaf(c.uc, u, c.c0)));
+            v[cc] = fmaf(sv, z[2 * h], un);
+            prev = u;
+          }
+        }
+      }
+    }
+
+    // epilogue: store, divergence flag, electrode log-likelihood
+    bool fin = true;
+#pragma unroll
+    for (int q = 0; q < HC; ++q) fin = fin && isfinite(v[q]) && isfinite(w[q]);
+    if (lane < ROWS) {
+      float *xd = xout + p * 2 * static_cast<int64_t>(NODES) + row * COLS + c0;
+#pragma unroll
+      for (int q = 0; q < HC; ++q) {
+        xd[q] = v[q];
+        xd[NODES + q] = w[q];
+        plane[pr][row * COLS + c0 + q] = v[q];
+      }
+    }
+    const bool any_bad = __any_sync(0xffffffffu, lane < ROWS && !fin);
+    if (half == 1 && lane == 0) bad[pr] = any_bad;
+    named_bar_sync(bar_id, 64);
+    if (half == 0) {
+      double acc = 0.0;
+      for (int i = lane; i < c.n_obs; i += 32) {
+        const double rsd = __ldg(y + i) - static_cast<double>(plane[pr][__ldg(obs_idx + i)]);
+        acc = fma(rsd, rsd, acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        logw[p] = static_cast<float>(c.obs_coef * acc);
+        if (any_bad || bad[pr]) atomicOr(status + f, PF_ST_DIVERGED);
+      }
+    }
+    named_bar_sync(bar_id, 64);  // plane / bad reused by the next particle
+  }
+}
+
+template <int ROWS, int COLS, bool TAPE>
+static int launch_fhn_pair_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
+                             const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
+                             int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
+                             uint32_t *status, cudaStream_t s) {
+  auto kern = fhn_pair_kernel<ROWS, COLS, TAPE>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
+  if (per_sm < 1) per_sm = 1;
+  int sms = kSmCount, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>((MN + 1) / 2, static_cast<int64_t>(sms) * per_sm);
+  kern<<<static_cast<unsigned>(grid), 128, 0, s>>>(
+      static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
+      static_cast<float *>(logw), MN, N, fc, keys, t, tape, status);
+  return check_launch("pf_fhn_interval(pair)");
+}
+
 // The fp32 fast path covers lattices with a compiled geometry; others use
 // the generic kernel.
 static bool fhn_fast_supported(const pf_fhn_params *p) {
@@ -667,6 +843,14 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   fc.sig_v = float(c.sig_v);
   fc.sig_w = float(c.sig_w);
   fc.obs_coef = c.obs_coef;
+  const char *kv = getenv("PF_FHN_KERNEL");
+  if (kv && kv[0] == 'p') {
+    if (tape)
+      return launch_fhn_pair_t<30, 50, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
+                                             t, tape, status, s);
+    return launch_fhn_pair_t<30, 50, false>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
+                                            t, tape, status, s);
+  }
   if (use_warp_kernel()) {
     if (tape)
       return launch_fhn_warp_t<30, 50, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
@@ -675,18 +859,18 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
                                             t, tape, status, s);
   }
   if (tape)
-    return launch_fhn_fast_t<30, 50, true, 4>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
-                                              t, tape, status, s);
-  const char *mb = getenv("PF_FHN_MINB");
-  const int minb = mb ? atoi(mb) : 5;
-  if (minb == 4)
-    return launch_fhn_fast_t<30, 50, false, 4>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
-                                               keys, t, tape, status, s);
-  if (minb == 6)
-    return launch_fhn_fast_t<30, 50, false, 6>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
-                                               keys, t, tape, status, s);
-  return launch_fhn_fast_t<30, 50, false, 5>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
-                                             t, tape, status, s);
+    return launch_fhn_fast_t<30, 50, true, 4, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                                 keys, t, tape, status, s);
+  const char *pp = getenv("PF_FHN_PP");
+  const int ppv = pp ? atoi(pp) : 2;
+  if (ppv == 2)
+    return launch_fhn_fast_t<30, 50, false, 3, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                                  keys, t, tape, status, s);
+  if (ppv == 3)
+    return launch_fhn_fast_t<30, 50, false, 2, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                                  keys, t, tape, status, s);
+  return launch_fhn_fast_t<30, 50, false, 4, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                                keys, t, tape, status, s);
 }
 
 }  // namespace pf

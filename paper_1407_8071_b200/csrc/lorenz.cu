@@ -21,6 +21,7 @@ namespace pf {
 struct LorenzConsts {
   double s, r, b, dt, dts, sq, ns, two_obs_var;
   int n_sub;
+  float f_dt, f_ndts, f_r, f_nb, f_cz;  // fp32 production constants (host-folded)
 };
 
 // One Euler-Maruyama substep in the reference's evaluation order
@@ -123,17 +124,20 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
       lorenz_substep<T>(x1, x2, x3, T(zk[0]), T(zk[1]), T(zk[2]), c);
     }
   } else if (sizeof(T) == 4) {
-    // 4 substeps = 12 normals = 3 Philox blocks
+    // 4 substeps = 12 normals = 3 Philox blocks; full chunks run unpredicated
     const Key2 key = load_key(keys, f);
-    const float dt = float(c.dt), ndts = float(-c.dts), r = float(c.r), nb = float(-c.b);
-    const float cz = float(c.sq * c.ns) * kSqrt2Ln2;  // normals are box_muller_fast_unscaled
+    const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb;
+    const float cz = c.f_cz;  // sqrt(dt)*noise_scale*sqrt(2 ln 2): unscaled Box-Muller
     float a1 = float(x1), a2 = float(x2), a3 = float(x3);
-    for (int k0 = 0; k0 < c.n_sub; k0 += 4) {
+    const int nfull = c.n_sub >> 2;
+    for (int k4 = 0; k4 <= nfull; ++k4) {
+      const int left = c.n_sub - 4 * k4;
+      if (left <= 0) break;
       float z[12];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const uint4 rr = philox10(
-            make_uint4(static_cast<uint32_t>(j), t, static_cast<uint32_t>((k0 >> 2) * 3 + q),
+            make_uint4(static_cast<uint32_t>(j), t, static_cast<uint32_t>(k4 * 3 + q),
                        kPurposeLorenz),
             key);
         const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
@@ -143,12 +147,18 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
         z[4 * q + 2] = g1.x;
         z[4 * q + 3] = g1.y;
       }
-      // fully unrolled with predication: z[] stays in registers
+      if (left >= 4) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (k0 + q < c.n_sub)
+        for (int q = 0; q < 4; ++q)
           lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r, nb,
                               cz);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (q < left)
+            lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r,
+                                nb, cz);
+      }
     }
     x1 = T(a1);
     x2 = T(a2);
@@ -208,6 +218,11 @@ static LorenzConsts make_consts(const pf_lorenz_params *p) {
   c.ns = p->noise_scale;
   c.two_obs_var = 2.0 * p->obs_var;
   c.n_sub = p->n_sub;
+  c.f_dt = static_cast<float>(c.dt);
+  c.f_ndts = static_cast<float>(-c.dts);
+  c.f_r = static_cast<float>(c.r);
+  c.f_nb = static_cast<float>(-c.b);
+  c.f_cz = static_cast<float>(c.sq * c.ns) * kSqrt2Ln2;
   return c;
 }
 

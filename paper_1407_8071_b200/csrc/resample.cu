@@ -273,6 +273,12 @@ struct WideWs {
   double *m, *total, *cN;                               // per filter
   int *flag;                                            // per filter: 0 ok, 1 collapse, 2 nan
   double *cum;                                          // M*N
+  // reference-order total: numpy pairwise leaves per filter (<= N/64 + 2)
+  int64_t *leaf_start;
+  int32_t *leaf_len;
+  double *leaf_sum;
+  int32_t *n_leaves;
+  int64_t max_leaves;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
@@ -298,6 +304,11 @@ static size_t wide_ws_layout(int64_t M, int64_t N, WideWs *w, char *base) {
   ws.cN = reinterpret_cast<double *>(take(M * 8));
   ws.flag = reinterpret_cast<int *>(take(M * 4));
   ws.cum = reinterpret_cast<double *>(take(static_cast<size_t>(M) * N * 8));
+  ws.max_leaves = N / 64 + 2;
+  ws.leaf_start = reinterpret_cast<int64_t *>(take(static_cast<size_t>(M) * ws.max_leaves * 8));
+  ws.leaf_len = reinterpret_cast<int32_t *>(take(static_cast<size_t>(M) * ws.max_leaves * 4));
+  ws.leaf_sum = reinterpret_cast<double *>(take(static_cast<size_t>(M) * ws.max_leaves * 8));
+  ws.n_leaves = reinterpret_cast<int32_t *>(take(M * 4));
   if (w) *w = ws;
   return off;
 }
@@ -494,6 +505,294 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_merge(
   }
 }
 
+
+// ---- reference-order ("exact") CDF ----------------------------------------
+// numpy's float64 sum is a fixed pairwise recursion (8 accumulators on
+// blocks of <= 128, halves rounded down to a multiple of 8) and cumsum is
+// strictly sequential.  Replicating both orders, plus IEEE division for
+// w = e/total, makes the CDF bit-identical to the reference's whenever the
+// exp() values agree, so ancestors are bit-exact even at N = 2^26 (the
+// blocked parallel scan leaves O(10^2) rounding ties there).  Used in oracle
+// (tape) mode for parity; the production path keeps the parallel scan.
+__device__ double np_pairwise_block(const double *a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
+    r0 = __dadd_rn(r0, a[i]);
+    r1 = __dadd_rn(r1, a[i + 1]);
+    r2 = __dadd_rn(r2, a[i + 2]);
+    r3 = __dadd_rn(r3, a[i + 3]);
+    r4 = __dadd_rn(r4, a[i + 4]);
+    r5 = __dadd_rn(r5, a[i + 5]);
+    r6 = __dadd_rn(r6, a[i + 6]);
+    r7 = __dadd_rn(r7, a[i + 7]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// numpy's pairwise recursion  pw(a, n) = n <= 128 ? block(a, n)
+//   : pw(a, n2) + pw(a + n2, n - n2),  n2 = n/2 - (n/2) % 8,
+// evaluated iteratively (explicit stack, no device recursion).  Leaves are
+// either summed here from `a` or, if leaf_sums != nullptr, taken in order
+// from precomputed leaf sums.
+__device__ double np_pairwise_iter(const double *a, int64_t n_total, const double *leaf_sums) {
+  int64_t st_lo[48], st_n[48];
+  double st_left[48];
+  int st_state[48];
+  int sp = 0;
+  st_lo[0] = 0;
+  st_n[0] = n_total;
+  st_state[0] = 0;
+  sp = 1;
+  double ret = 0.0;
+  int64_t leaf = 0;
+  while (sp > 0) {
+    const int top = sp - 1;
+    const int64_t n = st_n[top];
+    if (n <= 128) {
+      ret = leaf_sums ? leaf_sums[leaf++] : np_pairwise_block(a + st_lo[top], n);
+      --sp;
+      continue;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    if (st_state[top] == 0) {
+      st_state[top] = 1;
+      st_lo[sp] = st_lo[top];
+      st_n[sp] = n2;
+      st_state[sp] = 0;
+      ++sp;
+    } else if (st_state[top] == 1) {
+      st_left[top] = ret;
+      st_state[top] = 2;
+      st_lo[sp] = st_lo[top] + n2;
+      st_n[sp] = n - n2;
+      st_state[sp] = 0;
+      ++sp;
+    } else {
+      ret = __dadd_rn(st_left[top], ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+__device__ double np_pairwise_sum(const double *a, int64_t n) {
+  return np_pairwise_iter(a, n, nullptr);
+}
+
+// one thread, numpy cumsum order: c[0] = a[0], c[i] = c[i-1] + a[i]
+__device__ void np_cumsum_serial(const double *a, double *c, int64_t n) {
+  double run = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    run = i == 0 ? a[0] : __dadd_rn(run, a[i]);
+    c[i] = run;
+  }
+}
+
+// bank path, reference order; dynamic smem = 2*N doubles
+template <typename TW, int MODE>
+__global__ void __launch_bounds__(256) resample_bank_exact_kernel(
+    const TW *__restrict__ logw, int32_t N, const double *__restrict__ u_tape,
+    const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
+    double *__restrict__ lnc, uint8_t *__restrict__ collapsed, uint32_t *__restrict__ status) {
+  extern __shared__ double sx[];
+  double *s_a = sx, *s_cum = sx + N;
+  __shared__ double scratch[33];
+  __shared__ double s_total, s_cN;
+  const int tid = threadIdx.x;
+  const int64_t f = blockIdx.x, base = f * N;
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int i = tid; i < N; i += blockDim.x) {
+    const double v = static_cast<double>(logw[base + i]);
+    s_a[i] = v;
+    nan |= isnan(v);
+    mx = fmax(mx, v);
+  }
+  nan = __syncthreads_or(nan);
+  const double m = block_max(mx, scratch);
+  if (nan || m == -INFINITY) {
+    for (int i = tid; i < N; i += blockDim.x) anc[base + i] = static_cast<int32_t>(base + i);
+    if (tid == 0) {
+      collapsed[f] = nan ? 0 : 1;
+      if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
+    }
+    return;
+  }
+  for (int i = tid; i < N; i += blockDim.x) s_a[i] = exp(__dsub_rn(s_a[i], m));
+  __syncthreads();
+  if (tid == 0) s_total = np_pairwise_sum(s_a, N);  // shifted.sum(), core.py:135
+  __syncthreads();
+  const double total = s_total;
+  for (int i = tid; i < N; i += blockDim.x) s_a[i] = __ddiv_rn(s_a[i], total);
+  __syncthreads();
+  if (tid == 0) np_cumsum_serial(s_a, s_cum, N);  // np.cumsum(weights), resampling.py:41
+  __syncthreads();
+  if (MODE == 1) {
+    for (int i = tid; i < N; i += blockDim.x) s_a[i] = u_tape[base + i];
+  } else {
+    const Key2 key = load_key(keys, f);
+    for (int i = tid; i < N; i += blockDim.x) s_a[i] = spacing_exp_fast(key, t, i);
+    __syncthreads();
+    if (tid == 0) {
+      np_cumsum_serial(s_a, s_a, N);
+      s_cN = __dadd_rn(s_a[N - 1], spacing_exp_fast(key, t, N));
+    }
+    __syncthreads();
+    for (int i = tid; i < N; i += blockDim.x) s_a[i] = __ddiv_rn(s_a[i], s_cN);
+  }
+  __syncthreads();
+  const int per = (N + blockDim.x - 1) / blockDim.x;
+  const int j0 = tid * per, j1 = min(N, j0 + per);
+  if (j0 < j1) {
+    int k = lower_bound_f64(s_cum, N, s_a[j0]);
+    for (int j = j0; j < j1; ++j) {
+      while (k < N && s_cum[k] < s_a[j]) ++k;
+      anc[base + j] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+    }
+  }
+  if (tid == 0) {
+    collapsed[f] = 0;
+    const double lmr = __dsub_rn(__dadd_rn(m, log(total)), log(static_cast<double>(N)));
+    lnc[f] = __dadd_rn(lnc[f], lmr);
+  }
+}
+
+// wide path, reference order: e into ws.cum, numpy-order total (1 thread per
+// filter), w = e/total, sequential cumsum (1 thread per filter).
+template <typename TW>
+__global__ void wide_exact_e(const TW *__restrict__ logw, int64_t N, int64_t tpf, WideWs ws) {
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  if (ws.flag[f]) return;
+  const double m = ws.m[f];
+  const int64_t i0 = tt * kTile, i1 = min(N, i0 + kTile);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+    ws.cum[f * N + i] = exp(__dsub_rn(load_lw(logw + f * N + i), m));
+}
+
+// numpy's recursion, split into (1) leaf enumeration (left to right),
+// (2) parallel leaf sums, (3) the combine in the same tree order.
+__device__ void np_enum_leaves(int64_t n_total, int64_t *start, int32_t *len, int32_t *cnt) {
+  int64_t st_lo[48], st_n[48];
+  int sp = 1;
+  st_lo[0] = 0;
+  st_n[0] = n_total;
+  while (sp > 0) {
+    --sp;
+    const int64_t lo = st_lo[sp], n = st_n[sp];
+    if (n <= 128) {
+      start[*cnt] = lo;
+      len[*cnt] = static_cast<int32_t>(n);
+      ++*cnt;
+      continue;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    st_lo[sp] = lo + n2;  // right pushed first -> left popped first
+    st_n[sp] = n - n2;
+    ++sp;
+    st_lo[sp] = lo;
+    st_n[sp] = n2;
+    ++sp;
+  }
+}
+
+__global__ void wide_exact_leaves(int64_t N, WideWs ws) {
+  const int64_t f = blockIdx.x;
+  if (threadIdx.x) return;
+  int32_t cnt = 0;
+  np_enum_leaves(N, ws.leaf_start + f * ws.max_leaves, ws.leaf_len + f * ws.max_leaves, &cnt);
+  ws.n_leaves[f] = cnt;
+}
+
+__global__ void wide_exact_leafsum(int64_t N, WideWs ws) {
+  const int64_t f = blockIdx.y;
+  if (ws.flag[f]) return;
+  const int64_t l = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (l >= ws.n_leaves[f]) return;
+  const int64_t o = f * ws.max_leaves + l;
+  ws.leaf_sum[o] = np_pairwise_block(ws.cum + f * N + ws.leaf_start[o], ws.leaf_len[o]);
+}
+
+__global__ void wide_exact_total(int64_t N, WideWs ws, double *lnc) {
+  const int64_t f = blockIdx.x;
+  if (ws.flag[f] || threadIdx.x) return;
+  const double total = np_pairwise_iter(nullptr, N, ws.leaf_sum + f * ws.max_leaves);
+  ws.total[f] = total;
+  const double lmr = __dsub_rn(__dadd_rn(ws.m[f], log(total)), log(static_cast<double>(N)));
+  lnc[f] = __dadd_rn(lnc[f], lmr);
+}
+
+__global__ void wide_exact_w(int64_t N, int64_t tpf, WideWs ws) {
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  if (ws.flag[f]) return;
+  const double total = ws.total[f];
+  const int64_t i0 = tt * kTile, i1 = min(N, i0 + kTile);
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x)
+    ws.cum[f * N + i] = __ddiv_rn(ws.cum[f * N + i], total);
+}
+
+// one warp per filter: the warp streams 1024-element tiles through shared
+// memory (coalesced, next tile prefetched into registers) while lane 0 runs
+// the strictly sequential numpy cumsum over the current tile.
+__global__ void __launch_bounds__(32) wide_exact_cumsum(int64_t N, WideWs ws) {
+  __shared__ double tile[2][1024];
+  const int64_t f = blockIdx.x;
+  if (ws.flag[f]) return;
+  const int lane = threadIdx.x;
+  double *c = ws.cum + f * N;
+  const int64_t ntiles = (N + 1023) / 1024;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int64_t i = j * 32 + lane;
+    tile[0][j * 32 + lane] = i < N ? c[i] : 0.0;
+  }
+  __syncwarp();
+  double run = 0.0;
+  for (int64_t tt = 0; tt < ntiles; ++tt) {
+    const int cur = tt & 1;
+    double pre[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t i = (tt + 1) * 1024 + j * 32 + lane;
+      pre[j] = i < N ? c[i] : 0.0;
+    }
+    if (lane == 0) {
+      const int64_t i0 = tt * 1024;
+      const int cnt = static_cast<int>(N - i0 < 1024 ? N - i0 : 1024);
+      int i = 0;
+      if (tt == 0) {
+        run = tile[cur][0];
+        i = 1;
+      }
+#pragma unroll 8
+      for (; i < cnt; ++i) {
+        run = __dadd_rn(run, tile[cur][i]);
+        tile[cur][i] = run;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t i = tt * 1024 + j * 32 + lane;
+      if (i < N) c[i] = tile[cur][j * 32 + lane];
+      tile[cur ^ 1][j * 32 + lane] = pre[j];
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void wide_gather_kernel(const float *__restrict__ xin, const int32_t *__restrict__ anc,
                                    int64_t MN, int dims, float *__restrict__ xout) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -507,8 +806,21 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
                            const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
                            uint8_t *collapsed, uint32_t *status, void *ws_v, size_t ws_bytes,
                            cudaStream_t s, const float *gx_in = nullptr,
-                           float *gx_out = nullptr, int gdims = 0) {
+                           float *gx_out = nullptr, int gdims = 0, uint32_t flags = 0) {
   const TW *logw = static_cast<const TW *>(logw_v);
+  const bool exact = flags & PF_RS_REFERENCE_ORDER;
+  if (N <= kBankMaxN && exact) {
+    auto kern = u_tape ? resample_bank_exact_kernel<TW, 1> : resample_bank_exact_kernel<TW, 0>;
+    const size_t smem = 2 * static_cast<size_t>(N) * sizeof(double);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    kern<<<static_cast<unsigned>(M), 256, smem, s>>>(logw, static_cast<int32_t>(N), u_tape, keys,
+                                                     t, anc, lnc, collapsed, status);
+    if (gx_in)
+      wide_gather_kernel<<<grid_for(M * N, 256), 256, 0, s>>>(gx_in, anc, M * N, gdims, gx_out);
+    return check_launch("pf_segmented_resample(bank, reference order)");
+  }
   if (N <= kBankMaxN) {
     using K = void (*)(const TW *, int32_t, const double *, const uint32_t *, uint32_t, int32_t *,
                        double *, uint8_t *, uint32_t *, const float *, float *, int, int64_t);
@@ -549,15 +861,31 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
   const unsigned nt = static_cast<unsigned>(M * tpf);
   wide_tile_max<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
   wide_filter_max<<<static_cast<unsigned>(M), 256, 0, s>>>(tpf, ws, collapsed, status);
-  wide_tile_expsum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
-  wide_filter_total<<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, lnc);
-  if (u_tape)
-    wide_tile_sums<TW, 1><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
-  else
-    wide_tile_sums<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
-  wide_offsets_kernel<<<static_cast<unsigned>(M), 256, 2 * 1024 * sizeof(double), s>>>(M, tpf,
-                                                                                        ws);
-  wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+  if (exact) {
+    wide_exact_e<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+    wide_exact_leaves<<<static_cast<unsigned>(M), 32, 0, s>>>(N, ws);
+    wide_exact_leafsum<<<dim3(static_cast<unsigned>((ws.max_leaves + 127) / 128),
+                              static_cast<unsigned>(M)),
+                         128, 0, s>>>(N, ws);
+    wide_exact_total<<<static_cast<unsigned>(M), 32, 0, s>>>(N, ws, lnc);
+    wide_exact_w<<<nt, kTileThreads, 0, s>>>(N, tpf, ws);
+    wide_exact_cumsum<<<static_cast<unsigned>(M), 32, 0, s>>>(N, ws);
+    if (!u_tape) {  // tile offsets of the exponential spacings
+      wide_tile_sums<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
+      wide_offsets_kernel<<<static_cast<unsigned>(M), 256, 2 * 1024 * sizeof(double), s>>>(
+          M, tpf, ws);
+    }
+  } else {
+    wide_tile_expsum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+    wide_filter_total<<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, lnc);
+    if (u_tape)
+      wide_tile_sums<TW, 1><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
+    else
+      wide_tile_sums<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
+    wide_offsets_kernel<<<static_cast<unsigned>(M), 256, 2 * 1024 * sizeof(double), s>>>(M, tpf,
+                                                                                          ws);
+    wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+  }
   if (u_tape)
     wide_tile_merge<1><<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc);
   else
@@ -641,22 +969,23 @@ int pf_segmented_resample(pf_dtype logw_dtype, const void *logw, int64_t M, int6
                                 ws_bytes, s);
 }
 
-int pf_segmented_resample_gather(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
-                                 const double *u_tape, const uint32_t *keys, uint32_t t,
-                                 int32_t *anc_out, double *lnc, uint8_t *collapsed,
-                                 uint32_t *status, void *ws, size_t ws_bytes,
-                                 const float *x_in, float *x_out, int32_t dims, void *stream) {
-  PF_REQUIRE(logw && anc_out && lnc && collapsed && status && x_in && x_out && dims >= 1,
-             "pf_segmented_resample_gather: null / bad arguments");
-  PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_segmented_resample_gather: bad M/N");
-  PF_REQUIRE(u_tape || keys, "pf_segmented_resample_gather: need keys (Philox) or u_tape");
-  PF_REQUIRE(x_in != x_out, "pf_segmented_resample_gather: x_in and x_out must not alias");
+int pf_segmented_resample_ex(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
+                             const double *u_tape, const uint32_t *keys, uint32_t t,
+                             int32_t *anc_out, double *lnc, uint8_t *collapsed, uint32_t *status,
+                             void *ws, size_t ws_bytes, const float *x_in, float *x_out,
+                             int32_t dims, uint32_t flags, void *stream) {
+  PF_REQUIRE(logw && anc_out && lnc && collapsed && status, "pf_segmented_resample_ex: null");
+  PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_segmented_resample_ex: bad M/N");
+  PF_REQUIRE(u_tape || keys, "pf_segmented_resample_ex: need keys (Philox) or u_tape");
+  PF_REQUIRE(!x_in || (x_out && dims >= 1 && x_in != x_out),
+             "pf_segmented_resample_ex: gather needs x_out != x_in and dims >= 1");
+  PF_REQUIRE((flags & ~PF_RS_REFERENCE_ORDER) == 0, "pf_segmented_resample_ex: unknown flags");
   const cudaStream_t s = as_stream(stream);
   if (logw_dtype == PF_F64)
     return launch_resample<double>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status,
-                                   ws, ws_bytes, s, x_in, x_out, dims);
+                                   ws, ws_bytes, s, x_in, x_out, dims, flags);
   return launch_resample<float>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status, ws,
-                                ws_bytes, s, x_in, x_out, dims);
+                                ws_bytes, s, x_in, x_out, dims, flags);
 }
 
 int pf_op_normalize_log_weights(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,

@@ -242,7 +242,7 @@ def _resample_case(M, N, sigma, seed):
     return lw, u
 
 
-def _gpu_resample(lw, u):
+def _gpu_resample(lw, u, flags=0):
     M, N = lw.shape
     d_lw = torch.from_numpy(lw.reshape(-1)).cuda()
     d_u = torch.from_numpy(u.reshape(-1)).cuda()
@@ -252,9 +252,9 @@ def _gpu_resample(lw, u):
     st = torch.zeros(M, dtype=torch.int32, device="cuda")
     wsb = _lib.load().pf_resample_workspace_bytes(M, N)
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
-    _lib.call("pf_segmented_resample", _lib.PF_F32, _lib.ptr(d_lw), M, N, _lib.ptr(d_u), None, 1,
-              _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st), _lib.ptr(ws), wsb,
-              _lib.stream_ptr())
+    _lib.call("pf_segmented_resample_ex", _lib.PF_F32, _lib.ptr(d_lw), M, N, _lib.ptr(d_u), None,
+              1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st), _lib.ptr(ws), wsb,
+              None, None, 0, flags, _lib.stream_ptr())
     a = anc.cpu().numpy().reshape(M, N).astype(np.int64) - (np.arange(M) * N)[:, None]
     return a, lnc.cpu().numpy(), coll.cpu().numpy()
 
@@ -278,6 +278,31 @@ def test_wide_path_multi_filter(M, N):
     ref_anc, ref_lmr, _, cum = orc.resample_rows(lw, u)
     assert certify_ties(anc, ref_anc, cum, u) == 0
     assert np.max(np.abs(lmr - ref_lmr)) < 1e-12
+
+
+@pytest.mark.parametrize("M,N,sigma", [(1 << 12, 1 << 10, 1.0), (1 << 12, 1 << 10, 10.0),
+                                         (8, 8192, 3.0), (3, 20000, 1.0), (2, 70001, 10.0)])
+def test_reference_order_cdf_is_bit_exact(M, N, sigma):
+    """PF_RS_REFERENCE_ORDER: numpy-order total + sequential cumsum -> the
+    CDF equals the reference's bit for bit, hence zero ancestor mismatches."""
+    lw, u = _resample_case(M, N, sigma, seed=N + int(sigma))
+    anc, lmr, coll = _gpu_resample(lw, u, flags=_lib.PF_RS_REFERENCE_ORDER)
+    ref_anc, ref_lmr, _, _ = orc.resample_rows(lw, u)
+    assert np.array_equal(anc, ref_anc)
+    assert np.max(np.abs(lmr - ref_lmr)) < 1e-12
+
+
+@pytest.mark.parametrize("sigma", [1.0, 10.0])
+def test_cfg1_centralised_2pow26_reference_order_bit_exact(sigma):
+    """BASELINE cfg1 centralised case, M=1 x N=2^26: bit-exact ancestors."""
+    N = 1 << 26
+    lw, u = _resample_case(1, N, sigma, seed=100 + int(sigma))
+    anc, lmr, _ = _gpu_resample(lw, u, flags=_lib.PF_RS_REFERENCE_ORDER)
+    ref_anc, ref_lmr, _, _ = orc.resample_rows(lw, u)
+    n_bad = int(np.count_nonzero(anc != ref_anc))
+    print(f"N=2^26 sigma={sigma} reference order: {n_bad} mismatches")
+    assert n_bad == 0
+    assert abs(lmr[0] - ref_lmr[0]) < 1e-10
 
 
 @pytest.mark.parametrize("sigma", [1.0, 10.0])
@@ -398,9 +423,9 @@ def test_resample_gather_fused_matches_unfused(M, N):
     st = torch.zeros(M, dtype=torch.int32, device="cuda")
     wsb = _lib.load().pf_resample_workspace_bytes(M, N)
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
-    _lib.call("pf_segmented_resample_gather", _lib.PF_F32, _lib.ptr(d_lw), M, N, _lib.ptr(d_u),
+    _lib.call("pf_segmented_resample_ex", _lib.PF_F32, _lib.ptr(d_lw), M, N, _lib.ptr(d_u),
               None, 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st), _lib.ptr(ws),
-              wsb, _lib.ptr(x), _lib.ptr(xo), 3, _lib.stream_ptr())
+              wsb, _lib.ptr(x), _lib.ptr(xo), 3, 0, _lib.stream_ptr())
     a = anc.cpu().numpy().astype(np.int64)
     assert np.array_equal(a.reshape(M, N) - (np.arange(M) * N)[:, None], anc_ref)
     assert torch.equal(xo, x[:, anc.long()])
