@@ -17,8 +17,6 @@
 #include "common.cuh"
 #include "philox.cuh"
 
-#include <cstdlib>
-
 namespace pf {
 
 constexpr int kFhnRows = 6;  // rows per thread (even: Philox pairs rows)
@@ -517,307 +515,12 @@ static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t 
   return check_launch("pf_fhn_interval(fast)");
 }
 
-// ---- warp-per-particle variant ------------------------------------------
-// One warp owns one particle for the whole interval: lane r holds lattice
-// row r (ROWS <= 32) in registers (v[COLS], w[COLS]).  Left/right
-// neighbours are the lane's own registers, up/down come from
-// __shfl_sync with a clamped source lane (which *is* the ghost = self
-// Neumann boundary), so there is no shared memory traffic and no CTA
-// barrier inside the time loop; 25 independent column pairs per lane give
-// the scheduler instruction-level parallelism instead of thread-level.
-template <int ROWS, int COLS, bool TAPE>
-__global__ void __launch_bounds__(64, 5) fhn_warp_kernel(
-    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
-    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
-    int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
-    const double *__restrict__ tape, uint32_t *__restrict__ status) {
-  static_assert(ROWS <= 32 && COLS % 2 == 0, "warp kernel: ROWS <= 32, even COLS");
-  constexpr int NODES = ROWS * COLS;
-  constexpr int WPB = 2;  // warps per block
-  extern __shared__ __align__(16) float wsm[];  // [WPB][NODES], epilogue only
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float *vs = wsm + wib * NODES;
-  const int row = lane < ROWS ? lane : ROWS - 1;  // spare lanes shadow the last row
-  const int src_up = row > 0 ? row - 1 : 0;        // clamp = ghost = self
-  const int src_dn = row < ROWS - 1 ? row + 1 : ROWS - 1;
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * WPB;
-
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * WPB + wib; p < MN; p += nwarps) {
-    const int64_t f = p / N;
-    const uint32_t j = static_cast<uint32_t>(p - f * N);
-    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
-    const float2 *xs = reinterpret_cast<const float2 *>(xin + src * 2 * static_cast<int64_t>(NODES) +
-                                                        row * COLS);
-    float v[COLS], w[COLS];
-#pragma unroll
-    for (int q = 0; q < COLS / 2; ++q) {
-      const float2 a = __ldg(xs + q);
-      const float2 b = __ldg(xs + NODES / 2 + q);
-      v[2 * q] = a.x;
-      v[2 * q + 1] = a.y;
-      w[2 * q] = b.x;
-      w[2 * q + 1] = b.y;
-    }
-    Key2 key{0u, 0u};
-    if (!TAPE) key = load_key(keys, f);
-    const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
-    for (int k = 0; k < c.n_sub; ++k) {
-      float prev = v[0];  // left ghost of column 0 = itself
-#pragma unroll
-      for (int q = 0; q < COLS / 2; ++q) {
-        float z[4];
-        if (TAPE) {
-          const int64_t b0 = ((f * c.n_sub + k) * 2 * static_cast<int64_t>(N) + j) * NODES +
-                             row * COLS + 2 * q;
-          const int64_t wo = static_cast<int64_t>(N) * NODES;
-          z[0] = float(tape[b0]);
-          z[1] = float(tape[b0 + wo]);
-          z[2] = float(tape[b0 + 1]);
-          z[3] = float(tape[b0 + wo + 1]);
-        } else {
-          const uint4 rr = philox10(
-              make_uint4(j, step0 + k, static_cast<uint32_t>(row * (COLS / 2) + q), kPurposeFhn),
-              key);
-          const float2 g0 = box_muller_fast(rr.x, rr.y);
-          const float2 g1 = box_muller_fast(rr.z, rr.w);
-          z[0] = g0.x;
-          z[1] = g0.y;
-          z[2] = g1.x;
-          z[3] = g1.y;
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int cc = 2 * q + h;
-          const float u = v[cc];
-          const float up = __shfl_sync(0xffffffffu, u, src_up);
-          const float dn = __shfl_sync(0xffffffffu, u, src_dn);
-          const float rt = cc < COLS - 1 ? v[cc + 1] : u;
-          const float nb = ((up + dn) + prev) + rt;
-          const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
-          float un = fmaf(c.dt, p3 - w[cc], u);
-          un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
-          w[cc] = fmaf(c.sig_w, z[2 * h + 1], fmaf(c.wc, w[cc], fmaf(c.uc, u, c.c0)));
-          v[cc] = fmaf(c.sig_v, z[2 * h], un);
-          prev = u;
-        }
-      }
-    }
-
-    // epilogue: store, divergence flag, electrode log-likelihood
-    bool fin = true;
-#pragma unroll
-    for (int cc = 0; cc < COLS; ++cc) fin = fin && isfinite(v[cc]) && isfinite(w[cc]);
-    if (lane < ROWS) {
-      float2 *xd = reinterpret_cast<float2 *>(xout + p * 2 * static_cast<int64_t>(NODES) +
-                                              row * COLS);
-#pragma unroll
-      for (int q = 0; q < COLS / 2; ++q) {
-        xd[q] = make_float2(v[2 * q], v[2 * q + 1]);
-        xd[NODES / 2 + q] = make_float2(w[2 * q], w[2 * q + 1]);
-        reinterpret_cast<float2 *>(vs + row * COLS)[q] = make_float2(v[2 * q], v[2 * q + 1]);
-      }
-    }
-    const bool any_bad = __any_sync(0xffffffffu, lane < ROWS && !fin);
-    __syncwarp();
-    double acc = 0.0;
-    for (int i = lane; i < c.n_obs; i += 32) {
-      const double rsd = __ldg(y + i) - static_cast<double>(vs[__ldg(obs_idx + i)]);
-      acc = fma(rsd, rsd, acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      logw[p] = static_cast<float>(c.obs_coef * acc);
-      if (any_bad) atomicOr(status + f, PF_ST_DIVERGED);
-    }
-    __syncwarp();
-  }
-}
-
-template <int ROWS, int COLS, bool TAPE>
-static int launch_fhn_warp_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
-                             const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
-                             int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
-                             uint32_t *status, cudaStream_t s) {
-  constexpr int threads = 64;
-  const size_t smem = 2 * static_cast<size_t>(ROWS * COLS) * sizeof(float);
-  auto kern = fhn_warp_kernel<ROWS, COLS, TAPE>;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-  if (per_sm < 1) per_sm = 1;
-  int sms = kSmCount, dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t grid = std::min<int64_t>((MN + 1) / 2, static_cast<int64_t>(sms) * per_sm);
-  kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(
-      static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
-      static_cast<float *>(logw), MN, N, fc, keys, t, tape, status);
-  return check_launch("pf_fhn_interval(warp)");
-}
-
-// ---- warp-pair-per-particle variant ---------------------------------------
-// Two warps own one particle: lane r of warp h holds row r, columns
-// [h*HC, h*HC+HC) in registers.  Vertical neighbours come from __shfl_sync
-// with clamped source lanes (= the ghost = self Neumann boundary),
-// horizontal ones from the lane's own registers; only the two columns at the
-// half boundary cross warps, through a double-buffered shared slot and one
-// 64-thread named barrier per Euler step.  No shared-memory stencil, no
-// CTA-wide barrier.
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <int ROWS, int COLS, bool TAPE>
-__global__ void __launch_bounds__(128, 4) fhn_pair_kernel(
-    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
-    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
-    int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
-    const double *__restrict__ tape, uint32_t *__restrict__ status) {
-  static_assert(ROWS <= 32 && COLS % 2 == 0, "pair kernel: ROWS <= 32, even COLS");
-  constexpr int HC = COLS / 2;          // columns per warp
-  constexpr int NQ = (HC + 1) / 2;      // Philox blocks per lane per step
-  constexpr int NODES = ROWS * COLS;
-  constexpr int PPB = 2;                // particles per block (4 warps)
-  __shared__ float bnd[PPB][2][2][32];  // [pair][buffer][half][lane]
-  __shared__ __align__(16) float plane[PPB][NODES];
-  __shared__ int bad[PPB];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int pr = warp >> 1, half = warp & 1;
-  const int row = lane < ROWS ? lane : ROWS - 1;  // spare lanes shadow the last row
-  const int src_up = row > 0 ? row - 1 : 0;        // clamp = ghost = self
-  const int src_dn = row < ROWS - 1 ? row + 1 : ROWS - 1;
-  const int c0 = half * HC;
-  const int bar_id = 1 + pr;
-  const int64_t npairs = static_cast<int64_t>(gridDim.x) * PPB;
-
-  for (int64_t p = static_cast<int64_t>(blockIdx.x) * PPB + pr; p < MN; p += npairs) {
-    const int64_t f = p / N;
-    const uint32_t j = static_cast<uint32_t>(p - f * N);
-    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
-    const float *xs = xin + src * 2 * static_cast<int64_t>(NODES) + row * COLS + c0;
-    float v[HC], w[HC];
-#pragma unroll
-    for (int q = 0; q < HC; ++q) {
-      v[q] = __ldg(xs + q);
-      w[q] = __ldg(xs + NODES + q);
-    }
-    Key2 key{0u, 0u};
-    if (!TAPE) key = load_key(keys, f);
-    const float sv = TAPE ? c.sig_v : c.sig_v * kSqrt2Ln2;
-    const float sw = TAPE ? c.sig_w : c.sig_w * kSqrt2Ln2;
-    const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
-    for (int k = 0; k < c.n_sub; ++k) {
-      // exchange the half-boundary column (old values)
-      bnd[pr][k & 1][half][lane] = half == 0 ? v[HC - 1] : v[0];
-      named_bar_sync(bar_id, 64);
-      const float ob = bnd[pr][k & 1][half ^ 1][lane];
-      float prev = half == 0 ? v[0] : ob;             // left neighbour of column 0
-      const float last_rt = half == 0 ? ob : v[HC - 1];  // right neighbour of the last column
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        float z[4];
-        if (TAPE) {
-          const int64_t b0 = ((f * c.n_sub + k) * 2 * static_cast<int64_t>(N) + j) * NODES +
-                             row * COLS + c0 + 2 * q;
-          const int64_t wo = static_cast<int64_t>(N) * NODES;
-          z[0] = float(tape[b0]);
-          z[1] = float(tape[b0 + wo]);
-          z[2] = 2 * q + 1 < HC ? float(tape[b0 + 1]) : 0.f;
-          z[3] = 2 * q + 1 < HC ? float(tape[b0 + wo + 1]) : 0.f;
-        } else {
-          const uint4 rr = philox10(
-              make_uint4(j, step0 + k, static_cast<uint32_t>((row * 2 + half) * NQ + q),
-                         kPurposeFhn),
-              key);
-          const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
-          const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
-          z[0] = g0.x;
-          z[1] = g0.y;
-          z[2] = g1.x;
-          z[3] = g1.y;
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int cc = 2 * q + h;
-          if (cc < HC) {
-            const float u = v[cc];
-            const float up = __shfl_sync(0xffffffffu, u, src_up);
-            const float dn = __shfl_sync(0xffffffffu, u, src_dn);
-            const float rt = cc < HC - 1 ? v[cc + 1] : last_rt;
-            const float nb = ((up + dn) + prev) + rt;
-            const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
-            float un = fmaf(c.dt, p3 - w[cc], u);
-            un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
-            w[cc] = fmaf(sw, z[2 * h + 1], fmaf(c.wc, w[cc], fmaf(c.uc, u, c.c0)));
-            v[cc] = fmaf(sv, z[2 * h], un);
-            prev = u;
-          }
-        }
-      }
-    }
-
-    // epilogue: store, divergence flag, electrode log-likelihood
-    bool fin = true;
-#pragma unroll
-    for (int q = 0; q < HC; ++q) fin = fin && isfinite(v[q]) && isfinite(w[q]);
-    if (lane < ROWS) {
-      float *xd = xout + p * 2 * static_cast<int64_t>(NODES) + row * COLS + c0;
-#pragma unroll
-      for (int q = 0; q < HC; ++q) {
-        xd[q] = v[q];
-        xd[NODES + q] = w[q];
-        plane[pr][row * COLS + c0 + q] = v[q];
-      }
-    }
-    const bool any_bad = __any_sync(0xffffffffu, lane < ROWS && !fin);
-    if (half == 1 && lane == 0) bad[pr] = any_bad;
-    named_bar_sync(bar_id, 64);
-    if (half == 0) {
-      double acc = 0.0;
-      for (int i = lane; i < c.n_obs; i += 32) {
-        const double rsd = __ldg(y + i) - static_cast<double>(plane[pr][__ldg(obs_idx + i)]);
-        acc = fma(rsd, rsd, acc);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-      if (lane == 0) {
-        logw[p] = static_cast<float>(c.obs_coef * acc);
-        if (any_bad || bad[pr]) atomicOr(status + f, PF_ST_DIVERGED);
-      }
-    }
-    named_bar_sync(bar_id, 64);  // plane / bad reused by the next particle
-  }
-}
-
-template <int ROWS, int COLS, bool TAPE>
-static int launch_fhn_pair_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
-                             const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
-                             int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
-                             uint32_t *status, cudaStream_t s) {
-  auto kern = fhn_pair_kernel<ROWS, COLS, TAPE>;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
-  if (per_sm < 1) per_sm = 1;
-  int sms = kSmCount, dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t grid = std::min<int64_t>((MN + 1) / 2, static_cast<int64_t>(sms) * per_sm);
-  kern<<<static_cast<unsigned>(grid), 128, 0, s>>>(
-      static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
-      static_cast<float *>(logw), MN, N, fc, keys, t, tape, status);
-  return check_launch("pf_fhn_interval(pair)");
-}
-
 // The fp32 fast path covers lattices with a compiled geometry; others use
 // the generic kernel.
 static bool fhn_fast_supported(const pf_fhn_params *p) {
   return p->rows == 30 && p->cols == 50 && p->degree_drive == -p->coupling;
 }
 
-static bool use_warp_kernel() {
-  const char *e = getenv("PF_FHN_KERNEL");
-  return e && e[0] == 'w';  // "warp" selects the warp-per-particle kernel
-}
 
 static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *anc, void *x_out,
                            const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
@@ -843,33 +546,11 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   fc.sig_v = float(c.sig_v);
   fc.sig_w = float(c.sig_w);
   fc.obs_coef = c.obs_coef;
-  const char *kv = getenv("PF_FHN_KERNEL");
-  if (kv && kv[0] == 'p') {
-    if (tape)
-      return launch_fhn_pair_t<30, 50, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
-                                             t, tape, status, s);
-    return launch_fhn_pair_t<30, 50, false>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
-                                            t, tape, status, s);
-  }
-  if (use_warp_kernel()) {
-    if (tape)
-      return launch_fhn_warp_t<30, 50, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
-                                             t, tape, status, s);
-    return launch_fhn_warp_t<30, 50, false>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys,
-                                            t, tape, status, s);
-  }
   if (tape)
-    return launch_fhn_fast_t<30, 50, true, 4, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+    return launch_fhn_fast_t<30, 50, true, 3, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                  keys, t, tape, status, s);
-  const char *pp = getenv("PF_FHN_PP");
-  const int ppv = pp ? atoi(pp) : 2;
-  if (ppv == 2)
-    return launch_fhn_fast_t<30, 50, false, 3, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
-                                                  keys, t, tape, status, s);
-  if (ppv == 3)
-    return launch_fhn_fast_t<30, 50, false, 2, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
-                                                  keys, t, tape, status, s);
-  return launch_fhn_fast_t<30, 50, false, 4, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+  // production: 2 particles per CTA iteration, 3 resident CTAs/SM (80 regs)
+  return launch_fhn_fast_t<30, 50, false, 3, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                 keys, t, tape, status, s);
 }
 

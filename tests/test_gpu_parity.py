@@ -219,12 +219,15 @@ def test_fhn_filter_matches_golden(golden):
     assert norm_rel(out.log_norm_const, g["f_lnc"]) < 1e-12
 
 
-def test_fhn_one_interval_fp32_within_1e4(golden):
+@pytest.mark.parametrize("M,N", [(2, 16), (1, 7)])
+def test_fhn_one_interval_fp32_within_1e4(golden, M, N):
+    """The fp32 production kernel (tape-fed), incl. an odd particle count
+    (the 2-particles-per-CTA tail)."""
     g = golden["fhn"]
     om = orc.FhnConfigModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
     gm = pf.FhnLatticeModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
-    traces, _, _, noise, uni = tapes.ensemble_with_tape(om, g["obs"][:1], 2, 16, 8)
-    bank, _ = _run_bank_with_tape(gm, g["obs"][:1], 2, 16, None, noise, uni,
+    traces, _, _, noise, uni = tapes.ensemble_with_tape(om, g["obs"][:1], M, N, 8)
+    bank, _ = _run_bank_with_tape(gm, g["obs"][:1], M, N, None, noise, uni,
                                   dtype=torch.float32)
     x = bank.x[1].cpu().numpy().astype(np.float64)
     want = np.concatenate([tr.steps[0].propagated for tr in traces])

@@ -124,3 +124,24 @@ def test_bias_decays_like_one_over_N():
     assert diffs[0] > 5 * np.hypot(ses[0], ses[1])
     assert np.sign(means[0] - proxy) == np.sign(means[1] - proxy)
     assert -1.35 <= slope <= -0.65
+
+
+def test_fhn_production_bank_tracks_truth_like_cpu_reference():
+    """FH-N (cfg3 model) in production mode, fp32: the M-averaged v estimate
+    tracks the truth; its error matches the CPU reference algorithm's (fp64
+    oracle, fewer particles, so the GPU must do at least as well)."""
+    m, states, obs = orc.fhn_truth(seed=12, n_obs=6)
+    gm = pf.FhnLatticeModel(stim_row=m.stim_row, stim_col=m.stim_col)
+    out = pf.run_ensemble(gm, obs, "bootstrap", 8, 512, 3, dtype="float32",
+                          estimate="projection")
+    v_true = states[:, : m.nodes]
+    rmse_gpu = np.sqrt(((out.mean_estimates - v_true) ** 2).mean())
+    from oracle import ckernels
+
+    ckernels.install()
+    _, mean = orc.run_ensemble(m, obs, 2, 64, 4, workers=orc.cpu_cores())
+    rmse_cpu = np.sqrt(((mean[:, : m.nodes] - v_true) ** 2).mean())
+    print(f"FH-N rmse gpu(8x512, fp32) {rmse_gpu:.4f}  cpu(2x64, fp64) {rmse_cpu:.4f}")
+    assert np.all(np.isfinite(out.mean_estimates))
+    assert rmse_gpu < 0.1
+    assert rmse_gpu <= 1.2 * rmse_cpu
