@@ -29,6 +29,14 @@ def world():
     return 0, 1
 
 
+def initialized() -> bool:
+    try:
+        import torch.distributed as dist
+    except Exception:  # pragma: no cover
+        return False
+    return dist.is_available() and dist.is_initialized()
+
+
 def shard_range(n_filters: int, rank: int, world_size: int) -> tuple[int, int]:
     """Contiguous block [start, stop) of global filter ids owned by `rank`."""
     if n_filters < 1 or world_size < 1 or not 0 <= rank < world_size:
@@ -78,7 +86,7 @@ def allreduce_disjoint(t):
     """Blocking disjoint-support all-reduce (small end-of-run traces)."""
     import torch.distributed as dist
 
-    if world()[1] > 1:
+    if initialized():
         dist.all_reduce(t)
     return t
 

@@ -87,7 +87,10 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     obs = _validate(observations, variant, model)
     T = obs.shape[0]
     rank, world = dist.world()
-    if shard is False or world == 1:
+    # exchange path: any initialised process group (shard=True forces it even
+    # for world size 1, which exercises the NCCL side-stream exchange)
+    use_exch = (world > 1 and shard is not False) or (shard is True and dist.initialized())
+    if not use_exch:
         rank, world = 0, 1
     lo, hi = dist.shard_range(n_filters, rank, world) if world > 1 else (0, n_filters)
     keys = philox.filter_keys(master_seed, n_filters)
@@ -103,7 +106,7 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
                       est_row_offset=lo)
     bank.load_observations(obs)
     bank.init()
-    exch = dist.EstimateExchange(est_full) if world > 1 else None
+    exch = dist.EstimateExchange(est_full) if use_exch else None
     events = [torch.cuda.Event(enable_timing=True) for _ in range(T + 1)]
     events[0].record()
     for k in range(T):
@@ -123,7 +126,7 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     lnc_full[:, lo:hi] = bank.lnc_tr
     coll_full[:, lo:hi] = bank.coll_tr.to(torch.int32)
     st_full[lo:hi] = bank.status
-    if world > 1:
+    if use_exch:
         for t_ in (lnc_full, coll_full, st_full):
             dist.allreduce_disjoint(t_)
     torch.cuda.synchronize()
