@@ -191,6 +191,23 @@ int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t 
 int pf_ensemble_average(const double *est, int64_t T, int64_t M, int64_t dim, double *out,
                         void *stream);
 
+/* ---- auxiliary particle filter glue (filters.py:115-154) --------------- */
+/* First stage: filters whose lambda are all -inf get lambda := 0 (uniform
+ * first-stage weights, log_mean_first = 0, filters.py:136-140); coll1[f]=1. */
+int pf_apf_first_stage_prepare(pf_dtype dtype, void *lam, int64_t M, int64_t N, uint8_t *coll1,
+                               void *stream);
+/* out[j] = inner ? inner[outer[j]] : outer[j]  (state rows of the chosen
+ * first-stage ancestors: particles[ancestors] of filters.py:142). */
+int pf_compose_ancestors(const int32_t *outer, const int32_t *inner, int64_t MN, int32_t *out,
+                         void *stream);
+/* logw[j] -= lam[anc1[j]]  (filters.py:143). */
+int pf_apf_second_stage_weights(pf_dtype dtype, void *logw, const void *lam, const int32_t *anc1,
+                                int64_t MN, void *stream);
+/* After the second resampling: a second-stage collapse restores
+ * lnc_before (filters.py:146-148); collapsed |= collapsed_first. */
+int pf_apf_finish(double *lnc, const double *lnc_before, uint8_t *collapsed,
+                  const uint8_t *collapsed_first, int64_t M, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

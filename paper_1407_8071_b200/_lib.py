@@ -76,6 +76,10 @@ SIGNATURES = {
                                                 c_i32, c_u32, c_vp]),
     "pf_filter_estimate": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64,
                                           c_i64, c_vp, c_vp]),
+    "pf_apf_first_stage_prepare": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "pf_compose_ancestors": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "pf_apf_second_stage_weights": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pf_apf_finish": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pf_ensemble_average": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
 }
 

@@ -39,6 +39,7 @@ class DrawTape:
     prior: np.ndarray | None = None
     noise: list = field(default_factory=list)
     uniforms: list = field(default_factory=list)
+    uniforms_first: list = field(default_factory=list)  # auxiliary filter, first stage
 
 
 def _torch_dtype(dtype):
@@ -57,7 +58,7 @@ class FilterBank:
     def __init__(self, model, n_filters: int, n_particles: int, keys, n_steps: int, *,
                  dtype=None, tape: DrawTape | None = None, filter_offset: int = 0,
                  estimate: str = "full", est_buffer=None, est_row_offset: int = 0,
-                 reference_order: bool = True):
+                 reference_order: bool = True, variant: str = "bootstrap"):
         import torch
 
         _lib.require_cuda()
@@ -67,6 +68,9 @@ class FilterBank:
             raise ValueError("M*N per GPU must fit int32 particle indices")
         if model.kind not in ("lorenz", "fhn"):
             raise ValueError(f"model kind {model.kind!r} has no GPU descriptor")
+        if variant not in ("bootstrap", "auxiliary"):
+            raise ValueError(f"unknown filter variant {variant!r}")
+        self.variant = variant
         self.model = model
         self.M, self.N = int(n_filters), int(n_particles)
         self.MN = self.M * self.N
@@ -118,6 +122,14 @@ class FilterBank:
         # oracle mode builds the CDF in the reference's exact order (bit-exact
         # ancestors); production mode uses the parallel scan
         self.rs_flags = _lib.PF_RS_REFERENCE_ORDER if (tape is not None and reference_order) else 0
+        if variant == "auxiliary":  # apf_step scratch (filters.py:115-154)
+            self.params0 = model.params(noise_free=True)
+            self.lam = torch.empty(self.MN, dtype=self.dtype, **kw)
+            self.anc1 = torch.empty(self.MN, dtype=torch.int32, **kw)
+            self.anc_comp = torch.empty(self.MN, dtype=torch.int32, **kw)
+            self.x_tmp = torch.empty_like(self.x[0])
+            self.lnc_before = torch.empty(self.M, dtype=torch.float64, **kw)
+            self.coll1 = torch.empty(self.M, dtype=torch.uint8, **kw)
 
     # -- setup ----------------------------------------------------------------
     def load_observations(self, observations):
@@ -164,9 +176,31 @@ class FilterBank:
         self.steps_done = 0
 
     # -- one observation interval --------------------------------------------
-    def step(self, k: int):
+    def _propagate(self, params, xin, anc, xout, y_ptr, logw, t, noise):
+        s = _lib.stream_ptr()
+        if self.model.kind == "lorenz":
+            _lib.call("pf_lorenz_propagate_weight", params, self.code, _lib.ptr(xin),
+                      _lib.ptr(anc), _lib.ptr(xout), y_ptr, _lib.ptr(logw), self.M, self.N,
+                      _lib.ptr(self.keys), t, _lib.ptr(noise), _lib.ptr(self.status), s)
+        else:
+            _lib.call("pf_fhn_interval", params, self.code, _lib.ptr(xin), _lib.ptr(anc),
+                      _lib.ptr(xout), y_ptr, _lib.ptr(self.obs_idx), _lib.ptr(logw),
+                      self.M, self.N, _lib.ptr(self.keys), t, _lib.ptr(noise),
+                      _lib.ptr(self.status), s)
+
+    def _resample(self, logw, uni, t, anc_out):
+        _lib.call("pf_segmented_resample_ex", self.code, _lib.ptr(logw), self.M, self.N,
+                  _lib.ptr(uni), _lib.ptr(self.keys), t, _lib.ptr(anc_out), _lib.ptr(self.lnc),
+                  _lib.ptr(self.collapsed), _lib.ptr(self.status), _lib.ptr(self.ws),
+                  self.ws_bytes, None, None, 0, self.rs_flags, _lib.stream_ptr())
+
+    def _tape(self, lst, k):
         import torch
 
+        a = np.ascontiguousarray(lst[k][self._rows()], dtype=np.float64)
+        return torch.from_numpy(a).to(self.device)
+
+    def step(self, k: int):
         if self.obs is None:
             raise RuntimeError("load_observations() first")
         t = k + 1
@@ -174,30 +208,22 @@ class FilterBank:
         xin, xout = self.x[self.cur], self.x[1 - self.cur]
         anc = self.anc if self.steps_done > 0 else None
         y_ptr = _lib.c_vp(self.obs.data_ptr() + k * self.model.dim_y * 8)
-        noise = uni = None
+        noise = uni = uni1 = None
         if self.tape is not None:
-            noise = torch.from_numpy(np.ascontiguousarray(
-                self.tape.noise[k][self._rows()], dtype=np.float64)).to(self.device)
-            uni = torch.from_numpy(np.ascontiguousarray(
-                self.tape.uniforms[k][self._rows()], dtype=np.float64)).to(self.device)
-            self._tape_keepalive = (noise, uni)
-        if self.kernel_events is not None:
-            self.kernel_events[0].record()
-        if self.model.kind == "lorenz":
-            _lib.call("pf_lorenz_propagate_weight", self.params, self.code, _lib.ptr(xin),
-                      _lib.ptr(anc), _lib.ptr(xout), y_ptr, _lib.ptr(self.logw), self.M, self.N,
-                      _lib.ptr(self.keys), t, _lib.ptr(noise), _lib.ptr(self.status), s)
+            noise = self._tape(self.tape.noise, k)
+            uni = self._tape(self.tape.uniforms, k)
+            if self.variant == "auxiliary":
+                uni1 = self._tape(self.tape.uniforms_first, k)
+            self._tape_keepalive = (noise, uni, uni1)
+        if self.variant == "auxiliary":
+            self._apf_step(k, t, xin, xout, anc, y_ptr, noise, uni, uni1)
         else:
-            _lib.call("pf_fhn_interval", self.params, self.code, _lib.ptr(xin), _lib.ptr(anc),
-                      _lib.ptr(xout), y_ptr, _lib.ptr(self.obs_idx), _lib.ptr(self.logw),
-                      self.M, self.N, _lib.ptr(self.keys), t, _lib.ptr(noise),
-                      _lib.ptr(self.status), s)
-        if self.kernel_events is not None:
-            self.kernel_events[1].record()
-        _lib.call("pf_segmented_resample_ex", self.code, _lib.ptr(self.logw), self.M, self.N,
-                  _lib.ptr(uni), _lib.ptr(self.keys), t, _lib.ptr(self.anc), _lib.ptr(self.lnc),
-                  _lib.ptr(self.collapsed), _lib.ptr(self.status), _lib.ptr(self.ws),
-                  self.ws_bytes, None, None, 0, self.rs_flags, s)
+            if self.kernel_events is not None:
+                self.kernel_events[0].record()
+            self._propagate(self.params, xin, anc, xout, y_ptr, self.logw, t, noise)
+            if self.kernel_events is not None:
+                self.kernel_events[1].record()
+            self._resample(self.logw, uni, t, self.anc)
         est_ptr = _lib.c_vp(self.est[k].data_ptr() + self.est_row * self.est_dim * 8)
         sp, sd = self.est_strides
         _lib.call("pf_filter_estimate", self.code, _lib.ptr(xout), sp, sd, self.est_dim,
@@ -206,6 +232,30 @@ class FilterBank:
         self.coll_tr[k].copy_(self.collapsed)
         self.cur = 1 - self.cur
         self.steps_done += 1
+
+    def _apf_step(self, k, t, xin, xout, anc_prev, y_ptr, noise, uni, uni1):
+        """apf_step (filters.py:115-154) on the whole bank."""
+        s = _lib.stream_ptr()
+        # first stage: lambda = log p(y | noise-free prediction)
+        self._propagate(self.params0, xin, anc_prev, self.x_tmp, y_ptr, self.lam, t, noise)
+        _lib.call("pf_apf_first_stage_prepare", self.code, _lib.ptr(self.lam), self.M, self.N,
+                  _lib.ptr(self.coll1), s)
+        self.lnc_before.copy_(self.lnc)
+        # first-stage uniforms use a distinct Philox time word in production
+        self._resample(self.lam, uni1, t | 0x80000000, self.anc1)
+        _lib.call("pf_compose_ancestors", _lib.ptr(self.anc1), _lib.ptr(anc_prev), self.MN,
+                  _lib.ptr(self.anc_comp), s)
+        # second stage: propagate the chosen ancestors, weights / lambda[anc1]
+        if self.kernel_events is not None:
+            self.kernel_events[0].record()
+        self._propagate(self.params, xin, self.anc_comp, xout, y_ptr, self.logw, t, noise)
+        if self.kernel_events is not None:
+            self.kernel_events[1].record()
+        _lib.call("pf_apf_second_stage_weights", self.code, _lib.ptr(self.logw),
+                  _lib.ptr(self.lam), _lib.ptr(self.anc1), self.MN, s)
+        self._resample(self.logw, uni, t, self.anc)
+        _lib.call("pf_apf_finish", _lib.ptr(self.lnc), _lib.ptr(self.lnc_before),
+                  _lib.ptr(self.collapsed), _lib.ptr(self.coll1), self.M, s)
 
     def run(self, on_step=None):
         for k in range(self.T):

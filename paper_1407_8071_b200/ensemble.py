@@ -103,7 +103,7 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     est_full = torch.zeros((T, n_filters, est_dim), dtype=torch.float64, device=dev)
     bank = FilterBank(model, hi - lo, n_particles, keys[lo:hi], T, dtype=dtype, tape=tape,
                       filter_offset=lo, estimate=estimate, est_buffer=est_full,
-                      est_row_offset=lo)
+                      est_row_offset=lo, variant=variant)
     bank.load_observations(obs)
     bank.init()
     exch = dist.EstimateExchange(est_full) if use_exch else None

@@ -22,7 +22,7 @@ from .resampling import multinomial_resample_indices
 
 VARIANT_BOOTSTRAP = "bootstrap"
 VARIANT_AUXILIARY = "auxiliary"
-KNOWN_VARIANTS = (VARIANT_BOOTSTRAP,)
+KNOWN_VARIANTS = (VARIANT_BOOTSTRAP, VARIANT_AUXILIARY)
 
 
 @dataclass
@@ -89,14 +89,53 @@ def bf_step(model: StateSpaceModel, state: ParticleApproximation, y, rng) -> Par
                                  state.log_norm_const + log_mean_raw, t)
 
 
+def apf_step(model: StateSpaceModel, state: ParticleApproximation, y, rng) -> ParticleApproximation:
+    """One auxiliary step (filters.py:115-154), same control flow and draw
+    order, arithmetic on the GPU through the model hooks and L2 operators."""
+    import torch
+
+    if not model.has_point_prediction():
+        raise UnsupportedModelError("auxiliary filtering needs transition_point_prediction")
+    _check_uniform(state)
+    t = state.t + 1
+    n = state.n_particles
+    predicted = model.transition_point_prediction(state.particles, t)
+    lam = model.log_likelihood(y, predicted, t)
+    collapsed = False
+    try:
+        first_stage, log_mean_first = normalize_log_weights(lam)
+    except WeightCollapseError:
+        collapsed = True
+        lam = np.zeros(n)
+        first_stage, log_mean_first = uniform_weights(n), 0.0
+    ancestors = multinomial_resample_indices(first_stage, n, rng)
+    dev_x = torch.from_numpy(np.ascontiguousarray(state.particles)).cuda()
+    chosen = dev_x[torch.from_numpy(ancestors).cuda()].cpu().numpy()
+    propagated = model.sample_transition(chosen, t, rng)
+    d_lam = torch.from_numpy(np.ascontiguousarray(lam, dtype=np.float64)).cuda()
+    log_w = (torch.from_numpy(np.ascontiguousarray(model.log_likelihood(y, propagated, t))).cuda()
+             - d_lam[torch.from_numpy(ancestors).cuda()]).cpu().numpy()
+    try:
+        weights, log_mean_second = normalize_log_weights(log_w)
+    except WeightCollapseError:
+        return ParticleApproximation(propagated, uniform_weights(n), state.log_norm_const, t,
+                                     collapsed=True)
+    idx = multinomial_resample_indices(weights, n, rng)
+    gathered = torch.from_numpy(np.ascontiguousarray(propagated)).cuda()[
+        torch.from_numpy(idx).cuda()].cpu().numpy()
+    return ParticleApproximation(gathered, uniform_weights(n),
+                                 state.log_norm_const + log_mean_first + log_mean_second, t,
+                                 collapsed=collapsed)
+
+
 def _validate(observations, variant, model):
     obs = np.atleast_2d(np.asarray(observations, dtype=np.float64))
     if obs.shape[0] == 0:
         raise ValueError("observation sequence must be non-empty")
-    if variant == VARIANT_AUXILIARY:
-        raise UnsupportedModelError("the auxiliary variant is not on the GPU bank path yet")
     if variant not in KNOWN_VARIANTS:
         raise ValueError(f"unknown filter variant {variant!r}")
+    if variant == VARIANT_AUXILIARY and not model.has_point_prediction():
+        raise UnsupportedModelError("auxiliary filtering needs transition_point_prediction")
     if getattr(model, "dim_y", obs.shape[1]) == 1 and obs.ndim == 2 and obs.shape[1] != 1:
         obs = obs.reshape(-1, 1)
     return obs
@@ -123,7 +162,7 @@ def run_filter(model: StateSpaceModel, observations, variant: str, n_particles: 
         raise ValueError("n_particles must be >= 1")
     keys = philox.seed_key(seed)[None, :]
     bank = FilterBank(model, 1, n_particles, keys, obs.shape[0], dtype=dtype, tape=tape,
-                      estimate=estimate)
+                      estimate=estimate, variant=variant)
     bank.load_observations(obs)
     bank.init()
     events = [torch.cuda.Event(enable_timing=True) for _ in range(obs.shape[0] + 1)]

@@ -64,9 +64,12 @@ class Lorenz63Model(StateSpaceModel):
         self._prior_mean_arr = np.asarray(self.prior_mean, dtype=np.float64)
 
     # -- device descriptor ------------------------------------------------
-    def params(self, n_sub=None) -> _lib.LorenzParams:
+    def params(self, n_sub=None, noise_free=False) -> _lib.LorenzParams:
+        """Device descriptor; noise_free=True gives the point prediction
+        (transition_point_prediction, lorenz63.py:57-60)."""
         return _lib.LorenzParams(float(self.s), float(self.r), float(self.b), float(self.dt),
-                                 float(self.noise_scale), float(self.obs_var),
+                                 0.0 if noise_free else float(self.noise_scale),
+                                 float(self.obs_var),
                                  int(self.substeps if n_sub is None else n_sub), self.dim_y)
 
     def prior_sd(self) -> float:
@@ -173,7 +176,8 @@ class FhnLatticeModel(StateSpaceModel):
         self.dim_y = int(self.obs_indices.shape[0])
         self.sig_sqdt = self.noise_std * math.sqrt(self.dt)
 
-    def params(self, n_sub=None) -> _lib.FhnParams:
+    def params(self, n_sub=None, noise_free=False) -> _lib.FhnParams:
+        """Device descriptor; noise_free=True gives the point prediction."""
         p = _lib.FhnParams()
         p.rows, p.cols = self.rows, self.cols
         p.n_sub = int(self.substeps if n_sub is None else n_sub)
@@ -183,7 +187,7 @@ class FhnLatticeModel(StateSpaceModel):
             p.cubic[i] = float(self.cubic[i])
         for i in range(3):
             p.beta[i] = float(self.beta[i])
-        p.sig_v = p.sig_w = float(self.sig_sqdt)
+        p.sig_v = p.sig_w = 0.0 if noise_free else float(self.sig_sqdt)
         p.degree_drive = -1.0
         p.obs_var = float(self.obs_var)
         return p

@@ -110,6 +110,22 @@ class RefFhnCfg(StateSpaceModel):
             V = V + self.sig * zv
         return np.concatenate([U.reshape(n, -1), V.reshape(n, -1)], axis=1)
 
+    def _advance(self, x_prev, zs):
+        n = x_prev.shape[0]
+        U = x_prev[:, : self.nodes].reshape(n, self.rows, self.cols)
+        V = x_prev[:, self.nodes:].reshape(n, self.rows, self.cols)
+        for zu, zv in zs:
+            U, V = accel.fhn_euler_block_numpy(
+                U, V, -self.deg * U, zu, self.dt, 1.0, (-1.0, 1.13, -0.13, 0.0),
+                (0.01, -0.005, 0.0), self.sig)
+            V = V + self.sig * zv
+        return np.concatenate([U.reshape(n, -1), V.reshape(n, -1)], axis=1)
+
+    def transition_point_prediction(self, x_prev, t):
+        x_prev = np.atleast_2d(np.asarray(x_prev, dtype=np.float64))
+        z = np.zeros((x_prev.shape[0], self.rows, self.cols))
+        return self._advance(x_prev, [(z, z)] * self.substeps)
+
     def log_likelihood(self, y, x, t):
         y = np.asarray(y, dtype=np.float64).reshape(-1)
         x = np.atleast_2d(np.asarray(x, dtype=np.float64))
@@ -147,9 +163,9 @@ class _Recorder:
         ref_filters.multinomial_resample_indices = self._orig
 
 
-def _filter_with_steps(model, obs, n, seed):
+def _filter_with_steps(model, obs, n, seed, variant="bootstrap"):
     with _Recorder() as rec:
-        out = parpf.run_filter(model, obs, "bootstrap", n, seed)
+        out = parpf.run_filter(model, obs, variant, n, seed)
     return out, rec.calls
 
 
@@ -237,6 +253,21 @@ def gen_lorenz():
     outc = parpf.run_filter(model, obs_c, "bootstrap", 32, 11)
     d["c_obs"], d["c_est"], d["c_lnc"] = obs_c, outc.estimates, outc.log_norm_const
     d["c_steps"] = np.array(outc.collapse_steps)
+    # auxiliary filter (filters.py:115-154): two resampling calls per step
+    outa, calls = _filter_with_steps(model, obs[:12], 48, np.random.SeedSequence(4242),
+                                     "auxiliary")
+    d["a_est"], d["a_lnc"] = outa.estimates, outa.log_norm_const
+    d["a_u1"] = np.stack([c[0] for c in calls[0::2]])
+    d["a_anc1"] = np.stack([c[1] for c in calls[0::2]])
+    d["a_u2"] = np.stack([c[0] for c in calls[1::2]])
+    d["a_anc2"] = np.stack([c[1] for c in calls[1::2]])
+    ensa = parpf.run_ensemble(model, obs[:12], "auxiliary", 3, 64, 8)
+    d["ae_mean"] = ensa.mean_estimates
+    d["ae_lnc"] = np.stack([fo.log_norm_const for fo in ensa.filter_outputs])
+    # auxiliary collapse: infinite observation -> both stages collapse
+    outac = parpf.run_filter(model, obs_c, "auxiliary", 16, 12)
+    d["ac_est"], d["ac_lnc"] = outac.estimates, outac.log_norm_const
+    d["ac_steps"] = np.array(outac.collapse_steps)
     np.savez_compressed(os.path.join(HERE, "lorenz.npz"), **d)
 
 
@@ -255,6 +286,11 @@ def gen_fhn():
     ens = parpf.run_ensemble(model, obs[:2], "bootstrap", 2, 4, 17)
     d["e_mean_v"] = ens.mean_estimates[:, : m.nodes]
     d["e_lnc"] = np.stack([fo.log_norm_const for fo in ens.filter_outputs])
+    outa, calls = _filter_with_steps(model, obs, 6, np.random.SeedSequence(5151), "auxiliary")
+    d["a_est_v"] = outa.estimates[:, : m.nodes]
+    d["a_lnc"] = outa.log_norm_const
+    d["a_anc1"] = np.stack([c[1] for c in calls[0::2]])
+    d["a_anc2"] = np.stack([c[1] for c in calls[1::2]])
     np.savez_compressed(os.path.join(HERE, "fhn.npz"), **d)
 
 

@@ -1,0 +1,145 @@
+"""Auxiliary particle filter (filters.py:115-154) on the GPU bank, against the
+oracle and the golden fixtures generated from the reference."""
+
+import numpy as np
+import pytest
+
+from oracle import parpf_oracle as orc
+from oracle import tapes
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1407_8071_b200 as pf  # noqa: E402
+
+
+def norm_rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _lorenz(truth0):
+    om = orc.LorenzConfigModel(prior_mean=tuple(truth0))
+    gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(truth0), prior_var=1.0)
+    return om, gm
+
+
+def _run_apf_bank(gm, obs, M, N, prior, noise, uni, uni1, dtype=None):
+    tape = pf.DrawTape(prior=prior, noise=noise, uniforms=uni, uniforms_first=uni1)
+    bank = pf.FilterBank(gm, M, N, np.zeros((M, 2), np.uint32), len(obs), tape=tape,
+                         dtype=dtype, variant="auxiliary")
+    bank.load_observations(obs)
+    bank.init()
+    a1, a2 = [], []
+    off = np.arange(M)[:, None] * N
+    for k in range(len(obs)):
+        bank.step(k)
+        a1.append(bank.anc1.cpu().numpy().reshape(M, N) - off)
+        a2.append(bank.anc.cpu().numpy().reshape(M, N) - off)
+    torch.cuda.synchronize()
+    bank.check_status()
+    return bank, a1, a2
+
+
+def test_lorenz_apf_bank_oracle_mode_bit_exact(golden):
+    g = golden["lorenz"]
+    om, gm = _lorenz(g["truth0"])
+    obs = g["obs"][:12]
+    traces, mean, prior, noise, uni, uni1 = tapes.ensemble_with_tape(om, obs, 3, 64, 8,
+                                                                     variant="auxiliary")
+    assert np.array_equal(mean, g["ae_mean"])  # oracle == reference fixture
+    bank, a1, a2 = _run_apf_bank(gm, obs, 3, 64, prior, noise, uni, uni1)
+    for k in range(len(obs)):
+        assert np.array_equal(a1[k], np.stack([tr.steps[k].anc_first for tr in traces])), k
+        assert np.array_equal(a2[k], np.stack([tr.steps[k].ancestors for tr in traces])), k
+    assert norm_rel(bank.est.cpu().numpy(), np.stack([t.estimates for t in traces], 1)) < 1e-12
+    assert norm_rel(bank.lnc_tr.cpu().numpy(), g["ae_lnc"].T) < 1e-12
+
+
+def test_lorenz_apf_run_filter_matches_golden(golden):
+    g = golden["lorenz"]
+    om, gm = _lorenz(g["truth0"])
+    obs = g["obs"][:12]
+    rec = orc.TapeRecorder(np.random.SeedSequence(4242))
+    tr = orc.run_filter(om, obs, 48, rec, keep_steps=True, variant="auxiliary")
+    tape = pf.DrawTape(tr.prior_noise[None], [s.noise[None] for s in tr.steps],
+                       [s.u[None] for s in tr.steps], [s.u_first[None] for s in tr.steps])
+    out = pf.run_filter(gm, obs, "auxiliary", 48, 4242, tape=tape)
+    assert out.variant == "auxiliary"
+    assert norm_rel(out.estimates, g["a_est"]) < 1e-12
+    assert norm_rel(out.log_norm_const, g["a_lnc"]) < 1e-12
+
+
+def test_lorenz_apf_collapse_semantics(golden):
+    g = golden["lorenz"]
+    om, gm = _lorenz(g["truth0"])
+    rec = orc.TapeRecorder(12)
+    tr = orc.run_filter(om, g["c_obs"], 16, rec, keep_steps=True, variant="auxiliary")
+    assert tr.collapse_steps == list(g["ac_steps"])
+    nan = np.full(16, np.nan)
+    tape = pf.DrawTape(tr.prior_noise[None], [s.noise[None] for s in tr.steps],
+                       [(s.u if s.u is not None else nan)[None] for s in tr.steps],
+                       [s.u_first[None] for s in tr.steps])
+    out = pf.run_filter(gm, g["c_obs"], "auxiliary", 16, 12, tape=tape)
+    assert out.collapse_steps == list(g["ac_steps"])
+    assert norm_rel(out.estimates, g["ac_est"]) < 1e-12
+    assert norm_rel(out.log_norm_const, g["ac_lnc"]) < 1e-12
+
+
+def test_fhn_apf_bank_oracle_mode(golden):
+    g = golden["fhn"]
+    om = orc.FhnConfigModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    gm = pf.FhnLatticeModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
+    rec = orc.TapeRecorder(np.random.SeedSequence(5151))
+    tr = orc.run_filter(om, g["obs"], 6, rec, keep_steps=True, variant="auxiliary")
+    assert np.array_equal(np.stack([s.anc_first for s in tr.steps]), g["a_anc1"])
+    tape = pf.DrawTape(None, [s.noise.reshape(om.substeps, 2, 6, -1)[None] for s in tr.steps],
+                       [s.u[None] for s in tr.steps], [s.u_first[None] for s in tr.steps])
+    bank, a1, a2 = _run_apf_bank(gm, g["obs"], 1, 6, None, tape.noise, tape.uniforms,
+                                 tape.uniforms_first)
+    assert np.array_equal(np.stack([a[0] for a in a1]), g["a_anc1"])
+    assert np.array_equal(np.stack([a[0] for a in a2]), g["a_anc2"])
+    assert norm_rel(bank.est.cpu().numpy()[:, 0, : om.nodes], g["a_est_v"]) < 1e-12
+    assert norm_rel(bank.lnc_tr.cpu().numpy()[:, 0], g["a_lnc"]) < 1e-12
+
+
+def test_apf_production_mode_tracks_truth_and_is_deterministic():
+    truth0, states, obs = orc.lorenz_truth(seed=9, n_obs=30)
+    _, gm = _lorenz(truth0)
+    a = pf.run_ensemble(gm, obs, "auxiliary", 4, 1000, 2)
+    b = pf.run_ensemble(gm, obs, "auxiliary", 4, 1000, 2)
+    boot = pf.run_ensemble(gm, obs, "bootstrap", 4, 1000, 2)
+    assert a.same_result(b)
+    mse_a = np.mean((a.mean_estimates - states) ** 2)
+    mse_b = np.mean((boot.mean_estimates - states) ** 2)
+    print(f"APF mse {mse_a:.4f} bootstrap mse {mse_b:.4f}")
+    assert mse_a < 2.0 and mse_a < 2.0 * mse_b
+
+
+def test_apf_fhn_production_fp32_runs():
+    m, states, obs = orc.fhn_truth(seed=3, n_obs=3)
+    gm = pf.FhnLatticeModel(stim_row=m.stim_row, stim_col=m.stim_col)
+    out = pf.run_ensemble(gm, obs, "auxiliary", 2, 256, 1, dtype="float32",
+                          estimate="projection")
+    err = np.sqrt(((out.mean_estimates - states[:, : m.nodes]) ** 2).mean())
+    assert np.isfinite(err) and err < 0.1
+
+
+def test_apf_hook_level_step_matches_oracle(golden):
+    """pf.apf_step over host containers consumes the Generator like the
+    reference and reproduces the oracle step."""
+    g = golden["lorenz"]
+    om, gm = _lorenz(g["truth0"])
+    st = pf.bf_init(gm, 32, np.random.default_rng(3))
+    st1 = pf.apf_step(gm, st, g["obs"][0], np.random.default_rng(4))
+    x0 = orc.LorenzConfigModel(prior_mean=tuple(g["truth0"]))
+    ox = x0.sample_prior(np.random.default_rng(3), 32)
+    steps = []
+    x1, lnc1, _ = orc._apf_step(om, ox, 0.0, g["obs"][0], 1, np.random.default_rng(4), True,
+                                steps)
+    assert norm_rel(st1.particles, x1) < 1e-12
+    assert abs(st1.log_norm_const - lnc1) < 1e-12

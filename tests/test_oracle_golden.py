@@ -181,3 +181,44 @@ def test_ckernels_resample_golden(golden):
     for i in range(int(g["ri_count"])):
         assert np.array_equal(_ck().resample_indices(g[f"ri_cum_{i}"], g[f"ri_u_{i}"]),
                               g[f"ri_idx_{i}"])
+
+
+# ---- auxiliary particle filter (filters.py:115-154) -----------------------
+
+def test_lorenz_apf_filter_golden(golden):
+    g = golden["lorenz"]
+    tr = orc.run_filter(_lorenz_model(g), g["obs"][:12], 48, np.random.SeedSequence(4242),
+                        keep_steps=True, variant="auxiliary")
+    assert np.array_equal(tr.estimates, g["a_est"])
+    assert np.array_equal(tr.log_norm_const, g["a_lnc"])
+    assert np.array_equal(np.stack([s.anc_first for s in tr.steps]), g["a_anc1"])
+    assert np.array_equal(np.stack([s.u_first for s in tr.steps]), g["a_u1"])
+    assert np.array_equal(np.stack([s.ancestors for s in tr.steps]), g["a_anc2"])
+    assert np.array_equal(np.stack([s.u for s in tr.steps]), g["a_u2"])
+
+
+def test_lorenz_apf_ensemble_golden(golden):
+    g = golden["lorenz"]
+    traces, mean = orc.run_ensemble(_lorenz_model(g), g["obs"][:12], 3, 64, 8,
+                                    variant="auxiliary")
+    assert np.array_equal(mean, g["ae_mean"])
+    assert np.array_equal(np.stack([t.log_norm_const for t in traces]), g["ae_lnc"])
+
+
+def test_lorenz_apf_collapse_golden(golden):
+    g = golden["lorenz"]
+    tr = orc.run_filter(_lorenz_model(g), g["c_obs"], 16, 12, variant="auxiliary")
+    assert tr.collapse_steps == list(g["ac_steps"])
+    assert np.array_equal(tr.estimates, g["ac_est"])
+    assert np.array_equal(tr.log_norm_const, g["ac_lnc"])
+
+
+def test_fhn_apf_filter_golden(golden):
+    g = golden["fhn"]
+    m = _fhn_model(g)
+    tr = orc.run_filter(m, g["obs"], 6, np.random.SeedSequence(5151), keep_steps=True,
+                        variant="auxiliary")
+    assert np.array_equal(tr.estimates[:, : m.nodes], g["a_est_v"])
+    assert np.array_equal(tr.log_norm_const, g["a_lnc"])
+    assert np.array_equal(np.stack([s.anc_first for s in tr.steps]), g["a_anc1"])
+    assert np.array_equal(np.stack([s.ancestors for s in tr.steps]), g["a_anc2"])
