@@ -107,6 +107,35 @@ __device__ __forceinline__ int lower_bound_tm(const double *c, int n, double x) 
   return lo;
 }
 
+// Forward search from k for the first index >= k with c(i) >= x (n if none):
+// a short linear probe, then galloping + binary search.  Keeps the merge
+// O(log gap) per uniform when the CDF has long flat runs (weights that
+// underflow below the CDF's ulp, e.g. sigma = 10 log weights).
+template <typename I, typename F>
+__device__ __forceinline__ I advance_to(F c, I k, I n, double x) {
+  // common case: the next uniform lands within a few CDF entries
+  int probe = 0;
+  while (k < n && c(k) < x) {
+    ++k;
+    if (++probe == 8) break;
+  }
+  if (probe < 8 || k >= n || !(c(k) < x)) return k;
+  I lo = k, step = 1;  // invariant: c(lo - 1) < x
+  while (lo + step - 1 < n && c(lo + step - 1) < x) {
+    lo += step;
+    step <<= 1;
+  }
+  I hi = lo + step - 1 < n ? lo + step - 1 : n;  // c(hi) >= x or hi == n
+  while (lo < hi) {
+    const I mid = (lo + hi) >> 1;
+    if (c(mid) < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
 template <typename TW, int MODE, int THREADS, int IPT, bool GATHER>
 __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
     const TW *__restrict__ logw, int32_t N, const double *__restrict__ u_tape,
@@ -225,7 +254,8 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
 #pragma unroll
     for (int q = 0; q < IPT; ++q) {
       if (i0 + q < N) {
-        while (k < N && s_cum[cdf_slot<THREADS, IPT>(k)] < u[q]) ++k;
+        k = advance_to<int>([&](int i) { return s_cum[cdf_slot<THREADS, IPT>(i)]; }, k,
+                            static_cast<int>(N), u[q]);
         av[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
       } else {
         av[q] = 0;
@@ -500,7 +530,7 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_merge(
   int64_t k = lower_bound_f64_64(cum, N, s[j0]);
   for (int j = j0; j < j1; ++j) {
     const double u = s[j];
-    while (k < N && __ldg(cum + k) < u) ++k;
+    k = advance_to<int64_t>([&](int64_t i) { return __ldg(cum + i); }, k, N, u);
     anc[base + i0 + j] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
   }
 }
@@ -656,7 +686,7 @@ __global__ void __launch_bounds__(256) resample_bank_exact_kernel(
   if (j0 < j1) {
     int k = lower_bound_f64(s_cum, N, s_a[j0]);
     for (int j = j0; j < j1; ++j) {
-      while (k < N && s_cum[k] < s_a[j]) ++k;
+      k = advance_to<int>([&](int i) { return s_cum[i]; }, k, N, s_a[j]);
       anc[base + j] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
     }
   }

@@ -167,6 +167,8 @@ class FhnLatticeModel(StateSpaceModel):
             raise ValueError("substeps must be >= 1")
         if self.obs_var <= 0:
             raise ValueError("obs_var must be positive")
+        if min(self.rows, self.cols) < self.electrode_side:
+            raise ValueError("electrode grid does not fit on the lattice")
         self.nodes = self.rows * self.cols
         self.dim_x = 2 * self.nodes
         self.obs_indices = electrode_indices(self.rows, self.cols, self.electrode_side,
