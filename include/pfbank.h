@@ -191,6 +191,45 @@ int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t 
 int pf_ensemble_average(const double *est, int64_t T, int64_t M, int64_t dim, double *out,
                         void *stream);
 
+/* ---- native bank driver ------------------------------------------------ */
+/* Production-mode (Philox) bootstrap bank: runs observations k0..k0+n-1 back
+ * to back (propagate+weight, segmented resample, estimate, lnc/collapse trace
+ * copies per observation) without returning to the host - the loop of
+ * run_filter (filters.py:184-191) for every filter at once.  `cur` is the
+ * index of the state buffer holding the current particles; after the call the
+ * current buffer is cur ^ (n_steps & 1).  have_ancestors = 0 on the first
+ * interval (the prior has no ancestors). */
+#define PF_MODEL_LORENZ 0
+#define PF_MODEL_FHN 1
+typedef struct pf_bank_desc {
+  int32_t model; /* PF_MODEL_* */
+  pf_dtype dtype;
+  int64_t M, N;
+  const pf_lorenz_params *lorenz; /* host */
+  const pf_fhn_params *fhn;       /* host */
+  const int32_t *obs_idx;         /* FH-N electrodes */
+  void *x[2];                     /* state double buffer */
+  void *logw;
+  int32_t *anc;
+  double *lnc;
+  uint8_t *collapsed;
+  uint32_t *status;
+  const uint32_t *keys;
+  void *ws;
+  size_t ws_bytes;
+  const double *obs; /* (T, dim_y) */
+  int32_t dim_y;
+  double *est; /* step k's estimates at est + k*est_step_stride + est_offset */
+  int64_t est_step_stride, est_offset, est_stride_p, est_stride_d;
+  int32_t est_dim;
+  double *lnc_trace;        /* (T, M) or NULL */
+  uint8_t *collapsed_trace; /* (T, M) or NULL */
+  float *prop_ms; /* host (n_steps) or NULL: propagate-kernel durations; the call then
+                     waits for the last propagate to finish before returning */
+} pf_bank_desc;
+int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
+                int32_t have_ancestors, void *stream);
+
 /* ---- auxiliary particle filter glue (filters.py:115-154) --------------- */
 /* First stage: filters whose lambda are all -inf get lambda := 0 (uniform
  * first-stage weights, log_mean_first = 0, filters.py:136-140); coll1[f]=1. */

@@ -45,6 +45,20 @@ class FhnParams(ctypes.Structure):
                 ("obs_var", c_f64)]
 
 
+class BankDesc(ctypes.Structure):
+    _fields_ = [("model", c_i32), ("dtype", ctypes.c_int), ("M", c_i64), ("N", c_i64),
+                ("lorenz", ctypes.POINTER(LorenzParams)), ("fhn", ctypes.POINTER(FhnParams)),
+                ("obs_idx", c_vp), ("x", c_vp * 2), ("logw", c_vp), ("anc", c_vp), ("lnc", c_vp),
+                ("collapsed", c_vp), ("status", c_vp), ("keys", c_vp), ("ws", c_vp),
+                ("ws_bytes", c_sz), ("obs", c_vp), ("dim_y", c_i32), ("est", c_vp),
+                ("est_step_stride", c_i64), ("est_offset", c_i64), ("est_stride_p", c_i64),
+                ("est_stride_d", c_i64), ("est_dim", c_i32), ("lnc_trace", c_vp),
+                ("collapsed_trace", c_vp), ("prop_ms", ctypes.POINTER(ctypes.c_float))]
+
+
+PF_MODEL_LORENZ = 0
+PF_MODEL_FHN = 1
+
 # name -> (restype, argtypes); must match include/pfbank.h exactly
 SIGNATURES = {
     "pf_last_error": (ctypes.c_char_p, []),
@@ -76,6 +90,7 @@ SIGNATURES = {
                                                 c_i32, c_u32, c_vp]),
     "pf_filter_estimate": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64,
                                           c_i64, c_vp, c_vp]),
+    "pf_bank_run": (ctypes.c_int, [ctypes.POINTER(BankDesc), c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pf_apf_first_stage_prepare": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "pf_compose_ancestors": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "pf_apf_second_stage_weights": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp]),

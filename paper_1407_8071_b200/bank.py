@@ -119,6 +119,7 @@ class FilterBank:
         self.cur = 0
         self.steps_done = 0
         self.kernel_events = None  # optional (start, end) CUDA events around propagate
+        self._desc = None  # cached pf_bank_desc (buffers are fixed for the bank's lifetime)
         # oracle mode builds the CDF in the reference's exact order (bit-exact
         # ancestors); production mode uses the parallel scan
         self.rs_flags = _lib.PF_RS_REFERENCE_ORDER if (tape is not None and reference_order) else 0
@@ -141,10 +142,12 @@ class FilterBank:
         if obs.shape[0] < self.T:
             raise ValueError("fewer observations than steps")
         self.obs = torch.from_numpy(np.ascontiguousarray(obs[: self.T])).to(self.device)
+        self._desc = None
 
     def set_observation_buffer(self, obs_device):
         """Use a caller-owned (T, dim_y) float64 device tensor (bench/e2e)."""
         self.obs = obs_device
+        self._desc = None
 
     def _rows(self):
         return slice(self.offset, self.offset + self.M)
@@ -200,9 +203,68 @@ class FilterBank:
         a = np.ascontiguousarray(lst[k][self._rows()], dtype=np.float64)
         return torch.from_numpy(a).to(self.device)
 
+    def _native_ok(self):
+        return (self.tape is None and self.variant == "bootstrap"
+                and self.kernel_events is None)
+
+    def _bank_desc(self):
+        import ctypes
+
+        d = _lib.BankDesc()
+        d.model = _lib.PF_MODEL_LORENZ if self.model.kind == "lorenz" else _lib.PF_MODEL_FHN
+        d.dtype = self.code
+        d.M, d.N = self.M, self.N
+        if self.model.kind == "lorenz":
+            d.lorenz = ctypes.pointer(self.params)
+        else:
+            d.fhn = ctypes.pointer(self.params)
+            d.obs_idx = self.obs_idx.data_ptr()
+        d.x[0], d.x[1] = self.x[0].data_ptr(), self.x[1].data_ptr()
+        d.logw, d.anc, d.lnc = self.logw.data_ptr(), self.anc.data_ptr(), self.lnc.data_ptr()
+        d.collapsed, d.status = self.collapsed.data_ptr(), self.status.data_ptr()
+        d.keys, d.ws, d.ws_bytes = self.keys.data_ptr(), self.ws.data_ptr(), self.ws_bytes
+        d.obs, d.dim_y = self.obs.data_ptr(), self.model.dim_y
+        d.est = self.est.data_ptr()
+        d.est_step_stride = self.est.stride(0)
+        d.est_offset = self.est_row * self.est_dim
+        d.est_stride_p, d.est_stride_d = self.est_strides
+        d.est_dim = self.est_dim
+        d.lnc_trace = self.lnc_tr.data_ptr()
+        d.collapsed_trace = self.coll_tr.data_ptr()
+        return d
+
+    def run_native(self, k0: int, n_steps: int, time_propagate: bool = False):
+        """Observations k0..k0+n_steps-1 in one native call (pf_bank_run).
+
+        time_propagate=True returns the per-interval durations (ms) of the
+        propagate kernel, measured with CUDA events on the launch stream."""
+        import ctypes
+
+        if self.obs is None:
+            raise RuntimeError("load_observations() first")
+        if not self._native_ok():
+            raise RuntimeError("run_native: production bootstrap banks only")
+        if self._desc is None:
+            self._desc = self._bank_desc()
+        ms = None
+        if time_propagate and n_steps > 0:
+            ms = (ctypes.c_float * n_steps)()
+            self._desc.prop_ms = ctypes.cast(ms, ctypes.POINTER(ctypes.c_float))
+        try:
+            _lib.call("pf_bank_run", self._desc, k0, n_steps, self.cur,
+                      1 if self.steps_done > 0 else 0, _lib.stream_ptr())
+        finally:
+            self._desc.prop_ms = None
+        self.cur ^= n_steps & 1
+        self.steps_done += n_steps
+        return None if ms is None else list(ms)
+
     def step(self, k: int):
         if self.obs is None:
             raise RuntimeError("load_observations() first")
+        if self._native_ok():
+            self.run_native(k, 1)
+            return
         t = k + 1
         s = _lib.stream_ptr()
         xin, xout = self.x[self.cur], self.x[1 - self.cur]
@@ -258,6 +320,9 @@ class FilterBank:
                   _lib.ptr(self.collapsed), _lib.ptr(self.coll1), self.M, s)
 
     def run(self, on_step=None):
+        if on_step is None and self._native_ok():
+            self.run_native(0, self.T)
+            return
         for k in range(self.T):
             self.step(k)
             if on_step is not None:

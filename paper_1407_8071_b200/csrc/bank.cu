@@ -1,0 +1,93 @@
+// Native bank driver: runs observation intervals back to back from C++.
+//
+// The per-observation loop of run_filter (filters.py:184-191) and the
+// per-filter loop of run_ensemble (ensemble.py:96-99) collapse into one call
+// that enqueues, for each observation t, the propagate+weight kernel, the
+// segmented resample, the estimate and two trace copies - no host round trip
+// and no Python in between, so launch-bound configurations (small banks)
+// run at the device's launch rate.
+#include "common.cuh"
+
+#include <vector>
+
+extern "C" int pf_lorenz_propagate_weight(const pf_lorenz_params *, pf_dtype, const void *,
+                                          const int32_t *, void *, const double *, void *,
+                                          int64_t, int64_t, const uint32_t *, uint32_t,
+                                          const double *, uint32_t *, void *);
+extern "C" int pf_fhn_interval(const pf_fhn_params *, pf_dtype, const void *, const int32_t *,
+                               void *, const double *, const int32_t *, void *, int64_t, int64_t,
+                               const uint32_t *, uint32_t, const double *, uint32_t *, void *);
+
+using namespace pf;
+
+extern "C" {
+
+int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
+                int32_t have_ancestors, void *stream) {
+  PF_REQUIRE(d && n_steps >= 0 && k0 >= 0 && (cur == 0 || cur == 1), "pf_bank_run: bad arguments");
+  PF_REQUIRE(d->model == PF_MODEL_LORENZ ? d->lorenz != nullptr
+                                         : (d->model == PF_MODEL_FHN && d->fhn && d->obs_idx),
+             "pf_bank_run: model descriptor missing");
+  PF_REQUIRE(d->x[0] && d->x[1] && d->logw && d->anc && d->lnc && d->collapsed && d->status &&
+                 d->keys && d->obs && d->est,
+             "pf_bank_run: null buffer");
+  const cudaStream_t s = as_stream(stream);
+  const int64_t MN = d->M * d->N;
+  // optional per-interval timing of the propagate kernel (the dominant one)
+  struct Events {
+    std::vector<cudaEvent_t> e;
+    ~Events() {
+      for (cudaEvent_t x : e) cudaEventDestroy(x);
+    }
+  } evs;
+  cudaEvent_t *ev = nullptr;
+  if (d->prop_ms && n_steps > 0) {
+    evs.e.resize(2 * static_cast<size_t>(n_steps));
+    for (auto &x : evs.e) cudaEventCreate(&x);
+    ev = evs.e.data();
+  }
+  for (int32_t i = 0; i < n_steps; ++i) {
+    const int32_t k = k0 + i;
+    const uint32_t t = static_cast<uint32_t>(k + 1);
+    const void *xin = d->x[cur];
+    void *xout = d->x[cur ^ 1];
+    const int32_t *anc = (have_ancestors || i > 0) ? d->anc : nullptr;
+    const double *y = d->obs + static_cast<int64_t>(k) * d->dim_y;
+    int rc;
+    if (ev) cudaEventRecord(ev[2 * i], s);
+    if (d->model == PF_MODEL_LORENZ)
+      rc = pf_lorenz_propagate_weight(d->lorenz, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
+                                      d->keys, t, nullptr, d->status, stream);
+    else
+      rc = pf_fhn_interval(d->fhn, d->dtype, xin, anc, xout, y, d->obs_idx, d->logw, d->M, d->N,
+                           d->keys, t, nullptr, d->status, stream);
+    if (ev) cudaEventRecord(ev[2 * i + 1], s);
+    if (rc) return rc;
+    rc = pf_segmented_resample_ex(d->dtype, d->logw, d->M, d->N, nullptr, d->keys, t, d->anc,
+                                  d->lnc, d->collapsed, d->status, d->ws, d->ws_bytes, nullptr,
+                                  nullptr, 0, 0u, stream);
+    if (rc) return rc;
+    double *est = d->est + static_cast<int64_t>(k) * d->est_step_stride + d->est_offset;
+    rc = pf_filter_estimate(d->dtype, xout, d->est_stride_p, d->est_stride_d, d->est_dim, d->anc,
+                            d->M, d->N, est, stream);
+    if (rc) return rc;
+    if (d->lnc_trace &&
+        cudaMemcpyAsync(d->lnc_trace + static_cast<int64_t>(k) * d->M, d->lnc,
+                        d->M * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return check_launch("pf_bank_run(lnc trace)");
+    if (d->collapsed_trace &&
+        cudaMemcpyAsync(d->collapsed_trace + static_cast<int64_t>(k) * d->M, d->collapsed,
+                        d->M * sizeof(uint8_t), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return check_launch("pf_bank_run(collapse trace)");
+    cur ^= 1;
+  }
+  (void)MN;
+  if (ev) {
+    cudaEventSynchronize(ev[2 * n_steps - 1]);
+    for (int32_t i = 0; i < n_steps; ++i)
+      cudaEventElapsedTime(&d->prop_ms[i], ev[2 * i], ev[2 * i + 1]);
+  }
+  return check_launch("pf_bank_run");
+}
+
+}  // extern "C"
