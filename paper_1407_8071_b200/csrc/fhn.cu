@@ -489,12 +489,11 @@ static int launch_fhn(const FhnConsts &c, const void *x_in, const int32_t *anc, 
   return check_launch("pf_fhn_interval");
 }
 
-template <int ROWS, int COLS, bool TAPE, int MINB, int PP>
+template <int ROWS, int COLS, bool TAPE, int MINB, int PP, int R = kFhnRows>
 static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
                              const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                              int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
                              uint32_t *status, cudaStream_t s) {
-  constexpr int R = kFhnRows;
   constexpr int threads = (((ROWS + R - 1) / R * COLS) + 31) / 32 * 32;
   static_assert(threads <= 256, "lattice too large for the fast kernel");
   const size_t smem = PP * 2 * static_cast<size_t>((ROWS + 2) * (COLS + 2)) * sizeof(float);

@@ -432,3 +432,54 @@ def test_resample_gather_fused_matches_unfused(M, N):
     a = anc.cpu().numpy().astype(np.int64)
     assert np.array_equal(a.reshape(M, N) - (np.arange(M) * N)[:, None], anc_ref)
     assert torch.equal(xo, x[:, anc.long()])
+
+
+# ---------------------------------------------------------------- edge cases
+
+@pytest.mark.parametrize("M,N", [(1, 1), (3, 1), (5, 7), (2, 257), (1, 8192), (2, 9000)])
+def test_lorenz_bank_edge_sizes_bit_exact(M, N):
+    """Single particle, odd and non-power-of-two N, the bank/wide boundary
+    (8192 / 9000 -> wide path): ancestors bit-exact vs the oracle."""
+    truth0, _, obs = orc.lorenz_truth(seed=M * 31 + N, n_obs=3)
+    om, gm = _lorenz_models(truth0)
+    traces, mean, prior, noise, uni = tapes.ensemble_with_tape(om, obs, M, N, 77)
+    bank, ancs = _run_bank_with_tape(gm, obs, M, N, prior, noise, uni)
+    for k in range(len(obs)):
+        assert np.array_equal(ancs[k], np.stack([tr.steps[k].ancestors for tr in traces])), k
+    assert norm_rel(bank.est.cpu().numpy(), np.stack([tr.estimates for tr in traces], 1)) < 1e-12
+    assert norm_rel(bank.lnc_tr.cpu().numpy(),
+                    np.stack([tr.log_norm_const for tr in traces], 1)) < 1e-12
+
+
+def test_single_particle_filter_is_deterministic_copy():
+    """N=1: every step resamples the only particle (weights [1.0])."""
+    truth0, _, obs = orc.lorenz_truth(seed=2, n_obs=4)
+    _, gm = _lorenz_models(truth0)
+    out = pf.run_filter(gm, obs, "bootstrap", 1, 3)
+    assert out.estimates.shape == (4, 3) and np.all(np.isfinite(out.estimates))
+    apf = pf.run_filter(gm, obs, "auxiliary", 1, 3)
+    assert apf.estimates.shape == (4, 3)
+
+
+def test_stock_lorenz_model_observing_x1():
+    """The stock reference model (obs of x1 only, 100 substeps, prior
+    LORENZ_PRIOR_MEAN / var 10) through the bank, oracle mode, fp64."""
+    from oracle.parpf_oracle import LorenzConfigModel
+
+    om = LorenzConfigModel(substeps=100, noise_scale=1.0, obs_var=0.5,
+                           prior_mean=pf.LORENZ_PRIOR_MEAN, prior_var=10.0)
+    om.dim_y = 1
+
+    def ll(y, x, t, _m=om):
+        r = float(np.asarray(y).reshape(-1)[0]) - np.asarray(x)[:, 0]
+        return -(r * r) / (2.0 * _m.obs_var)
+
+    om.log_likelihood = ll
+    rng = np.random.default_rng(0)
+    obs = (np.array(pf.LORENZ_PRIOR_MEAN)[0] + rng.normal(size=(4, 1)))
+    traces, mean, prior, noise, uni = tapes.ensemble_with_tape(om, obs, 2, 50, 5)
+    gm = pf.Lorenz63Model()
+    bank, ancs = _run_bank_with_tape(gm, obs, 2, 50, prior, noise, uni)
+    for k in range(len(obs)):
+        assert np.array_equal(ancs[k], np.stack([tr.steps[k].ancestors for tr in traces]))
+    assert norm_rel(bank.est.cpu().numpy(), np.stack([tr.estimates for tr in traces], 1)) < 1e-12
