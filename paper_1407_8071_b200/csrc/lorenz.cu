@@ -123,46 +123,6 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
       const double *zk = z + k * kstride;
       lorenz_substep<T>(x1, x2, x3, T(zk[0]), T(zk[1]), T(zk[2]), c);
     }
-  } else if (sizeof(T) == 4) {
-    // 4 substeps = 12 normals = 3 Philox blocks; full chunks run unpredicated
-    const Key2 key = load_key(keys, f);
-    const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb;
-    const float cz = c.f_cz;  // sqrt(dt)*noise_scale*sqrt(2 ln 2): unscaled Box-Muller
-    float a1 = float(x1), a2 = float(x2), a3 = float(x3);
-    const int nfull = c.n_sub >> 2;
-    for (int k4 = 0; k4 <= nfull; ++k4) {
-      const int left = c.n_sub - 4 * k4;
-      if (left <= 0) break;
-      float z[12];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const uint4 rr = philox10(
-            make_uint4(static_cast<uint32_t>(j), t, static_cast<uint32_t>(k4 * 3 + q),
-                       kPurposeLorenz),
-            key);
-        const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
-        const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
-        z[4 * q + 0] = g0.x;
-        z[4 * q + 1] = g0.y;
-        z[4 * q + 2] = g1.x;
-        z[4 * q + 3] = g1.y;
-      }
-      if (left >= 4) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r, nb,
-                              cz);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          if (q < left)
-            lorenz_substep_fast(a1, a2, a3, z[3 * q], z[3 * q + 1], z[3 * q + 2], dt, ndts, r,
-                                nb, cz);
-      }
-    }
-    x1 = T(a1);
-    x2 = T(a2);
-    x3 = T(a3);
   } else {
     // fp64 Philox: 2 substeps = 6 normals = 3 Philox blocks (fp64 Box-Muller)
     const Key2 key = load_key(keys, f);
@@ -189,6 +149,84 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
   xout[MN + p] = x2;
   xout[2 * MN + p] = x3;
   logw[p] = lorenz_loglik<T>(x1, x3, y, obs_dim, c.two_obs_var);
+}
+
+// fp32 production kernel (Philox): constants host-folded, unpredicated
+// 4-substep chunks (12 normals = 3 Philox blocks).  PP > 1 advances several
+// particles per thread (strided by the block size, loads stay coalesced);
+// measured slower on B200 (the kernel is issue/XU-bound, not latency-bound),
+// so the launcher uses PP = 1.
+template <int PP>
+__global__ void __launch_bounds__(256) lorenz_fast_kernel(
+    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
+    const double *__restrict__ y, float *__restrict__ logw, int64_t MN, int32_t N, int obs_dim,
+    LorenzConsts c, const uint32_t *__restrict__ keys, uint32_t t,
+    uint32_t *__restrict__ status) {
+  const int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x) * PP + threadIdx.x;
+  float a1[PP], a2[PP], a3[PP];
+  Key2 key[PP];
+  uint32_t jj[PP];
+  int64_t ff[PP];
+#pragma unroll
+  for (int e = 0; e < PP; ++e) {
+    int64_t p = base + static_cast<int64_t>(e) * blockDim.x;
+    if (p >= MN) p = MN - 1;  // tail: recompute the last particle, no store
+    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+    a1[e] = xin[src];
+    a2[e] = xin[MN + src];
+    a3[e] = xin[2 * MN + src];
+    ff[e] = p / N;
+    jj[e] = static_cast<uint32_t>(p - ff[e] * N);
+    key[e] = load_key(keys, ff[e]);
+  }
+  const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb, cz = c.f_cz;
+  const int nfull = c.n_sub >> 2;
+  for (int k4 = 0; k4 <= nfull; ++k4) {
+    const int left = c.n_sub - 4 * k4;
+    if (left <= 0) break;
+    float z[PP][12];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+#pragma unroll
+      for (int e = 0; e < PP; ++e) {
+        const uint4 rr = philox10(
+            make_uint4(jj[e], t, static_cast<uint32_t>(k4 * 3 + q), kPurposeLorenz), key[e]);
+        const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
+        const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
+        z[e][4 * q + 0] = g0.x;
+        z[e][4 * q + 1] = g0.y;
+        z[e][4 * q + 2] = g1.x;
+        z[e][4 * q + 3] = g1.y;
+      }
+    }
+    if (left >= 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < PP; ++e)
+          lorenz_substep_fast(a1[e], a2[e], a3[e], z[e][3 * q], z[e][3 * q + 1], z[e][3 * q + 2],
+                              dt, ndts, r, nb, cz);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (q < left)
+#pragma unroll
+          for (int e = 0; e < PP; ++e)
+            lorenz_substep_fast(a1[e], a2[e], a3[e], z[e][3 * q], z[e][3 * q + 1],
+                                z[e][3 * q + 2], dt, ndts, r, nb, cz);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < PP; ++e) {
+    const int64_t p = base + static_cast<int64_t>(e) * blockDim.x;
+    if (p >= MN) continue;
+    if (!(isfinite(a1[e]) && isfinite(a2[e]) && isfinite(a3[e])))
+      atomicOr(status + ff[e], PF_ST_DIVERGED);
+    xout[p] = a1[e];
+    xout[MN + p] = a2[e];
+    xout[2 * MN + p] = a3[e];
+    logw[p] = lorenz_loglik<float>(a1[e], a3[e], y, obs_dim, c.two_obs_var);
+  }
 }
 
 // accel.lorenz_euler_block: states (n,3) row-major, noise (n_sub, n, 3)
@@ -285,8 +323,8 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
       lorenz_pw_kernel<float, 1><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
                                                       c, keys, t, z_tape, status);
     else
-      lorenz_pw_kernel<float, 0><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
-                                                      c, keys, t, z_tape, status);
+      lorenz_fast_kernel<1><<<grid_for(MN, 256), 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32,
+                                                              p->obs_dim, c, keys, t, status);
   }
   return check_launch("pf_lorenz_propagate_weight");
 }
