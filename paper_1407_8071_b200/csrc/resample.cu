@@ -309,6 +309,7 @@ struct WideWs {
   double *leaf_sum;
   int32_t *n_leaves;
   int64_t max_leaves;
+  int64_t *klo, *khi;  // per u-tile CDF window (merge partition)
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
@@ -339,6 +340,8 @@ static size_t wide_ws_layout(int64_t M, int64_t N, WideWs *w, char *base) {
   ws.leaf_len = reinterpret_cast<int32_t *>(take(static_cast<size_t>(M) * ws.max_leaves * 4));
   ws.leaf_sum = reinterpret_cast<double *>(take(static_cast<size_t>(M) * ws.max_leaves * 8));
   ws.n_leaves = reinterpret_cast<int32_t *>(take(M * 4));
+  ws.klo = reinterpret_cast<int64_t *>(take(nt * 8));
+  ws.khi = reinterpret_cast<int64_t *>(take(nt * 8));
   if (w) *w = ws;
   return off;
 }
@@ -384,38 +387,7 @@ __global__ void wide_filter_max(int64_t tpf, WideWs ws, uint8_t *collapsed, uint
   }
 }
 
-template <typename TW>
-__global__ void __launch_bounds__(kTileThreads) wide_tile_expsum(const TW *__restrict__ logw,
-                                                                 int64_t N, int64_t tpf,
-                                                                 WideWs ws) {
-  __shared__ double scratch[33];
-  const int64_t tile = blockIdx.x;
-  const int64_t f = tile / tpf, tt = tile - f * tpf;
-  if (ws.flag[f]) return;
-  const double m = ws.m[f];
-  const int64_t i0 = tt * kTile, i1 = min(N, i0 + kTile);
-  double part = 0.0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x)
-    part = __dadd_rn(part, exp(__dsub_rn(load_lw(logw + f * N + i), m)));
-  const double s = block_sum(part, scratch);
-  if (threadIdx.x == 0) ws.tsum[tile] = s;
-}
 
-__global__ void wide_filter_total(int64_t N, int64_t tpf, WideWs ws, double *lnc) {
-  __shared__ double scratch[33];
-  const int64_t f = blockIdx.x;
-  if (ws.flag[f]) return;
-  double part = 0.0;
-  for (int64_t i = threadIdx.x; i < tpf; i += blockDim.x)
-    part = __dadd_rn(part, ws.tsum[f * tpf + i]);
-  const double total = block_sum(part, scratch);
-  if (threadIdx.x == 0) {
-    ws.total[f] = total;
-    const double lmr =
-        __dsub_rn(__dadd_rn(ws.m[f], log(total)), log(static_cast<double>(N)));
-    lnc[f] = __dadd_rn(lnc[f], lmr);
-  }
-}
 
 // tile sums of w and of the exponential spacings
 template <typename TW, int MODE>
@@ -444,7 +416,8 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_sums(
 }
 
 // exclusive tile offsets per filter: block per filter, carry across chunks
-__global__ void wide_offsets_kernel(int64_t M, int64_t tpf, WideWs ws) {
+__global__ void wide_offsets_kernel(int64_t M, int64_t tpf, WideWs ws, int64_t N,
+                                    const uint32_t *keys, uint32_t t) {
   // block per filter, sequential carry over tiles via block scan
   __shared__ double scratch[33];
   extern __shared__ double sbuf[];  // 2 * 1024 doubles
@@ -470,70 +443,83 @@ __global__ void wide_offsets_kernel(int64_t M, int64_t tpf, WideWs ws) {
     cw = cw_next;
     ce = ce_next;
   }
-  if (threadIdx.x == 0) ws.cN[f] = ce;  // sum of E_0..E_{N-1}; E_N added by the merge
+  if (threadIdx.x == 0)  // c[N] = E_0 + ... + E_N
+    ws.cN[f] = keys ? __dadd_rn(ce, spacing_exp_fast(load_key(keys, f), t, N)) : ce;
 }
 
 // cum for one tile -> ws.cum
+// ---- per-thread runs for the wide path ------------------------------------
+// Thread t of a tile owns the kRun consecutive elements [t*kRun, t*kRun+kRun)
+// in registers: one block scan of run totals per tile (instead of one per
+// 256 elements), vector loads, and a padded thread-major shared transpose for
+// coalesced stores.
+constexpr int kRun = kTile / kTileThreads;  // 16
+constexpr int kPad = kTileThreads + 1;     // transpose row pitch (conflict-free)
+
+template <typename TW>
+__device__ __forceinline__ void load_run(const TW *p, int64_t avail, bool aligned, double *v) {
+  if (sizeof(TW) == 4 && aligned && avail >= kRun) {
+#pragma unroll
+    for (int q = 0; q < kRun; q += 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4 *>(p + q));
+      v[q] = x.x;
+      v[q + 1] = x.y;
+      v[q + 2] = x.z;
+      v[q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) v[q] = q < avail ? static_cast<double>(p[q]) : -INFINITY;
+  }
+}
+
+// kRun exponential spacings E_i, i = i0 .. i0+kRun-1 (i0 % 4 == 0): 4 Philox
+// blocks, one 32-bit word per draw (same stream as spacing_exp_fast).
+__device__ __forceinline__ void spacing_run(Key2 key, uint32_t t, int64_t i0, int64_t limit,
+                                            double *e) {
+#pragma unroll
+  for (int q = 0; q < kRun; q += 4) {
+    const uint4 r = philox10(make_uint4(static_cast<uint32_t>((i0 + q) >> 2), t,
+                                        static_cast<uint32_t>((i0 + q) >> 34), kPurposeResample),
+                             key);
+    e[q] = i0 + q < limit ? spacing_exp_fast_word(r.x) : 0.0;
+    e[q + 1] = i0 + q + 1 < limit ? spacing_exp_fast_word(r.y) : 0.0;
+    e[q + 2] = i0 + q + 2 < limit ? spacing_exp_fast_word(r.z) : 0.0;
+    e[q + 3] = i0 + q + 3 < limit ? spacing_exp_fast_word(r.w) : 0.0;
+  }
+}
+
 template <typename TW>
 __global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restrict__ logw,
                                                               int64_t N, int64_t tpf,
                                                               WideWs ws) {
   __shared__ double scratch[33];
-  __shared__ double s[kTile];
+  __shared__ double s[kRun * kPad];
   const int64_t tile = blockIdx.x;
   const int64_t f = tile / tpf, tt = tile - f * tpf;
   if (ws.flag[f]) return;
   const double m = ws.m[f], total = ws.total[f];
   const int64_t i0 = tt * kTile;
   const int n = static_cast<int>((N - i0 < kTile ? N - i0 : kTile));
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-    s[i] = __ddiv_rn(exp(__dsub_rn(load_lw(logw + f * N + i0 + i), m)), total);
+  const int r0 = threadIdx.x * kRun;
+  double v[kRun];
+  load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, v);
+  double run = 0.0;
+#pragma unroll
+  for (int q = 0; q < kRun; ++q) {
+    const double w = r0 + q < n ? __ddiv_rn(exp(__dsub_rn(v[q], m)), total) : 0.0;
+    run = __dadd_rn(run, w);
+    v[q] = run;
+  }
+  double tot;
+  const double off = __dadd_rn(ws.twoff[tile], block_exclusive_scan(run, scratch, &tot));
+#pragma unroll
+  for (int q = 0; q < kRun; ++q) s[q * kPad + threadIdx.x] = __dadd_rn(off, v[q]);
   __syncthreads();
-  block_scan_inplace(s, n, ws.twoff[tile], scratch);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) ws.cum[f * N + i0 + i] = s[i];
+  double *out = ws.cum + f * N + i0;
+  for (int e = threadIdx.x; e < n; e += kTileThreads) out[e] = s[(e % kRun) * kPad + e / kRun];
 }
 
-// sorted uniforms for one u-tile, then merge against ws.cum
-template <int MODE>
-__global__ void __launch_bounds__(kTileThreads) wide_tile_merge(
-    int64_t N, int64_t tpf, WideWs ws, const double *__restrict__ u_tape,
-    const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc) {
-  __shared__ double scratch[33];
-  __shared__ double s[kTile];
-  const int64_t tile = blockIdx.x;
-  const int64_t f = tile / tpf, tt = tile - f * tpf;
-  const int64_t i0 = tt * kTile;
-  const int n = static_cast<int>((N - i0 < kTile ? N - i0 : kTile));
-  const int64_t base = f * N;
-  if (ws.flag[f]) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-      anc[base + i0 + i] = static_cast<int32_t>(base + i0 + i);
-    return;
-  }
-  if (MODE == 1) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = u_tape[base + i0 + i];
-    __syncthreads();
-  } else {
-    const Key2 key = load_key(keys, f);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = spacing_exp_fast(key, t, i0 + i);
-    __syncthreads();
-    block_scan_inplace(s, n, ws.teoff[tile], scratch);
-    const double cN = __dadd_rn(ws.cN[f], spacing_exp_fast(key, t, N));
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = __ddiv_rn(s[i], cN);
-    __syncthreads();
-  }
-  // each thread merges a contiguous run of u's: binary search then walk
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int j0 = threadIdx.x * per, j1 = min(n, j0 + per);
-  if (j0 >= j1) return;
-  const double *cum = ws.cum + base;
-  int64_t k = lower_bound_f64_64(cum, N, s[j0]);
-  for (int j = j0; j < j1; ++j) {
-    const double u = s[j];
-    k = advance_to<int64_t>([&](int64_t i) { return __ldg(cum + i); }, k, N, u);
-    anc[base + i0 + j] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
-  }
-}
 
 
 // ---- reference-order ("exact") CDF ----------------------------------------
@@ -823,6 +809,247 @@ __global__ void __launch_bounds__(32) wide_exact_cumsum(int64_t N, WideWs ws) {
   }
 }
 
+// ---- wide path, production (4 launches) -----------------------------------
+// A: per tile, one read of the log weights: tile max m_t, s_t = sum exp(lw -
+//    m_t) (online logsumexp) and the tile's sum of exponential spacings.
+// B: per filter: m = max m_t, total = sum_t s_t exp(m_t - m) (fixed order),
+//    lnc, exclusive tile offsets of the weights and of the spacings, c[N].
+// C: per tile: w = exp(lw - m)/total, in-tile scan + offset -> cum (fp64).
+// D: per u-tile: sorted uniforms, the CDF window they fall into is staged in
+//    shared memory when it fits (galloping search in global memory when it
+//    does not), ancestors and the fused gather written coalesced.
+template <typename TW, int MODE>
+__global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
+    const TW *__restrict__ logw, int64_t N, int64_t tpf, WideWs ws,
+    const uint32_t *__restrict__ keys, uint32_t t) {
+  __shared__ double scratch[33];
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  const int64_t i0 = tt * kTile;
+  const int n = static_cast<int>(N - i0 < kTile ? N - i0 : kTile);
+  const int r0 = threadIdx.x * kRun;
+  double lv[kRun];
+  load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, lv);
+  double mx = -INFINITY;
+  int nan = 0;
+#pragma unroll
+  for (int q = 0; q < kRun; ++q) {
+    if (r0 + q >= n) lv[q] = -INFINITY;
+    nan |= isnan(lv[q]);
+    mx = fmax(mx, lv[q]);
+  }
+  nan = __syncthreads_or(nan);
+  const double m = block_max(mx, scratch);
+  double part = 0.0;
+  if (m != -INFINITY) {
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) part = __dadd_rn(part, exp(__dsub_rn(lv[q], m)));
+  }
+  const double ssum = block_sum(part, scratch);
+  double se = 0.0;
+  if (MODE == 0) {
+    double e[kRun];
+    spacing_run(load_key(keys, f), t, i0 + r0, N, e);
+    double pe = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) pe = __dadd_rn(pe, e[q]);
+    se = block_sum(pe, scratch);
+  }
+  if (threadIdx.x == 0) {
+    ws.tmax[tile] = nan ? NAN : m;
+    ws.tsum[tile] = m == -INFINITY ? 0.0 : ssum;
+    ws.tesum[tile] = se;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) wide2_filter(int64_t N, int64_t tpf, WideWs ws,
+                                                    uint8_t *collapsed, uint32_t *status,
+                                                    double *lnc, const uint32_t *keys,
+                                                    uint32_t t) {
+  __shared__ double scratch[33];
+  __shared__ double sw[1024], se[1024];
+  const int64_t f = blockIdx.x;
+  const double *tmax = ws.tmax + f * tpf, *tsum = ws.tsum + f * tpf, *tes = ws.tesum + f * tpf;
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int64_t i = threadIdx.x; i < tpf; i += blockDim.x) {
+    nan |= isnan(tmax[i]);
+    mx = fmax(mx, tmax[i]);
+  }
+  nan = __syncthreads_or(nan);
+  const double m = block_max(mx, scratch);
+  const int fl = nan ? 2 : (m == -INFINITY ? 1 : 0);
+  if (threadIdx.x == 0) {
+    ws.flag[f] = fl;
+    ws.m[f] = m;
+    collapsed[f] = fl == 1 ? 1 : 0;
+    if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
+  }
+  if (fl) return;
+  double part = 0.0;
+  for (int64_t i = threadIdx.x; i < tpf; i += blockDim.x)
+    part = __dadd_rn(part, __dmul_rn(tsum[i], exp(__dsub_rn(tmax[i], m))));
+  const double total = block_sum(part, scratch);
+  double cw = 0.0, ce = 0.0;
+  for (int64_t b0 = 0; b0 < tpf; b0 += 1024) {
+    const int n = static_cast<int>(tpf - b0 < 1024 ? tpf - b0 : 1024);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      sw[i] = __ddiv_rn(__dmul_rn(tsum[b0 + i], exp(__dsub_rn(tmax[b0 + i], m))), total);
+      se[i] = tes[b0 + i];
+    }
+    __syncthreads();
+    const double cw_next = block_scan_inplace(sw, n, cw, scratch);
+    const double ce_next = block_scan_inplace(se, n, ce, scratch);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      ws.twoff[f * tpf + b0 + i] = i == 0 ? cw : sw[i - 1];
+      ws.teoff[f * tpf + b0 + i] = i == 0 ? ce : se[i - 1];
+    }
+    __syncthreads();
+    cw = cw_next;
+    ce = ce_next;
+  }
+  if (threadIdx.x == 0) {
+    ws.total[f] = total;
+    if (MODE == 0) ws.cN[f] = __dadd_rn(ce, spacing_exp_fast(load_key(keys, f), t, N));
+    const double lmr = __dsub_rn(__dadd_rn(m, log(total)), log(static_cast<double>(N)));
+    lnc[f] = __dadd_rn(lnc[f], lmr);
+  }
+}
+
+constexpr int kWin = 4096;  // CDF window staged in shared memory (32 KB)
+
+// Merge partition: one thread per (u-tile, end) finds the CDF index range the
+// tile's uniforms fall into.  Thousands of independent binary searches run
+// concurrently, so their dependent-load latency overlaps (a search inside
+// the merge CTA would stall the whole block).  The tile's first and last
+// uniforms are recomputed from the tile offsets; a relative margin absorbs
+// the different association of the in-tile scan.
+template <int MODE>
+__global__ void wide2_partition(int64_t N, int64_t tpf, int64_t ntiles, WideWs ws,
+                                const double *__restrict__ u_tape,
+                                const uint32_t *__restrict__ keys, uint32_t t) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= 2 * ntiles) return;
+  const int64_t tile = g >> 1;
+  const bool last = g & 1;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  if (ws.flag[f]) return;
+  const int64_t i0 = tt * kTile;
+  const int64_t n = N - i0 < kTile ? N - i0 : kTile;
+  double u;
+  if (MODE == 1) {
+    u = u_tape[f * N + i0 + (last ? n - 1 : 0)];
+  } else {
+    const double c = last ? __dadd_rn(ws.teoff[tile], ws.tesum[tile])
+                          : __dadd_rn(ws.teoff[tile], spacing_exp_fast(load_key(keys, f), t, i0));
+    u = c / ws.cN[f];
+  }
+  const double x = last ? u * (1.0 + 1e-12) : u * (1.0 - 1e-12);
+  int64_t k = lower_bound_f64_64(ws.cum + f * N, N, x);
+  if (last) {
+    k = k + 1 < N ? k + 1 : N - 1;
+    ws.khi[tile] = k;
+  } else {
+    ws.klo[tile] = k > 0 ? k - 1 : 0;
+  }
+}
+
+template <int MODE, bool GATHER>
+__global__ void __launch_bounds__(kTileThreads) wide2_merge(
+    int64_t N, int64_t tpf, WideWs ws, const double *__restrict__ u_tape,
+    const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
+    const float *__restrict__ gx_in, float *__restrict__ gx_out, int gdims, int64_t gMN) {
+  __shared__ double s_c[kWin];  // CDF window, then reused for the ancestor transpose
+  __shared__ double scratch[33];
+  static_assert(kRun * kPad * sizeof(int32_t) <= kWin * sizeof(double), "transpose must fit");
+  int32_t *s_a = reinterpret_cast<int32_t *>(s_c);
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  const int64_t i0 = tt * kTile;
+  const int n = static_cast<int>(N - i0 < kTile ? N - i0 : kTile);
+  const int64_t base = f * N;
+  if (ws.flag[f]) {  // collapse / NaN: identity ancestors (filters.py:105-109)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      anc[base + i0 + i] = static_cast<int32_t>(base + i0 + i);
+      if (GATHER)
+        for (int d = 0; d < gdims; ++d)
+          gx_out[d * gMN + base + i0 + i] = gx_in[d * gMN + base + i0 + i];
+    }
+    return;
+  }
+  // this thread's run of sorted uniforms, in registers
+  const int r0 = threadIdx.x * kRun;
+  double u[kRun];
+  if (MODE == 1) {
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) u[q] = r0 + q < n ? u_tape[base + i0 + r0 + q] : 2.0;
+  } else {
+    spacing_run(load_key(keys, f), t, i0 + r0, N, u);
+    double run = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      run = __dadd_rn(run, u[q]);
+      u[q] = run;
+    }
+    double tot;
+    const double off = __dadd_rn(ws.teoff[tile], block_exclusive_scan(run, scratch, &tot));
+    const double inv = 1.0 / ws.cN[f];
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) u[q] = r0 + q < n ? __dadd_rn(off, u[q]) * inv : 2.0;
+  }
+  const double *cum = ws.cum + base;
+  const int64_t lo = ws.klo[tile], hi = ws.khi[tile];
+  const int64_t wlen = hi - lo + 1;
+  int32_t a[kRun];
+  if (wlen <= kWin) {
+    for (int64_t i = threadIdx.x; i < wlen; i += blockDim.x) s_c[i] = __ldg(cum + lo + i);
+    __syncthreads();
+    const int w = static_cast<int>(wlen);
+    int k = r0 < n ? lower_bound_f64(s_c, w, u[0]) : 0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      if (r0 + q < n) k = advance_to<int>([&](int i) { return s_c[i]; }, k, w, u[q]);
+      const int64_t g = lo + k;
+      a[q] = static_cast<int32_t>(base + (g < N - 1 ? g : N - 1));
+    }
+  } else {  // very wide window: galloping search in global memory
+    int64_t k = r0 < n ? lo + lower_bound_f64_64(cum + lo, wlen, u[0]) : lo;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      if (r0 + q < n) k = advance_to<int64_t>([&](int64_t i) { return __ldg(cum + i); }, k, N, u[q]);
+      a[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+    }
+  }
+  __syncthreads();  // all window reads done before s_c is reused
+#pragma unroll
+  for (int q = 0; q < kRun; ++q) s_a[q * kPad + threadIdx.x] = a[q];
+  __syncthreads();
+  // coalesced write-out (thread-strided elements), gather loads batched 4 deep
+  for (int e0 = threadIdx.x; e0 < n; e0 += 4 * kTileThreads) {
+    int32_t ai[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int e = e0 + h * kTileThreads;
+      ai[h] = e < n ? s_a[(e % kRun) * kPad + e / kRun] : 0;
+      if (e < n) anc[base + i0 + e] = ai[h];
+    }
+    if (GATHER) {
+      for (int d = 0; d < gdims; ++d) {
+        float v[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          v[h] = e0 + h * kTileThreads < n ? __ldg(gx_in + d * gMN + ai[h]) : 0.f;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int e = e0 + h * kTileThreads;
+          if (e < n) gx_out[d * gMN + base + i0 + e] = v[h];
+        }
+      }
+    }
+  }
+}
+
 __global__ void wide_gather_kernel(const float *__restrict__ xin, const int32_t *__restrict__ anc,
                                    int64_t MN, int dims, float *__restrict__ xout) {
   const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -889,9 +1116,9 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
              ws_bytes, need);
   const int64_t tpf = (N + kTile - 1) / kTile;
   const unsigned nt = static_cast<unsigned>(M * tpf);
-  wide_tile_max<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
-  wide_filter_max<<<static_cast<unsigned>(M), 256, 0, s>>>(tpf, ws, collapsed, status);
   if (exact) {
+    wide_tile_max<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+    wide_filter_max<<<static_cast<unsigned>(M), 256, 0, s>>>(tpf, ws, collapsed, status);
     wide_exact_e<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
     wide_exact_leaves<<<static_cast<unsigned>(M), 32, 0, s>>>(N, ws);
     wide_exact_leafsum<<<dim3(static_cast<unsigned>((ws.max_leaves + 127) / 128),
@@ -903,25 +1130,27 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
     if (!u_tape) {  // tile offsets of the exponential spacings
       wide_tile_sums<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
       wide_offsets_kernel<<<static_cast<unsigned>(M), 256, 2 * 1024 * sizeof(double), s>>>(
-          M, tpf, ws);
+          M, tpf, ws, N, keys, t);
     }
   } else {
-    wide_tile_expsum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
-    wide_filter_total<<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, lnc);
-    if (u_tape)
-      wide_tile_sums<TW, 1><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
-    else
-      wide_tile_sums<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t);
-    wide_offsets_kernel<<<static_cast<unsigned>(M), 256, 2 * 1024 * sizeof(double), s>>>(M, tpf,
-                                                                                          ws);
+    if (u_tape) {
+      wide2_tile_stats<TW, 1><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, keys, t);
+      wide2_filter<1><<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, collapsed, status,
+                                                               lnc, keys, t);
+    } else {
+      wide2_tile_stats<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, keys, t);
+      wide2_filter<0><<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, collapsed, status,
+                                                               lnc, keys, t);
+    }
     wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
   }
   if (u_tape)
-    wide_tile_merge<1><<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc);
+    wide2_partition<1><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
   else
-    wide_tile_merge<0><<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc);
-  if (gx_in)
-    wide_gather_kernel<<<grid_for(M * N, 256), 256, 0, s>>>(gx_in, anc, M * N, gdims, gx_out);
+    wide2_partition<0><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
+  auto mk = u_tape ? (gx_in ? wide2_merge<1, true> : wide2_merge<1, false>)
+                   : (gx_in ? wide2_merge<0, true> : wide2_merge<0, false>);
+  mk<<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc, gx_in, gx_out, gdims, M * N);
   return check_launch("pf_segmented_resample(wide)");
 }
 

@@ -483,3 +483,49 @@ def test_stock_lorenz_model_observing_x1():
     for k in range(len(obs)):
         assert np.array_equal(ancs[k], np.stack([tr.steps[k].ancestors for tr in traces]))
     assert norm_rel(bank.est.cpu().numpy(), np.stack([tr.estimates for tr in traces], 1)) < 1e-12
+
+
+# ---------------------------------------------------------------- production resampling law
+
+def _offspring_counts(lw, reps, flags, seed):
+    """Total offspring counts over `reps` production-mode (Philox) resamples
+    of the same log weights (different time words)."""
+    M, N = lw.shape
+    d_lw = torch.from_numpy(lw.reshape(-1)).cuda()
+    anc = torch.empty(M * N, dtype=torch.int32, device="cuda")
+    lnc = torch.zeros(M, dtype=torch.float64, device="cuda")
+    coll = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    st = torch.zeros(M, dtype=torch.int32, device="cuda")
+    keys = torch.from_numpy(pf.philox.filter_keys(seed, M).view(np.int32)).cuda()
+    wsb = _lib.load().pf_resample_workspace_bytes(M, N)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    counts = torch.zeros(M * N, dtype=torch.int64, device="cuda")
+    for r in range(reps):
+        _lib.call("pf_segmented_resample_ex", _lib.PF_F32, _lib.ptr(d_lw), M, N, None,
+                  _lib.ptr(keys), r + 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll),
+                  _lib.ptr(st), _lib.ptr(ws), wsb, None, None, 0, flags, _lib.stream_ptr())
+        counts += torch.bincount(anc.long(), minlength=M * N)
+    return counts.cpu().numpy().reshape(M, N)
+
+
+@pytest.mark.parametrize("M,N,flags", [(64, 1024, 0), (2, 20000, 0), (2, 20000, 1),
+                                       (1, 1 << 20, 0)])
+def test_production_resampling_is_multinomial(M, N, flags):
+    """Offspring counts follow multinomial(N, w) (test_resampling.py:40-67
+    analogue): chi-square over 64 equal-mass bins per filter at 0.1 %."""
+    from scipy import stats
+
+    rng = np.random.default_rng(N + M)
+    lw = rng.standard_normal((M, N)).astype(np.float32)
+    w = np.exp(lw.astype(np.float64) - lw.max(axis=1, keepdims=True))
+    w /= w.sum(axis=1, keepdims=True)
+    reps = 40
+    counts = _offspring_counts(lw, reps, flags, seed=3)
+    assert np.all(counts.sum(axis=1) == reps * N)
+    B = 64
+    for f in range(M):
+        edges = np.searchsorted(np.cumsum(w[f]), np.linspace(0, 1, B + 1)[1:-1])
+        obs = np.add.reduceat(counts[f], np.r_[0, edges])
+        exp_ = np.add.reduceat(w[f], np.r_[0, edges]) * reps * N
+        chi2 = float(((obs - exp_) ** 2 / exp_).sum())
+        assert chi2 < stats.chi2.ppf(0.999, df=B - 1), (f, chi2)
