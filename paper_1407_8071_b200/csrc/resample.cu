@@ -956,7 +956,7 @@ __global__ void wide2_partition(int64_t N, int64_t tpf, int64_t ntiles, WideWs w
 }
 
 template <int MODE, bool GATHER>
-__global__ void __launch_bounds__(kTileThreads) wide2_merge(
+__global__ void __launch_bounds__(kTileThreads, 2) wide2_merge(
     int64_t N, int64_t tpf, WideWs ws, const double *__restrict__ u_tape,
     const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
     const float *__restrict__ gx_in, float *__restrict__ gx_out, int gdims, int64_t gMN) {
@@ -978,6 +978,22 @@ __global__ void __launch_bounds__(kTileThreads) wide2_merge(
     }
     return;
   }
+  const double *cum = ws.cum + base;
+  const int64_t lo = ws.klo[tile], hi = ws.khi[tile];
+  const int64_t wlen = hi - lo + 1;
+  const bool chunked = wlen <= 16 * static_cast<int64_t>(kWin);
+  // issue the first CDF chunk's loads now; they land while the uniforms
+  // are generated below
+  constexpr int kPer = kWin / kTileThreads;
+  double cv[kPer];
+  const int len0 = static_cast<int>(wlen < kWin ? wlen : kWin);
+  if (chunked) {
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int i = r * kTileThreads + threadIdx.x;
+      cv[r] = i < len0 ? __ldg(cum + lo + i) : 0.0;
+    }
+  }
   // this thread's run of sorted uniforms, in registers
   const int r0 = threadIdx.x * kRun;
   double u[kRun];
@@ -998,22 +1014,48 @@ __global__ void __launch_bounds__(kTileThreads) wide2_merge(
 #pragma unroll
     for (int q = 0; q < kRun; ++q) u[q] = r0 + q < n ? __dadd_rn(off, u[q]) * inv : 2.0;
   }
-  const double *cum = ws.cum + base;
-  const int64_t lo = ws.klo[tile], hi = ws.khi[tile];
-  const int64_t wlen = hi - lo + 1;
   int32_t a[kRun];
-  if (wlen <= kWin) {
-    for (int64_t i = threadIdx.x; i < wlen; i += blockDim.x) s_c[i] = __ldg(cum + lo + i);
-    __syncthreads();
-    const int w = static_cast<int>(wlen);
-    int k = r0 < n ? lower_bound_f64(s_c, w, u[0]) : 0;
+  if (chunked) {
+    // stream the CDF window through shared memory in kWin chunks; every
+    // uniform is placed in the chunk holding its answer (answers are
+    // non-decreasing, so each thread resumes from its previous answer)
+    uint32_t done = 0;
+    int64_t k = lo;
+    for (int64_t c0 = lo; c0 <= hi; c0 += kWin) {
+      const int len = static_cast<int>(hi - c0 + 1 < kWin ? hi - c0 + 1 : kWin);
+      __syncthreads();  // previous chunk consumed
+      if (c0 != lo) {
 #pragma unroll
-    for (int q = 0; q < kRun; ++q) {
-      if (r0 + q < n) k = advance_to<int>([&](int i) { return s_c[i]; }, k, w, u[q]);
-      const int64_t g = lo + k;
-      a[q] = static_cast<int32_t>(base + (g < N - 1 ? g : N - 1));
+        for (int r = 0; r < kPer; ++r) {
+          const int i = r * kTileThreads + threadIdx.x;
+          cv[r] = i < len ? __ldg(cum + c0 + i) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kPer; ++r) {
+        const int i = r * kTileThreads + threadIdx.x;
+        if (i < len) s_c[i] = cv[r];
+      }
+      __syncthreads();
+      const bool last = c0 + len > hi;
+      const double cmax = s_c[len - 1];
+#pragma unroll
+      for (int q = 0; q < kRun; ++q) {
+        if ((done >> q) & 1u) continue;
+        if (r0 + q >= n) {
+          a[q] = static_cast<int32_t>(base);
+          done |= 1u << q;
+          continue;
+        }
+        if (!(u[q] <= cmax) && !last) break;  // this and later uniforms: later chunks
+        int kl = static_cast<int>(k - c0 > 0 ? k - c0 : 0);
+        kl = advance_to<int>([&](int i) { return s_c[i]; }, kl, len, u[q]);
+        k = c0 + kl;
+        a[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+        done |= 1u << q;
+      }
     }
-  } else {  // very wide window: galloping search in global memory
+  } else {  // extreme window: galloping search in global memory
     int64_t k = r0 < n ? lo + lower_bound_f64_64(cum + lo, wlen, u[0]) : lo;
 #pragma unroll
     for (int q = 0; q < kRun; ++q) {
@@ -1048,6 +1090,28 @@ __global__ void __launch_bounds__(kTileThreads) wide2_merge(
       }
     }
   }
+}
+
+// 3-plane fp32 gather, 4 consecutive particles per thread: one int4 ancestor
+// load, 12 independent gathered loads in flight, three float4 stores.
+__global__ void __launch_bounds__(256) gather3_kernel(const float *__restrict__ xin,
+                                                      const int32_t *__restrict__ anc, int64_t MN,
+                                                      float *__restrict__ xout) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (4 * q >= MN) return;
+  const int4 a = __ldg(reinterpret_cast<const int4 *>(anc) + q);
+  float v[3][4];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const float *src = xin + d * MN;
+    v[d][0] = __ldg(src + a.x);
+    v[d][1] = __ldg(src + a.y);
+    v[d][2] = __ldg(src + a.z);
+    v[d][3] = __ldg(src + a.w);
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    reinterpret_cast<float4 *>(xout + d * MN)[q] = make_float4(v[d][0], v[d][1], v[d][2], v[d][3]);
 }
 
 __global__ void wide_gather_kernel(const float *__restrict__ xin, const int32_t *__restrict__ anc,
@@ -1148,9 +1212,16 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
     wide2_partition<1><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
   else
     wide2_partition<0><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
-  auto mk = u_tape ? (gx_in ? wide2_merge<1, true> : wide2_merge<1, false>)
-                   : (gx_in ? wide2_merge<0, true> : wide2_merge<0, false>);
-  mk<<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc, gx_in, gx_out, gdims, M * N);
+  // merge -> ancestors, then the gather as its own high-occupancy pass
+  auto mk = u_tape ? wide2_merge<1, false> : wide2_merge<0, false>;
+  mk<<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc, nullptr, nullptr, 0, M * N);
+  if (gx_in) {
+    const int64_t MN = M * N;
+    if (gdims == 3 && (MN & 3) == 0)
+      gather3_kernel<<<grid_for(MN / 4, 256), 256, 0, s>>>(gx_in, anc, MN, gx_out);
+    else
+      wide_gather_kernel<<<grid_for(MN, 256), 256, 0, s>>>(gx_in, anc, MN, gdims, gx_out);
+  }
   return check_launch("pf_segmented_resample(wide)");
 }
 
