@@ -19,6 +19,26 @@ from . import _lib, philox
 from .models import FhnLatticeModel, Lorenz63Model
 
 
+def simulate(model, n_steps: int, seed):
+    """One state trajectory and its observations through the model hooks
+    (parpf/models/simulate.py:10-29): same control flow and draw order
+    (prior, then per step transition then observation), arithmetic on the
+    GPU.  Returns (states (n_steps+1, dim_x), observations (n_steps, dim_y)).
+    """
+    if n_steps < 0:
+        raise ValueError("n_steps must be >= 0")
+    rng = np.random.default_rng(seed)
+    x = model.sample_prior(rng, 1)[0]
+    states = np.empty((n_steps + 1, model.dim_x))
+    observations = np.empty((n_steps, model.dim_y))
+    states[0] = x
+    for t in range(1, n_steps + 1):
+        x = model.sample_transition(x[None, :], t, rng)[0]
+        states[t] = x
+        observations[t - 1] = np.asarray(model.sample_observation(x, t, rng)).reshape(-1)
+    return states, observations
+
+
 def _truth_key(seed):
     ss = philox.as_seed_sequence(seed)
     return np.random.SeedSequence(ss.entropy, spawn_key=tuple(ss.spawn_key) + (0x7457,)) \

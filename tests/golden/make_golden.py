@@ -268,6 +268,19 @@ def gen_lorenz():
     outac = parpf.run_filter(model, obs_c, "auxiliary", 16, 12)
     d["ac_est"], d["ac_lnc"] = outac.estimates, outac.log_norm_const
     d["ac_steps"] = np.array(outac.collapse_steps)
+    # ground truth / observation generator (models/simulate.py:10-29), stock model
+    from parpf.models import simulate as ref_simulate
+
+    d["sim_states"], d["sim_obs"] = ref_simulate(Lorenz63Model(), 20, 11)
+    # the .17g CSV format (io.py:36-42) as written by the reference
+    import tempfile
+
+    from parpf import io as ref_io
+
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "obs.csv")
+        ref_io.write_array_csv(path, "y", d["sim_obs"][:5])
+        d["csv_text"] = np.array(open(path).read())
     np.savez_compressed(os.path.join(HERE, "lorenz.npz"), **d)
 
 
