@@ -81,6 +81,28 @@ typedef struct pf_fhn_params {
   double obs_var;
 } pf_fhn_params;
 
+/* Stochastically forced FH-N network, the paper's lattice model
+ * (models/fhn.py:85-207): J x J nodes, ONE Euler step per transition with
+ * drive = forcing_mask * forcing(t) + stim_amp * [stimulus in the last
+ * stim_hold steps], random stimuli behind travelling waves (stim_prob per
+ * particle-step at a uniformly chosen cell of the (u_minus, u_plus) region,
+ * plus its von Neumann neighbours).  Device layout per particle p: U, V planes
+ * x[p*2*J*J + {0, J*J} + node] and the stimulus history as bits
+ * q[p*J*J + node] (bit k = Q(t-k), so stim_hold <= 32). */
+typedef struct pf_fhnnet_params {
+  int32_t J, stim_hold, n_obs;
+  int32_t stochastic; /* 0 = transition_point_prediction (fhn.py:191-197): no new
+                         stimulus, no noise; forcing and latched stimuli apply */
+  double dt, coupling;
+  double cubic[4]; /* a3, a2, a1, a0 */
+  double beta[3];  /* b0, b1, b2 */
+  double u_minus, u_plus;
+  double stim_prob, stim_amp;
+  double forcing_amp, forcing_period, forcing_width;
+  double sig_sqdt; /* sqrt(dyn_var) * sqrt(dt) */
+  double obs_var;
+} pf_fhnnet_params;
+
 /* ---- library ------------------------------------------------------- */
 const char *pf_last_error(void);
 int pf_version(void);
@@ -186,10 +208,46 @@ int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t 
                        int32_t dim, const int32_t *anc, int64_t M, int64_t N, double *est_out,
                        void *stream);
 
+/* pf_filter_estimate writing filter f's row at est_out + f*est_stride. */
+int pf_filter_estimate_strided(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,
+                               int32_t dim, const int32_t *anc, int64_t M, int64_t N,
+                               double *est_out, int64_t est_stride, void *stream);
+
 /* average_estimates (ensemble.py:68-73): out[t][d] = (e_0 + e_1 + ...) / M,
  * left to right over filters, fp64.  est is (T, M, dim), out is (T, dim). */
 int pf_ensemble_average(const double *est, int64_t T, int64_t M, int64_t dim, double *out,
                         void *stream);
+
+/* ---- FH-N network (models/fhn.py:85-207) ------------------------------- */
+/* One transition of the network model for M*N particles (sample_transition
+ * fhn.py:153-192, or transition_point_prediction when p->stochastic == 0):
+ * x_out/q_out[p] = step(x_in/q_in[anc[p]]) (anc NULL = identity), and when
+ * logw_out != NULL the zone log-likelihood of y (n_obs doubles at obs_idx,
+ * fhn.py:199-207).  Draws: stim_tape (M, 2, N) fp64 [fire, select uniforms]
+ * plus z_tape (M, N, J*J) fp64 normals (oracle mode), or Philox (both NULL). */
+int pf_fhnnet_step(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
+                   const uint32_t *q_in, const int32_t *anc, void *x_out, uint32_t *q_out,
+                   const double *forcing_mask, const double *y, const int32_t *obs_idx,
+                   void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                   const double *stim_tape, const double *z_tape, uint32_t *status,
+                   void *stream);
+/* Reference state rows (n, (2 + hold) * nodes) fp64 [U, V, Q(t) .. Q(t-hold+1)]
+ * <-> device planes + history bits (fhn.py:122-138 unpack/pack).  Q entries
+ * are indicators; any nonzero value packs as 1.  unpack gathers rows anc[p]
+ * when anc != NULL. */
+int pf_fhnnet_pack(pf_dtype dtype, const double *rows, int64_t n, int32_t nodes, int32_t hold,
+                   void *x, uint32_t *q, void *stream);
+int pf_fhnnet_unpack(pf_dtype dtype, const void *x, const uint32_t *q, const int32_t *anc,
+                     int64_t n, int32_t nodes, int32_t hold, double *rows, void *stream);
+/* Zone log-likelihood of stored states (fhn.py:199-207): out[r] (fp64) =
+ * -0.5/obs_var * sum_i (y[i] - x[r*row_stride + obs_idx[i]])^2, numpy order. */
+int pf_zone_loglik(pf_dtype dtype, const void *x, int64_t n, int64_t row_stride,
+                   const int32_t *obs_idx, int32_t n_obs, const double *y, double obs_var,
+                   double *out, void *stream);
+/* posterior_mean of the history indicators over the resampled set:
+ * est[f*est_stride + k*nodes + node] = (1/N) #{j : bit k of q[anc[f*N+j]][node]}. */
+int pf_bits_estimate(const uint32_t *q, int32_t nodes, int32_t nbits, const int32_t *anc,
+                     int64_t M, int64_t N, double *est, int64_t est_stride, void *stream);
 
 /* ---- native bank driver ------------------------------------------------ */
 /* Production-mode (Philox) bootstrap bank: runs observations k0..k0+n-1 back
@@ -201,6 +259,7 @@ int pf_ensemble_average(const double *est, int64_t T, int64_t M, int64_t dim, do
  * interval (the prior has no ancestors). */
 #define PF_MODEL_LORENZ 0
 #define PF_MODEL_FHN 1
+#define PF_MODEL_FHNNET 2
 typedef struct pf_bank_desc {
   int32_t model; /* PF_MODEL_* */
   pf_dtype dtype;
@@ -226,6 +285,12 @@ typedef struct pf_bank_desc {
   uint8_t *collapsed_trace; /* (T, M) or NULL */
   float *prop_ms; /* host (n_steps) or NULL: propagate-kernel durations; the call then
                      waits for the last propagate to finish before returning */
+  /* FH-N network only */
+  const pf_fhnnet_params *fhnnet; /* host */
+  uint32_t *q[2];                 /* stimulus-history double buffer */
+  const double *forcing_mask;     /* (J*J) */
+  int64_t est_stride_f; /* distance between filters' estimate rows (0 = est_dim) */
+  int32_t est_bits;     /* > 0: history bit means written after the est_dim state means */
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);

@@ -45,6 +45,14 @@ class FhnParams(ctypes.Structure):
                 ("obs_var", c_f64)]
 
 
+class FhnNetParams(ctypes.Structure):
+    _fields_ = [("J", c_i32), ("stim_hold", c_i32), ("n_obs", c_i32), ("stochastic", c_i32),
+                ("dt", c_f64), ("coupling", c_f64), ("cubic", c_f64 * 4), ("beta", c_f64 * 3),
+                ("u_minus", c_f64), ("u_plus", c_f64), ("stim_prob", c_f64), ("stim_amp", c_f64),
+                ("forcing_amp", c_f64), ("forcing_period", c_f64), ("forcing_width", c_f64),
+                ("sig_sqdt", c_f64), ("obs_var", c_f64)]
+
+
 class BankDesc(ctypes.Structure):
     _fields_ = [("model", c_i32), ("dtype", ctypes.c_int), ("M", c_i64), ("N", c_i64),
                 ("lorenz", ctypes.POINTER(LorenzParams)), ("fhn", ctypes.POINTER(FhnParams)),
@@ -53,11 +61,14 @@ class BankDesc(ctypes.Structure):
                 ("ws_bytes", c_sz), ("obs", c_vp), ("dim_y", c_i32), ("est", c_vp),
                 ("est_step_stride", c_i64), ("est_offset", c_i64), ("est_stride_p", c_i64),
                 ("est_stride_d", c_i64), ("est_dim", c_i32), ("lnc_trace", c_vp),
-                ("collapsed_trace", c_vp), ("prop_ms", ctypes.POINTER(ctypes.c_float))]
+                ("collapsed_trace", c_vp), ("prop_ms", ctypes.POINTER(ctypes.c_float)),
+                ("fhnnet", ctypes.POINTER(FhnNetParams)), ("q", c_vp * 2),
+                ("forcing_mask", c_vp), ("est_stride_f", c_i64), ("est_bits", c_i32)]
 
 
 PF_MODEL_LORENZ = 0
 PF_MODEL_FHN = 1
+PF_MODEL_FHNNET = 2
 
 # name -> (restype, argtypes); must match include/pfbank.h exactly
 SIGNATURES = {
@@ -90,6 +101,18 @@ SIGNATURES = {
                                                 c_i32, c_u32, c_vp]),
     "pf_filter_estimate": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64,
                                           c_i64, c_vp, c_vp]),
+    "pf_filter_estimate_strided": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_i32, c_vp,
+                                                  c_i64, c_i64, c_vp, c_i64, c_vp]),
+    "pf_fhnnet_step": (ctypes.c_int, [ctypes.POINTER(FhnNetParams), ctypes.c_int, c_vp, c_vp,
+                                      c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
+                                      c_vp, c_u32, c_vp, c_vp, c_vp, c_vp]),
+    "pf_fhnnet_pack": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "pf_fhnnet_unpack": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32,
+                                        c_vp, c_vp]),
+    "pf_zone_loglik": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_i32, c_vp, c_f64,
+                                      c_vp, c_vp]),
+    "pf_bits_estimate": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp, c_i64, c_i64, c_vp, c_i64,
+                                        c_vp]),
     "pf_bank_run": (ctypes.c_int, [ctypes.POINTER(BankDesc), c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pf_apf_first_stage_prepare": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "pf_compose_ancestors": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),

@@ -30,8 +30,9 @@ class DrawTape:
     """Oracle-mode draws, indexed by GLOBAL filter id (rows).
 
     prior:    (M, N, 3) standard normals (Lorenz) or None (deterministic prior)
-    noise:    per step k, (M, n_sub, N, 3) [Lorenz] or (M, n_sub, 2, N, nodes)
-              [FH-N] standard normals
+    noise:    per step k, (M, n_sub, N, 3) [Lorenz], (M, n_sub, 2, N, nodes)
+              [FH-N lattice] or (M, N, nodes) [FH-N network] standard normals
+    stim:     per step k, (M, 2, N) fire / select uniforms [FH-N network]
     uniforms: per step k, (M, N) sorted uniforms (rows of collapsed filters
               are ignored - the reference draws none for them)
     """
@@ -40,6 +41,7 @@ class DrawTape:
     noise: list = field(default_factory=list)
     uniforms: list = field(default_factory=list)
     uniforms_first: list = field(default_factory=list)  # auxiliary filter, first stage
+    stim: list = field(default_factory=list)  # FH-N network stimulus uniforms
 
 
 def _torch_dtype(dtype):
@@ -66,7 +68,7 @@ class FilterBank:
             raise ValueError("n_filters and n_particles must be >= 1")
         if n_filters * n_particles > 2**31 - 1:
             raise ValueError("M*N per GPU must fit int32 particle indices")
-        if model.kind not in ("lorenz", "fhn"):
+        if model.kind not in ("lorenz", "fhn", "fhnnet"):
             raise ValueError(f"model kind {model.kind!r} has no GPU descriptor")
         if variant not in ("bootstrap", "auxiliary"):
             raise ValueError(f"unknown filter variant {variant!r}")
@@ -83,11 +85,26 @@ class FilterBank:
         self.device = dev
         kw = dict(device=dev)
 
+        from .models import estimate_width
+
+        self.est_width = estimate_width(model, estimate)
+        self.est_bits = 0
+        self.q = [None, None]
         if model.kind == "lorenz":
             self.x = [torch.empty((3, self.MN), dtype=self.dtype, **kw) for _ in range(2)]
             self.params = model.params()
             self.est_dim = 3
             self.est_strides = (1, self.MN)
+        elif model.kind == "fhnnet":
+            nodes = model.nodes
+            self.x = [torch.empty((self.MN, 2 * nodes), dtype=self.dtype, **kw) for _ in range(2)]
+            self.q = [torch.empty((self.MN, nodes), dtype=torch.int32, **kw) for _ in range(2)]
+            self.params = model.params()
+            self.obs_idx = torch.from_numpy(model.obs_indices.astype(np.int32)).to(dev)
+            self.fmask = model.device_mask(dev)
+            self.est_dim = 2 * nodes if estimate == "full" else nodes
+            self.est_bits = model.stim_hold if estimate == "full" else 0
+            self.est_strides = (2 * nodes, 1)
         else:
             self.x = [torch.empty((self.MN, model.dim_x), dtype=self.dtype, **kw)
                       for _ in range(2)]
@@ -108,7 +125,7 @@ class FilterBank:
         self.ws_bytes = int(ws)
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, **kw)
         if est_buffer is None:
-            self.est = torch.empty((self.T, self.M, self.est_dim), dtype=torch.float64, **kw)
+            self.est = torch.empty((self.T, self.M, self.est_width), dtype=torch.float64, **kw)
             self.est_row = 0
         else:
             self.est = est_buffer
@@ -129,6 +146,7 @@ class FilterBank:
             self.anc1 = torch.empty(self.MN, dtype=torch.int32, **kw)
             self.anc_comp = torch.empty(self.MN, dtype=torch.int32, **kw)
             self.x_tmp = torch.empty_like(self.x[0])
+            self.q_tmp = torch.empty_like(self.q[0]) if self.q[0] is not None else None
             self.lnc_before = torch.empty(self.M, dtype=torch.float64, **kw)
             self.coll1 = torch.empty(self.M, dtype=torch.uint8, **kw)
 
@@ -168,6 +186,9 @@ class FilterBank:
                 ztape = torch.from_numpy(z).to(self.device)
             _lib.call("pf_lorenz_prior", self.code, _lib.ptr(self.x[0]), self.M, self.N, mean_p,
                       m.prior_sd(), _lib.ptr(self.keys), _lib.ptr(ztape), s)
+        elif m.kind == "fhnnet":
+            self.x[0].zero_()  # quiescent prior, no history (fhn.py:144-147)
+            self.q[0].zero_()
         else:
             row = torch.from_numpy(m.initial_state()).to(self.device)
             _lib.call("pf_fill_rows", self.code, _lib.ptr(self.x[0]), self.MN, m.dim_x,
@@ -179,9 +200,16 @@ class FilterBank:
         self.steps_done = 0
 
     # -- one observation interval --------------------------------------------
-    def _propagate(self, params, xin, anc, xout, y_ptr, logw, t, noise):
+    def _propagate(self, params, xin, anc, xout, y_ptr, logw, t, noise, qin=None, qout=None):
         s = _lib.stream_ptr()
-        if self.model.kind == "lorenz":
+        if self.model.kind == "fhnnet":
+            stim, z = noise if noise is not None else (None, None)
+            _lib.call("pf_fhnnet_step", params, self.code, _lib.ptr(xin), _lib.ptr(qin),
+                      _lib.ptr(anc), _lib.ptr(xout), _lib.ptr(qout), _lib.ptr(self.fmask),
+                      y_ptr, _lib.ptr(self.obs_idx), _lib.ptr(logw), self.M, self.N,
+                      _lib.ptr(self.keys), t, _lib.ptr(stim), _lib.ptr(z),
+                      _lib.ptr(self.status), s)
+        elif self.model.kind == "lorenz":
             _lib.call("pf_lorenz_propagate_weight", params, self.code, _lib.ptr(xin),
                       _lib.ptr(anc), _lib.ptr(xout), y_ptr, _lib.ptr(logw), self.M, self.N,
                       _lib.ptr(self.keys), t, _lib.ptr(noise), _lib.ptr(self.status), s)
@@ -211,11 +239,18 @@ class FilterBank:
         import ctypes
 
         d = _lib.BankDesc()
-        d.model = _lib.PF_MODEL_LORENZ if self.model.kind == "lorenz" else _lib.PF_MODEL_FHN
+        d.model = {"lorenz": _lib.PF_MODEL_LORENZ, "fhn": _lib.PF_MODEL_FHN,
+                   "fhnnet": _lib.PF_MODEL_FHNNET}[self.model.kind]
         d.dtype = self.code
         d.M, d.N = self.M, self.N
         if self.model.kind == "lorenz":
             d.lorenz = ctypes.pointer(self.params)
+        elif self.model.kind == "fhnnet":
+            d.fhnnet = ctypes.pointer(self.params)
+            d.obs_idx = self.obs_idx.data_ptr()
+            d.q[0], d.q[1] = self.q[0].data_ptr(), self.q[1].data_ptr()
+            d.forcing_mask = self.fmask.data_ptr()
+            d.est_bits = self.est_bits
         else:
             d.fhn = ctypes.pointer(self.params)
             d.obs_idx = self.obs_idx.data_ptr()
@@ -226,7 +261,8 @@ class FilterBank:
         d.obs, d.dim_y = self.obs.data_ptr(), self.model.dim_y
         d.est = self.est.data_ptr()
         d.est_step_stride = self.est.stride(0)
-        d.est_offset = self.est_row * self.est_dim
+        d.est_offset = self.est_row * self.est_width
+        d.est_stride_f = self.est_width
         d.est_stride_p, d.est_stride_d = self.est_strides
         d.est_dim = self.est_dim
         d.lnc_trace = self.lnc_tr.data_ptr()
@@ -273,6 +309,8 @@ class FilterBank:
         noise = uni = uni1 = None
         if self.tape is not None:
             noise = self._tape(self.tape.noise, k)
+            if self.model.kind == "fhnnet":
+                noise = (self._tape(self.tape.stim, k), noise)
             uni = self._tape(self.tape.uniforms, k)
             if self.variant == "auxiliary":
                 uni1 = self._tape(self.tape.uniforms_first, k)
@@ -282,14 +320,19 @@ class FilterBank:
         else:
             if self.kernel_events is not None:
                 self.kernel_events[0].record()
-            self._propagate(self.params, xin, anc, xout, y_ptr, self.logw, t, noise)
+            self._propagate(self.params, xin, anc, xout, y_ptr, self.logw, t, noise,
+                            self.q[self.cur], self.q[1 - self.cur])
             if self.kernel_events is not None:
                 self.kernel_events[1].record()
             self._resample(self.logw, uni, t, self.anc)
-        est_ptr = _lib.c_vp(self.est[k].data_ptr() + self.est_row * self.est_dim * 8)
+        est_base = self.est[k].data_ptr() + self.est_row * self.est_width * 8
         sp, sd = self.est_strides
-        _lib.call("pf_filter_estimate", self.code, _lib.ptr(xout), sp, sd, self.est_dim,
-                  _lib.ptr(self.anc), self.M, self.N, est_ptr, s)
+        _lib.call("pf_filter_estimate_strided", self.code, _lib.ptr(xout), sp, sd, self.est_dim,
+                  _lib.ptr(self.anc), self.M, self.N, _lib.c_vp(est_base), self.est_width, s)
+        if self.est_bits:
+            _lib.call("pf_bits_estimate", _lib.ptr(self.q[1 - self.cur]), self.model.nodes,
+                      self.est_bits, _lib.ptr(self.anc), self.M, self.N,
+                      _lib.c_vp(est_base + self.est_dim * 8), self.est_width, s)
         self.lnc_tr[k].copy_(self.lnc)
         self.coll_tr[k].copy_(self.collapsed)
         self.cur = 1 - self.cur
@@ -299,7 +342,8 @@ class FilterBank:
         """apf_step (filters.py:115-154) on the whole bank."""
         s = _lib.stream_ptr()
         # first stage: lambda = log p(y | noise-free prediction)
-        self._propagate(self.params0, xin, anc_prev, self.x_tmp, y_ptr, self.lam, t, noise)
+        self._propagate(self.params0, xin, anc_prev, self.x_tmp, y_ptr, self.lam, t, noise,
+                        self.q[self.cur], self.q_tmp)
         _lib.call("pf_apf_first_stage_prepare", self.code, _lib.ptr(self.lam), self.M, self.N,
                   _lib.ptr(self.coll1), s)
         self.lnc_before.copy_(self.lnc)
@@ -310,7 +354,8 @@ class FilterBank:
         # second stage: propagate the chosen ancestors, weights / lambda[anc1]
         if self.kernel_events is not None:
             self.kernel_events[0].record()
-        self._propagate(self.params, xin, self.anc_comp, xout, y_ptr, self.logw, t, noise)
+        self._propagate(self.params, xin, self.anc_comp, xout, y_ptr, self.logw, t, noise,
+                        self.q[self.cur], self.q[1 - self.cur])
         if self.kernel_events is not None:
             self.kernel_events[1].record()
         _lib.call("pf_apf_second_stage_weights", self.code, _lib.ptr(self.logw),
@@ -337,6 +382,9 @@ class FilterBank:
         import torch
 
         x = self.x[self.cur]
+        if self.model.kind == "fhnnet":
+            anc = self.anc if self.steps_done > 0 else None
+            return self.model.from_device(x, self.q[self.cur], anc).reshape(self.M, self.N, -1)
         anc = self.anc.long() if self.steps_done > 0 else torch.arange(self.MN, device=x.device)
         if self.model.kind == "lorenz":
             g = x[:, anc].t()

@@ -14,6 +14,10 @@ extern "C" int pf_lorenz_propagate_weight(const pf_lorenz_params *, pf_dtype, co
                                           const int32_t *, void *, const double *, void *,
                                           int64_t, int64_t, const uint32_t *, uint32_t,
                                           const double *, uint32_t *, void *);
+extern "C" int pf_fhnnet_step(const pf_fhnnet_params *, pf_dtype, const void *, const uint32_t *,
+                              const int32_t *, void *, uint32_t *, const double *, const double *,
+                              const int32_t *, void *, int64_t, int64_t, const uint32_t *,
+                              uint32_t, const double *, const double *, uint32_t *, void *);
 extern "C" int pf_fhn_interval(const pf_fhn_params *, pf_dtype, const void *, const int32_t *,
                                void *, const double *, const int32_t *, void *, int64_t, int64_t,
                                const uint32_t *, uint32_t, const double *, uint32_t *, void *);
@@ -25,8 +29,12 @@ extern "C" {
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream) {
   PF_REQUIRE(d && n_steps >= 0 && k0 >= 0 && (cur == 0 || cur == 1), "pf_bank_run: bad arguments");
-  PF_REQUIRE(d->model == PF_MODEL_LORENZ ? d->lorenz != nullptr
-                                         : (d->model == PF_MODEL_FHN && d->fhn && d->obs_idx),
+  PF_REQUIRE(d->model == PF_MODEL_LORENZ
+                 ? d->lorenz != nullptr
+                 : d->model == PF_MODEL_FHN
+                       ? (d->fhn && d->obs_idx)
+                       : (d->model == PF_MODEL_FHNNET && d->fhnnet && d->obs_idx && d->q[0] &&
+                          d->q[1] && d->forcing_mask),
              "pf_bank_run: model descriptor missing");
   PF_REQUIRE(d->x[0] && d->x[1] && d->logw && d->anc && d->lnc && d->collapsed && d->status &&
                  d->keys && d->obs && d->est,
@@ -58,6 +66,10 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     if (d->model == PF_MODEL_LORENZ)
       rc = pf_lorenz_propagate_weight(d->lorenz, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
                                       d->keys, t, nullptr, d->status, stream);
+    else if (d->model == PF_MODEL_FHNNET)
+      rc = pf_fhnnet_step(d->fhnnet, d->dtype, xin, d->q[cur], anc, xout, d->q[cur ^ 1],
+                          d->forcing_mask, y, d->obs_idx, d->logw, d->M, d->N, d->keys, t,
+                          nullptr, nullptr, d->status, stream);
     else
       rc = pf_fhn_interval(d->fhn, d->dtype, xin, anc, xout, y, d->obs_idx, d->logw, d->M, d->N,
                            d->keys, t, nullptr, d->status, stream);
@@ -68,9 +80,16 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                                   nullptr, 0, 0u, stream);
     if (rc) return rc;
     double *est = d->est + static_cast<int64_t>(k) * d->est_step_stride + d->est_offset;
-    rc = pf_filter_estimate(d->dtype, xout, d->est_stride_p, d->est_stride_d, d->est_dim, d->anc,
-                            d->M, d->N, est, stream);
+    const int64_t est_f = d->est_stride_f ? d->est_stride_f : d->est_dim;
+    rc = pf_filter_estimate_strided(d->dtype, xout, d->est_stride_p, d->est_stride_d, d->est_dim,
+                                    d->anc, d->M, d->N, est, est_f, stream);
     if (rc) return rc;
+    if (d->model == PF_MODEL_FHNNET && d->est_bits > 0) {
+      const int32_t nodes = d->fhnnet->J * d->fhnnet->J;
+      rc = pf_bits_estimate(d->q[cur ^ 1], nodes, d->est_bits, d->anc, d->M, d->N,
+                            est + d->est_dim, est_f, stream);
+      if (rc) return rc;
+    }
     if (d->lnc_trace &&
         cudaMemcpyAsync(d->lnc_trace + static_cast<int64_t>(k) * d->M, d->lnc,
                         d->M * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)

@@ -16,7 +16,7 @@ constexpr int kSmallDim = 8;
 template <typename T>
 __global__ void __launch_bounds__(256) estimate_small_kernel(
     const T *__restrict__ x, int64_t sp, int64_t sd, int dim, const int32_t *__restrict__ anc,
-    int32_t N, double invN, double *__restrict__ est) {
+    int32_t N, double invN, double *__restrict__ est, int64_t est_stride) {
   __shared__ double scratch[33];
   const int64_t f = blockIdx.x;
   double acc[kSmallDim];
@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) estimate_small_kernel(
   }
   for (int d = 0; d < dim; ++d) {
     const double s = block_sum(acc[d], scratch);
-    if (threadIdx.x == 0) est[f * dim + d] = __dmul_rn(s, invN);
+    if (threadIdx.x == 0) est[f * est_stride + d] = __dmul_rn(s, invN);
   }
 }
 
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) estimate_small_kernel(
 template <typename T>
 __global__ void __launch_bounds__(256) estimate_wide_kernel(
     const T *__restrict__ x, int64_t sp, int64_t sd, int dim, const int32_t *__restrict__ anc,
-    int32_t N, double invN, double *__restrict__ est) {
+    int32_t N, double invN, double *__restrict__ est, int64_t est_stride) {
   __shared__ double part[8][32];
   const int64_t f = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) estimate_wide_kernel(
   if (warp == 0 && d < dim) {
     double s = part[0][lane];
     for (int w = 1; w < 8; ++w) s = __dadd_rn(s, part[w][lane]);
-    est[f * dim + d] = __dmul_rn(s, invN);
+    est[f * est_stride + d] = __dmul_rn(s, invN);
   }
 }
 
@@ -72,10 +72,11 @@ using namespace pf;
 
 extern "C" {
 
-int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,
-                       int32_t dim, const int32_t *anc, int64_t M, int64_t N, double *est_out,
-                       void *stream) {
-  PF_REQUIRE(x && anc && est_out && dim >= 1 && M >= 1 && N >= 1 && M * N <= INT32_MAX,
+int pf_filter_estimate_strided(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,
+                               int32_t dim, const int32_t *anc, int64_t M, int64_t N,
+                               double *est_out, int64_t est_stride, void *stream) {
+  PF_REQUIRE(x && anc && est_out && dim >= 1 && M >= 1 && N >= 1 && M * N <= INT32_MAX &&
+                 est_stride >= dim,
              "pf_filter_estimate: bad arguments");
   const cudaStream_t s = as_stream(stream);
   const double invN = 1.0 / static_cast<double>(N);  // uniform_weights value, core.py:112-113
@@ -83,20 +84,27 @@ int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t 
   if (dim <= kSmallDim) {
     if (dtype == PF_F64)
       estimate_small_kernel<double><<<static_cast<unsigned>(M), 256, 0, s>>>(
-          static_cast<const double *>(x), stride_p, stride_d, dim, anc, n32, invN, est_out);
+          static_cast<const double *>(x), stride_p, stride_d, dim, anc, n32, invN, est_out, est_stride);
     else
       estimate_small_kernel<float><<<static_cast<unsigned>(M), 256, 0, s>>>(
-          static_cast<const float *>(x), stride_p, stride_d, dim, anc, n32, invN, est_out);
+          static_cast<const float *>(x), stride_p, stride_d, dim, anc, n32, invN, est_out, est_stride);
   } else {
     const dim3 grid(static_cast<unsigned>(M), static_cast<unsigned>((dim + 31) / 32));
     if (dtype == PF_F64)
       estimate_wide_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double *>(x), stride_p,
-                                                        stride_d, dim, anc, n32, invN, est_out);
+                                                        stride_d, dim, anc, n32, invN, est_out, est_stride);
     else
       estimate_wide_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float *>(x), stride_p,
-                                                       stride_d, dim, anc, n32, invN, est_out);
+                                                       stride_d, dim, anc, n32, invN, est_out, est_stride);
   }
   return check_launch("pf_filter_estimate");
+}
+
+int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,
+                       int32_t dim, const int32_t *anc, int64_t M, int64_t N, double *est_out,
+                       void *stream) {
+  return pf_filter_estimate_strided(dtype, x, stride_p, stride_d, dim, anc, M, N, est_out, dim,
+                                    stream);
 }
 
 }  // extern "C"

@@ -180,10 +180,20 @@ __global__ void __launch_bounds__(256) fhn_interval_kernel(
     }
     if (!fin) bad = 1;
     const T *fin_v = vs + buf * c.nodes;
-    if (tid < 32) {
-      // numpy pairwise order for n <= 128 (8 strided accumulators, then
-      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder) - the
-      // order of np.sum(resid*resid, axis=1) in fhn.py:207.
+    if (tid == 0 && N >= 2) {
+      // a filter of N >= 2 particles: np.sum(resid*resid, axis=1) over the
+      // column-major fancy-indexed block is a sequential sum (npsum.cuh)
+      double res = 0.0;
+      for (int i = 0; i < c.n_obs; ++i) {
+        const double rsd = __dsub_rn(y[i], double(fin_v[obs_idx[i]]));
+        const double sq = __dmul_rn(rsd, rsd);
+        res = i == 0 ? sq : __dadd_rn(res, sq);
+      }
+      red[0] = res;
+    } else if (tid < 32 && N < 2) {
+      // a single particle: contiguous row, numpy pairwise order for n <= 128
+      // (8 strided accumulators, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+      // then the remainder).
       const int n = c.n_obs;
       const int lane = tid;
       double acc = 0.0;

@@ -16,6 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib, dist, philox
+from .models import estimate_width
 from .bank import DrawTape, FilterBank
 from .filters import FilterOutput, _bank_seconds, _validate
 
@@ -96,10 +97,7 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     keys = philox.filter_keys(master_seed, n_filters)
     started = time.perf_counter()
     dev = torch.device("cuda", torch.cuda.current_device())
-    if model.kind == "lorenz":
-        est_dim = 3
-    else:
-        est_dim = model.dim_x if estimate == "full" else model.nodes
+    est_dim = estimate_width(model, estimate)
     est_full = torch.zeros((T, n_filters, est_dim), dtype=torch.float64, device=dev)
     bank = FilterBank(model, hi - lo, n_particles, keys[lo:hi], T, dtype=dtype, tape=tape,
                       filter_offset=lo, estimate=estimate, est_buffer=est_full,

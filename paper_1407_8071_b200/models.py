@@ -7,6 +7,8 @@
 * :class:`FhnLatticeModel` - the classical FitzHugh-Nagumo lattice of
   BASELINE cfg3/cfg4 expressed in the reference lattice kernel's general form
   (accel.py:110-129; mapping in SURVEY §8a-A9 and DESIGN.md §2).
+* :class:`FhnNetworkModel` - the paper's stochastically forced FH-N network
+  (parpf/models/fhn.py:85-207): same fields, state row and hooks.
 
 Their per-hook methods (sample_prior, sample_transition, log_likelihood,
 transition_point_prediction) run on the GPU through libpfbank in fp64 with
@@ -35,6 +37,16 @@ def _torch():
 
     _lib.require_cuda()
     return torch
+
+
+def estimate_width(model, estimate: str) -> int:
+    """Columns of one filter's estimate row: the full state or the error
+    projection (the voltage block of the lattice models)."""
+    if estimate not in ("full", "projection"):
+        raise ValueError("estimate must be 'full' or 'projection'")
+    if model.kind == "lorenz":
+        return 3
+    return model.dim_x if estimate == "full" else model.nodes
 
 
 @dataclass
@@ -266,3 +278,227 @@ class FhnLatticeModel(StateSpaceModel):
 
     def error_projection(self, states):
         return np.asarray(states)[..., : self.nodes]
+
+
+# ---------------------------------------------------------------------------
+# The paper's forced FH-N network (parpf/models/fhn.py)
+# ---------------------------------------------------------------------------
+
+
+def von_neumann_neighbors(i: int, j: int, J: int) -> list[tuple[int, int]]:
+    """Axis neighbours of (i, j) truncated at the border, order up, down,
+    left, right (fhn.py:38-49)."""
+    return [(a, b) for a, b in ((i - 1, j), (i + 1, j), (i, j - 1), (i, j + 1))
+            if 0 <= a < J and 0 <= b < J]
+
+
+def fhn_stimulus_region(U, u_minus: float = -1.8, u_plus: float = -1.6) -> np.ndarray:
+    """Mask of nodes whose own or an axis neighbour's voltage lies strictly in
+    (u_minus, u_plus) on the trailing two axes (fhn.py:52-67).  Host helper;
+    the bank evaluates the region inside pf_fhnnet_step."""
+    U = np.asarray(U)
+    band = (U > u_minus) & (U < u_plus)
+    out = band.copy()
+    out[..., 1:, :] |= band[..., :-1, :]
+    out[..., :-1, :] |= band[..., 1:, :]
+    out[..., :, 1:] |= band[..., :, :-1]
+    out[..., :, :-1] |= band[..., :, 1:]
+    return out
+
+
+def observation_zone_indices(J: int, n_zones: int = 5, zone_width: int = 2) -> np.ndarray:
+    """Sorted flat indices of an n_zones x n_zones grid of square zones
+    (fhn.py:70-82)."""
+    if n_zones * zone_width > J:
+        raise ValueError("observation zones do not fit on the lattice")
+    starts = ([(J - zone_width) // 2] if n_zones == 1
+              else [(k * (J - zone_width)) // (n_zones - 1) for k in range(n_zones)])
+    lines = np.concatenate([np.arange(s0, s0 + zone_width) for s0 in starts])
+    return np.sort((lines[:, None] * J + lines[None, :]).reshape(-1)).astype(np.intp)
+
+
+@dataclass
+class FhnNetworkModel(StateSpaceModel):
+    """Drop-in for parpf.models.FhnNetworkModel (fhn.py:85-207).
+
+    Same fields and defaults, same flat state row
+    ``[U, V, Q(t), .., Q(t-stim_hold+1)]`` at the hook boundary.  On the GPU
+    the history is held as bits (stim_hold <= 32), U/V as fp32 or fp64
+    planes; the hooks run in fp64 and reproduce the reference bit-for-bit
+    for the same Generator draws.
+    """
+
+    J: int = 32
+    dt: float = 5e-3
+    coupling: float = 4.5e-3
+    cubic: tuple = (-1.0, 0.0, 18.0 / 5.0, 0.0)
+    beta: tuple = (2.1, -0.6, 0.6)
+    u_minus: float = -1.8
+    u_plus: float = -1.6
+    stim_prob: float = 1e-3
+    stim_amp: float = 200.0
+    stim_hold: int = 25
+    forcing_amp: float = 200.0
+    forcing_period: float = 20.0
+    forcing_width: float = 1.0
+    forcing_mask: np.ndarray | None = None
+    dyn_var: float = 0.5
+    obs_var: float = 0.5
+    n_zones: int = 5
+    zone_width: int = 2
+
+    kind = "fhnnet"
+
+    def __post_init__(self):
+        if self.u_minus >= self.u_plus:
+            raise ValueError("u_minus must be below u_plus")
+        if self.stim_hold < 1:
+            raise ValueError("stim_hold must be >= 1")
+        if self.stim_hold > 32:
+            raise ValueError("stim_hold > 32 is not supported (history is a 32-bit field)")
+        J = self.J
+        if self.forcing_mask is None:
+            mask = np.zeros((J, J))
+            mask[:, 0] = 1.0
+            self.forcing_mask = mask
+        else:
+            self.forcing_mask = np.asarray(self.forcing_mask, dtype=np.float64)
+            if self.forcing_mask.shape != (J, J):
+                raise ValueError("forcing_mask must be (J, J)")
+        self.obs_indices = observation_zone_indices(J, self.n_zones, self.zone_width)
+        self.nodes = J * J
+        self.dim_x = (2 + self.stim_hold) * self.nodes
+        self.dim_y = self.obs_indices.shape[0]
+        self._sig_sqdt = np.sqrt(self.dyn_var) * np.sqrt(self.dt)
+
+    # -- state packing (fhn.py:122-138) --------------------------------------
+    def unpack(self, x):
+        x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+        n, K = x.shape[0], self.nodes
+        return (x[:, :K].reshape(n, self.J, self.J), x[:, K:2 * K].reshape(n, self.J, self.J),
+                x[:, 2 * K:].reshape(n, self.stim_hold, self.J, self.J))
+
+    def pack(self, U, V, Q):
+        n = U.shape[0]
+        return np.concatenate([U.reshape(n, -1), V.reshape(n, -1), Q.reshape(n, -1)], axis=1)
+
+    # -- device descriptor ------------------------------------------------------
+    def params(self, n_sub=None, noise_free=False) -> _lib.FhnNetParams:
+        p = _lib.FhnNetParams()
+        p.J, p.stim_hold, p.n_obs = self.J, self.stim_hold, self.dim_y
+        p.stochastic = 0 if noise_free else 1
+        p.dt, p.coupling = float(self.dt), float(self.coupling)
+        for i in range(4):
+            p.cubic[i] = float(self.cubic[i])
+        for i in range(3):
+            p.beta[i] = float(self.beta[i])
+        p.u_minus, p.u_plus = float(self.u_minus), float(self.u_plus)
+        p.stim_prob, p.stim_amp = float(self.stim_prob), float(self.stim_amp)
+        p.forcing_amp = float(self.forcing_amp)
+        p.forcing_period = float(self.forcing_period)
+        p.forcing_width = float(self.forcing_width)
+        p.sig_sqdt = float(self._sig_sqdt)
+        p.obs_var = float(self.obs_var)
+        return p
+
+    def device_mask(self, device="cuda"):
+        torch = _torch()
+        return torch.from_numpy(np.ascontiguousarray(self.forcing_mask.reshape(-1))).to(device)
+
+    def to_device(self, rows, dtype=None):
+        """Reference rows (n, dim_x) -> device (U/V planes, history bits)."""
+        torch = _torch()
+        dtype = dtype or torch.float64
+        rows = np.atleast_2d(np.asarray(rows, dtype=np.float64))
+        if rows.shape[1] != self.dim_x:
+            raise ValueError(f"expected states with {self.dim_x} columns, got {rows.shape[1]}")
+        q = rows[:, 2 * self.nodes:]
+        if not np.all((q == 0.0) | (q == 1.0)):
+            raise ValueError("stimulus history entries must be 0 or 1")
+        n = rows.shape[0]
+        d_rows = torch.from_numpy(np.ascontiguousarray(rows)).cuda()
+        x = torch.empty((n, 2 * self.nodes), dtype=dtype, device="cuda")
+        qb = torch.empty((n, self.nodes), dtype=torch.int32, device="cuda")
+        _lib.call("pf_fhnnet_pack", _lib.dtype_code(dtype), _lib.ptr(d_rows), n, self.nodes,
+                  self.stim_hold, _lib.ptr(x), _lib.ptr(qb), _lib.stream_ptr())
+        return x, qb
+
+    def from_device(self, x, qb, anc=None):
+        torch = _torch()
+        n = int(anc.numel()) if anc is not None else int(x.shape[0])
+        rows = torch.empty((n, self.dim_x), dtype=torch.float64, device=x.device)
+        _lib.call("pf_fhnnet_unpack", _lib.dtype_code(x.dtype), _lib.ptr(x), _lib.ptr(qb),
+                  _lib.ptr(anc), n, self.nodes, self.stim_hold, _lib.ptr(rows),
+                  _lib.stream_ptr())
+        return rows.cpu().numpy()
+
+    # -- model hooks -------------------------------------------------------------
+    def sample_prior(self, rng, n):
+        # quiescent start, no draws (fhn.py:144-147)
+        return np.zeros((n, self.dim_x))
+
+    def forcing_value(self, t: int) -> float:
+        s = t * self.dt
+        return self.forcing_amp if np.mod(s, self.forcing_period) <= self.forcing_width else 0.0
+
+    def _advance(self, x_prev, t, rng=None):
+        torch = _torch()
+        x_prev = np.atleast_2d(np.asarray(x_prev, dtype=np.float64))
+        n = x_prev.shape[0]
+        x, qb = self.to_device(x_prev)
+        xo, qo = torch.empty_like(x), torch.empty_like(qb)
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        stim = z = None
+        if rng is not None:
+            # draw order of fhn.py:158-176: fire, select, then the noise
+            fire, sel = rng.random(n), rng.random(n)
+            noise = rng.standard_normal((n, self.J, self.J))
+            stim = torch.from_numpy(np.stack([fire, sel])).cuda()
+            z = torch.from_numpy(np.ascontiguousarray(noise.reshape(n, -1))).cuda()
+        mask = self.device_mask()
+        _lib.call("pf_fhnnet_step", self.params(noise_free=rng is None), _lib.PF_F64,
+                  _lib.ptr(x), _lib.ptr(qb), None, _lib.ptr(xo), _lib.ptr(qo), _lib.ptr(mask),
+                  None, None, None, 1, n, None, int(t), _lib.ptr(stim), _lib.ptr(z),
+                  _lib.ptr(st), _lib.stream_ptr())
+        if int(st.item()) & _lib.PF_ST_DIVERGED:
+            raise NumericalDivergenceError("FH-N transition produced non-finite states")
+        return self.from_device(xo, qo)
+
+    def sample_transition(self, x_prev, t, rng):
+        return self._advance(x_prev, t, rng)
+
+    def transition_point_prediction(self, x_prev, t):
+        # no new random stimulus, no noise; forcing and latched stimuli apply
+        return self._advance(x_prev, t, rng=None)
+
+    def log_likelihood(self, y, x, t):
+        torch = _torch()
+        y = np.asarray(y, dtype=np.float64).reshape(-1)
+        if y.shape[0] != self.dim_y:
+            raise ValueError(f"expected {self.dim_y} observed nodes, got {y.shape[0]}")
+        x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+        n = x.shape[0]
+        d_x = torch.from_numpy(np.ascontiguousarray(x[:, : self.nodes])).cuda()
+        d_y = torch.from_numpy(y).cuda()
+        idx = torch.from_numpy(self.obs_indices.astype(np.int32)).cuda()
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.call("pf_zone_loglik", _lib.PF_F64, _lib.ptr(d_x), n, self.nodes, _lib.ptr(idx),
+                  self.dim_y, _lib.ptr(d_y), float(self.obs_var), _lib.ptr(out),
+                  _lib.stream_ptr())
+        return out.cpu().numpy()
+
+    def sample_observation(self, x, t, rng):
+        x = np.asarray(x).reshape(-1)
+        u_obs = x[: self.nodes][self.obs_indices]
+        return u_obs + np.sqrt(self.obs_var) * rng.standard_normal(self.dim_y)
+
+    def error_projection(self, states):
+        """Voltage block (fhn.py:214-217)."""
+        return np.asarray(states)[..., : self.nodes]
+
+
+def simulate(model, n_steps: int, seed):
+    """parpf.models.simulate (models/simulate.py:10-29); see simulate.py."""
+    from .simulate import simulate as _simulate
+
+    return _simulate(model, n_steps, seed)

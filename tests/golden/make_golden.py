@@ -307,11 +307,58 @@ def gen_fhn():
     np.savez_compressed(os.path.join(HERE, "fhn.npz"), **d)
 
 
+def gen_fhnnet():
+    """The paper's forced FH-N network (models/fhn.py:85-207), stock model."""
+    from parpf.models import FhnNetworkModel
+    from parpf.models import simulate as ref_simulate
+
+    d = {}
+    kw8 = dict(J=8, n_zones=2, zone_width=2, stim_prob=0.05)
+    m8 = FhnNetworkModel(**kw8)
+    d["m8_stim_prob"] = np.array(kw8["stim_prob"])
+    st8, ob8 = ref_simulate(m8, 120, 3)
+    d["sim8_states"], d["sim8_obs"] = st8, ob8
+    m16 = FhnNetworkModel(J=16, stim_prob=0.02)
+    d["sim16_states"], d["sim16_obs"] = ref_simulate(m16, 150, 3)
+    # hooks on hand-made states: latched history, forcing on/off, band region
+    rng = np.random.default_rng(55)
+    x = np.zeros((5, m8.dim_x))
+    x[:, : 2 * 64] = rng.normal(size=(5, 128)) * 2.0
+    q = (rng.random((5, m8.stim_hold * 64)) < 0.05).astype(float)
+    x[:, 2 * 64:] = q
+    d["hook_x"] = x
+    d["tpp_t1"] = m8.transition_point_prediction(x, 1)
+    d["tpp_t250"] = m8.transition_point_prediction(x, 250)
+    xb = x.copy()
+    xb[:, :64] = -1.7
+    xb[2, :64] = 0.0  # no region for particle 2
+    d["band_x"] = xb
+    mfire = FhnNetworkModel(**{**kw8, "stim_prob": 1.0})
+    d["band_out"] = mfire.sample_transition(xb, 7, np.random.default_rng(19))
+    y = rng.normal(size=m8.dim_y)
+    d["ll_y"] = y
+    d["ll_out"] = m8.log_likelihood(y, x, 1)
+    # filters on the simulated record
+    out, calls = _filter_with_steps(m8, ob8[:60], 32, np.random.SeedSequence(808))
+    d["f_est"], d["f_lnc"] = out.estimates, out.log_norm_const
+    d["f_u"] = np.stack([c[0] for c in calls])
+    d["f_anc"] = np.stack([c[1] for c in calls])
+    outa, calls = _filter_with_steps(m8, ob8[:40], 24, np.random.SeedSequence(909), "auxiliary")
+    d["a_est"], d["a_lnc"] = outa.estimates, outa.log_norm_const
+    d["a_anc1"] = np.stack([c[1] for c in calls[0::2]])
+    d["a_anc2"] = np.stack([c[1] for c in calls[1::2]])
+    ens = parpf.run_ensemble(m8, ob8[:40], "bootstrap", 3, 16, 21)
+    d["e_mean"] = ens.mean_estimates
+    d["e_lnc"] = np.stack([fo.log_norm_const for fo in ens.filter_outputs])
+    np.savez_compressed(os.path.join(HERE, "fhnnet.npz"), **d)
+
+
 if __name__ == "__main__":
     print("reference backend:", accel.backend_name())
     gen_kernels()
     gen_lorenz()
     gen_fhn()
+    gen_fhnnet()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -87,3 +87,53 @@ def test_product_fails_loudly_without_cuda():
 
     with pytest.raises(RuntimeError, match="CUDA"):
         pf.normalize_log_weights(np.zeros(4))
+
+
+def _header_prototypes():
+    src = open(os.path.join(REPO, "include", "pfbank.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(pf_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", src):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else len(args.split(","))
+    return out
+
+
+def test_ctypes_argument_counts_match_header():
+    from paper_1407_8071_b200 import _lib
+
+    protos = _header_prototypes()
+    for name, (_, argtypes) in _lib.SIGNATURES.items():
+        assert protos[name] == len(argtypes), name
+
+
+def test_ctypes_struct_layouts_match_c(tmp_path):
+    """sizeof/offsetof of every ABI struct as gcc lays it out == ctypes."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    from paper_1407_8071_b200 import _lib
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    structs = {"pf_lorenz_params": _lib.LorenzParams, "pf_fhn_params": _lib.FhnParams,
+               "pf_fhnnet_params": _lib.FhnNetParams, "pf_bank_desc": _lib.BankDesc}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pfbank.h"',
+             "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(REPO, "include"), str(c), "-o", str(exe)],
+                   check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True,
+                                                       text=True, check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, (cname, fname)
