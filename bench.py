@@ -52,10 +52,16 @@ CONFIGS = {
                        "N(0, sigma^2), logsumexp + multinomial + 3-float ancestor gather"),
     "cfg0": dict(kind="lorenz", M=4, N=1000, dtype="float64",
                  desc="Lorenz-63, M=4 x N=1000, 40 Euler steps/obs, fp64"),
+    # the paper's own lattice (models/fhn.py:85-207): not a
+    # BASELINE config; same metric, one Euler step per observation
+    "net": dict(kind="fhnnet", M=64, N=4096, dtype="float32",
+                desc="paper FH-N network 32x32 (stimuli, forcing, 25-step history), "
+                     "M=64 x N=4096, 1 Euler step/obs, fp32"),
 }
 
 # Algorithmic work per particle-step
 FHN_BYTES_PER_PS = 24000.0   # 16 B/node/Euler step (v,w read+write fp32) x 1500 nodes
+NET_BYTES_PER_NODE = 24.0    # U,V fp32 + history bits, read + write, per node-step
 LORENZ_FLOP_PER_PS = 20.0    # FMA = 2 (accel.py:73-75)
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4
 
@@ -156,6 +162,11 @@ def _make_model_and_obs(cfg, n_obs, seed=2026):
 
     if cfg["kind"] == "fhn":
         model, _, obs = simulate.fhn_truth(seed, n_obs, FhnLatticeModel())
+    elif cfg["kind"] == "fhnnet":
+        from paper_1407_8071_b200.models import FhnNetworkModel
+
+        model = FhnNetworkModel()
+        _, obs = simulate.simulate(model, n_obs, seed)
     else:
         base = Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3")
         truth0, _, obs = simulate.lorenz_truth(seed, n_obs, base)
@@ -182,6 +193,10 @@ def cpu_baseline(cfg, budget_s=12.0, steps=1):
         model, _, obs = orc.fhn_truth(seed=2026, n_obs=max(steps, 1))
         n_part, per_ps = 16, None
         n_sub = model.substeps
+    elif cfg["kind"] == "fhnnet":
+        model = orc.FhnNetworkModel()
+        _, obs = orc.simulate(model, max(steps, 1), 2026)
+        n_part, n_sub = 64, 1
     else:
         truth0, _, obs = orc.lorenz_truth(seed=2026, n_obs=max(steps, 1))
         model = orc.LorenzConfigModel(prior_mean=tuple(truth0))
@@ -198,6 +213,9 @@ def cpu_baseline(cfg, budget_s=12.0, steps=1):
     workers = min(cores, n_filters)
     if cfg["kind"] == "fhn":
         n_part = max(4, min(256, int(16 * budget_s / max(steps, 1) / one)))
+        n_filters = cores
+    elif cfg["kind"] == "fhnnet":
+        n_part = max(16, min(cfg["N"], int(64 * budget_s / max(steps, 1) / one)))
         n_filters = cores
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=workers, mp_context=get_context("fork")) as pool:
@@ -378,7 +396,7 @@ def run_ours(args, cfg):
         raise SystemExit(f"M={M} not divisible by {world} GPUs")
     T = args.warmup + args.steps
     model, obs = _make_model_and_obs(cfg, T)
-    n_sub = model.substeps
+    n_sub = getattr(model, "substeps", 1)
     lo, hi = pdist.shard_range(M, rank, world)
     keys = philox.filter_keys(7, M)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -427,7 +445,15 @@ def run_ours(args, cfg):
     ps_per_launch = (hi - lo) * N * n_sub
 
     peaks, peak_src = _peaks()
-    if cfg["kind"] == "fhn":
+    if cfg["kind"] == "fhnnet":
+        per_ps = NET_BYTES_PER_NODE * model.nodes
+        achieved = ps_per_launch * per_ps / (kern_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
+                "kernel": "fhnnet_step_kernel<float,0,4>",
+                "algorithmic": f"{per_ps:.0f} B/particle-step (24 B/node: U,V fp32 + history "
+                               f"bits, read + write) x {ps_per_launch} particle-steps per launch"}
+    elif cfg["kind"] == "fhn":
         achieved = ps_per_launch * FHN_BYTES_PER_PS / (kern_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
@@ -484,8 +510,9 @@ def run_ours(args, cfg):
                 "config": {"workload": args.config, "desc": cfg["desc"], "M": M, "N": N,
                            "euler_steps_per_obs": n_sub, "parallelism": f"filters/{world}",
                            "l2": "inputs larger than L2 (state "
-                                 f"{2 * M * N * model.dim_x * 4 / 1e9:.2f} GB)"
-                           if cfg["kind"] == "fhn" else "state < L2; compute-bound kernel"},
+                                 f"{2 * M * N * _state_bytes(model):.3g} B, double-buffered)"
+                           if cfg["kind"] in ("fhn", "fhnnet")
+                           else "state < L2; compute-bound kernel"},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": 3 * args.steps,  # propagate, resample, estimate per step
                 "clocks": clocks.summary()}
@@ -495,6 +522,13 @@ def run_ours(args, cfg):
 
         dist.destroy_process_group()
     return 0
+
+
+def _state_bytes(model):
+    """Device bytes of one fp32 particle."""
+    if model.kind == "fhnnet":
+        return model.nodes * 12  # U, V fp32 + 32-bit history field
+    return model.dim_x * 4
 
 
 def _ncu_traffic(config):

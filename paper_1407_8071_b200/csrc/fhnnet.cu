@@ -25,11 +25,14 @@
 // cell search only runs for the ~stim_prob of particles that fire
 // (CTA-uniform branch).  fp64 uses the exact-order Ar<double> arithmetic and
 // is bit-identical to the reference on identical draws.
+#include "bulk.cuh"
 #include "common.cuh"
 #include "npsum.cuh"
 #include "philox.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace pf {
 
@@ -373,6 +376,298 @@ __global__ void __launch_bounds__(256) bits_estimate_kernel(
     if (k < nbits) e[static_cast<int64_t>(k) * nodes + node] = __dmul_rn(double(cnt[k]), invN);
 }
 
+// ---- fp32 production kernel: particle rows streamed by bulk copies ---------
+// Warp-specialised: one producer warp streams each particle's gathered
+// ancestor rows (U|V 8 B/node, history 4 B/node) into an S-stage shared
+// ring with cp.async.bulk (completion on full[s]) and publishes the
+// particle's per-step scalars with it (filter, index, Philox key, stimulus
+// draws); CW compute warps walk the same particle sequence
+// p = blockIdx.x + i*gridDim.x and release the stage through empty[s] (one
+// arrival per warp) - no CTA-wide barrier on the common path.  Each compute
+// thread owns the same 4-node group of every particle, so its lattice
+// position, boundary flags, forcing term and observation bits are computed
+// once per launch and live in registers.  Results leave as 16-B stores from
+// registers; the zone likelihood is summed per warp and the last warp to
+// finish a particle combines the partials in warp order (deterministic).
+struct NetMeta {
+  int64_t p, f;
+  uint32_t j, fire;
+  uint32_t k0, k1;
+  double sel;
+};
+
+template <int CW, int S>
+__global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW >= 2 ? 8 : 12) fhnnet_fast_kernel(
+    const float *__restrict__ xin, const uint32_t *__restrict__ qin,
+    const int32_t *__restrict__ anc, float *__restrict__ xout, uint32_t *__restrict__ qout,
+    const double *__restrict__ fmask, const double *__restrict__ y,
+    const int32_t *__restrict__ obs_idx, float *__restrict__ logw, int64_t MN, int32_t N,
+    NetConsts c, const uint32_t *__restrict__ keys, uint32_t t, uint32_t *__restrict__ status) {
+  using A = Ar<float>;
+  constexpr int kCompute = CW * 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int nodes = c.nodes;
+  const uint32_t stage_bytes = static_cast<uint32_t>(nodes) * 12u;
+  double *s_y = reinterpret_cast<double *>(smem_raw + S * stage_bytes);  // y at observed nodes
+  uint32_t *s_mask = reinterpret_cast<uint32_t *>(s_y + nodes);        // stimulus region bits
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  __shared__ NetMeta meta[S];
+  __shared__ double s_part[S][CW];
+  __shared__ int s_cnt[S];
+  __shared__ int s_cell;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int words = (nodes + 31) >> 5;
+  const int groups = nodes >> 2;
+  const int J = c.J;
+
+  if (tid == 0) {
+    for (int k = 0; k < S; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], CW);
+      s_cnt[k] = 0;
+    }
+    mbar_fence_init();
+  }
+  if (logw)
+    for (int i = tid; i < c.n_obs; i += blockDim.x) s_y[__ldg(obs_idx + i)] = y[i];
+  __syncthreads();
+
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t count = first < MN ? (MN - 1 - first) / stride + 1 : 0;
+
+  if (warp == CW) {  // ---- producer warp
+    if (lane == 0) {
+      for (int64_t i = 0; i < count; ++i) {
+        const int k = static_cast<int>(i % S);
+        if (i >= S) mbar_wait(&empty[k], static_cast<uint32_t>(((i / S) - 1) & 1));
+        const int64_t p = first + i * stride;
+        const int64_t f = p / N;
+        const uint32_t j = static_cast<uint32_t>(p - f * N);
+        const Key2 key = load_key(keys, f);
+        // stimulus draws (fhn.py:158-159): fire, then cell select
+        const uint4 r = philox10(make_uint4(j, t, 0u, kPurposeNetStim), key);
+        NetMeta &m = meta[k];
+        m.p = p;
+        m.f = f;
+        m.j = j;
+        m.fire = u53_closed0(r.x, r.y) < c.stim_prob;
+        m.sel = u53_closed0(r.z, r.w);
+        m.k0 = key.k0;
+        m.k1 = key.k1;
+        const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+        unsigned char *st = smem_raw + k * stage_bytes;
+        mbar_arrive_expect_tx(&full[k], stage_bytes);  // release: meta visible with the data
+        bulk_g2s(st, xin + src * 2 * static_cast<int64_t>(nodes), 8u * nodes, &full[k]);
+        bulk_g2s(st + 8 * nodes, qin + src * static_cast<int64_t>(nodes), 4u * nodes,
+                 &full[k]);
+      }
+    }
+    return;
+  }
+
+  // ---- compute warps: loop-invariant per-thread geometry
+  const int g = tid;  // node group (4 nodes, one lattice row)
+  const bool active = g < groups;
+  const int n0 = 4 * (active ? g : 0);
+  const int r = n0 / J, c0 = n0 - r * J;
+  const bool has_up = r > 0, has_dn = r < J - 1, has_l = c0 > 0, has_r = c0 + 4 < J;
+  float drv[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    drv[e] = active ? A::mul(float(__ldg(fmask + n0 + e)), float(c.forcing)) : 0.f;
+  uint32_t obits = 0;
+  if (logw && active)
+    for (int i = 0; i < c.n_obs; ++i) {
+      const int o = __ldg(obs_idx + i) - n0;
+      if (o >= 0 && o < 4) obits |= 1u << o;
+    }
+  const float dt = float(c.dt), fa3 = float(c.a3), fa2 = float(c.a2), fa1 = float(c.a1),
+              fa0 = float(c.a0), fb0 = float(c.b0), fb1 = float(c.b1), fb2 = float(c.b2),
+              fcpl = float(c.coupling), famp = float(c.stim_amp);
+  const float fsig = float(c.sig) * kSqrt2Ln2;  // normals from box_muller_fast_unscaled
+
+  for (int64_t i = 0; i < count; ++i) {
+    const int k = static_cast<int>(i % S);
+    mbar_wait(&full[k], static_cast<uint32_t>((i / S) & 1));
+    const NetMeta m = meta[k];
+    const float *su = reinterpret_cast<const float *>(smem_raw + k * stage_bytes);
+    const float *sv = su + nodes;
+    const uint32_t *sq = reinterpret_cast<const uint32_t *>(su + 2 * nodes);
+
+    int ci = -4, cj = -4;
+    if (m.fire) {  // uniform over the compute warps, rare: named barrier 1
+      const float lo = float(c.u_minus), hi = float(c.u_plus);
+      auto inside = [&](float u) { return u > lo && u < hi; };
+      for (int base = 0; base < nodes; base += kCompute) {
+        const int n = base + tid;
+        bool in_region = false;
+        if (n < nodes) {
+          const int rr = n / J, cc = n - rr * J;
+          in_region = inside(su[n]) || (rr > 0 && inside(su[n - J])) ||
+                      (rr < J - 1 && inside(su[n + J])) || (cc > 0 && inside(su[n - 1])) ||
+                      (cc < J - 1 && inside(su[n + 1]));
+        }
+        const uint32_t bits = __ballot_sync(0xffffffffu, in_region);
+        if (lane == 0 && (base >> 5) + warp < words) s_mask[(base >> 5) + warp] = bits;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
+      if (warp == 0) {
+        int cnt = 0;
+        for (int w0 = 0; w0 < words; w0 += 32)
+          cnt += __reduce_add_sync(0xffffffffu,
+                                   __popc(w0 + lane < words ? s_mask[w0 + lane] : 0u));
+        int found = -1;
+        if (cnt > 0) {
+          const int rank = static_cast<int>(__dmul_rn(m.sel, static_cast<double>(cnt)));
+          int before = 0;
+          for (int w0 = 0; w0 < words; w0 += 32) {
+            const uint32_t mw = w0 + lane < words ? s_mask[w0 + lane] : 0u;
+            const int pc = __popc(mw);
+            int incl = pc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int v = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += v;
+            }
+            if (pc > 0 && before + incl - pc <= rank && rank < before + incl) {
+              uint32_t mm = mw;
+              for (int q = rank - (before + incl - pc); q > 0; --q) mm &= mm - 1;
+              found = (w0 + lane) * 32 + (__ffs(mm) - 1);
+            }
+            before += __shfl_sync(0xffffffffu, incl, 31);
+          }
+          found = __reduce_max_sync(0xffffffffu, found);
+        }
+        if (lane == 0) s_cell = found;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kCompute) : "memory");
+      const int cell = s_cell;  // rewritten only after another bar.sync 1
+      if (cell >= 0) {
+        ci = cell / J;
+        cj = cell - ci * J;
+      }
+    }
+
+    double part = 0.0;
+    if (active) {
+      const float4 u4 = *reinterpret_cast<const float4 *>(su + n0);
+      const float4 v4 = *reinterpret_cast<const float4 *>(sv + n0);
+      const uint4 q4 = *reinterpret_cast<const uint4 *>(sq + n0);
+      const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 up = has_up ? *reinterpret_cast<const float4 *>(su + n0 - J) : zero4;
+      const float4 dn = has_dn ? *reinterpret_cast<const float4 *>(su + n0 + J) : zero4;
+      const float left = has_l ? su[n0 - 1] : 0.f;
+      const float right = has_r ? su[n0 + 4] : 0.f;
+      const uint4 rr = philox10(make_uint4(m.j, t, static_cast<uint32_t>(g), kPurposeNetNoise),
+                                Key2{m.k0, m.k1});
+      const float2 za = box_muller_fast_unscaled(rr.x, rr.y);
+      const float2 zb = box_muller_fast_unscaled(rr.z, rr.w);
+      const float uu[6] = {left, u4.x, u4.y, u4.z, u4.w, right};
+      const float upv[4] = {up.x, up.y, up.z, up.w}, dnv[4] = {dn.x, dn.y, dn.z, dn.w};
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+      const float z[4] = {za.x, za.y, zb.x, zb.y};
+      const uint32_t qq[4] = {q4.x, q4.y, q4.z, q4.w};
+      float un[4], vn[4];
+      uint32_t qn[4];
+      float big = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int cc = c0 + e;
+        const float u = uu[e + 1];
+        // reference neighbour order up, down, left, right; a missing
+        // neighbour contributes an exact +0 (x + 0 == x)
+        const float nb = A::add(A::add(A::add(upv[e], dnv[e]), uu[e]), uu[e + 2]);
+        const bool qnew = (r == ci && (cc == cj || cc == cj - 1 || cc == cj + 1)) ||
+                          (cc == cj && (r == ci - 1 || r == ci + 1));
+        const float psi = (qnew || (qq[e] & c.recent_mask)) ? famp : 0.0f;
+        const float drive = A::add(drv[e], psi);
+        const float p3 =
+            A::add(A::mul(A::add(A::mul(A::add(A::mul(fa3, u), fa2), u), fa1), u), fa0);
+        const float t1 = A::add(u, A::mul(dt, A::sub(p3, vv[e])));
+        const float t2 = A::add(t1, A::mul(dt, A::add(A::mul(fcpl, nb), drive)));
+        un[e] = A::add(t2, A::mul(fsig, z[e]));
+        vn[e] = A::add(vv[e], A::mul(dt, A::add(A::add(A::mul(fb0, u), A::mul(fb1, vv[e])), fb2)));
+        big = fmaxf(big, fmaxf(fabsf(un[e]), fabsf(vn[e])));
+        qn[e] = ((qq[e] << 1) | (qnew ? 1u : 0u)) & c.hist_mask;
+      }
+      float *xd = xout + m.p * 2 * static_cast<int64_t>(nodes);
+      uint32_t *qd = qout + m.p * static_cast<int64_t>(nodes);
+      *reinterpret_cast<float4 *>(xd + n0) = make_float4(un[0], un[1], un[2], un[3]);
+      *reinterpret_cast<float4 *>(xd + nodes + n0) = make_float4(vn[0], vn[1], vn[2], vn[3]);
+      *reinterpret_cast<uint4 *>(qd + n0) = make_uint4(qn[0], qn[1], qn[2], qn[3]);
+      // fmaxf drops NaN operands, so test the values themselves too
+      if (!(big <= 3.402823466e38f) || un[0] != un[0] || un[1] != un[1] || un[2] != un[2] ||
+          un[3] != un[3] || vn[0] != vn[0] || vn[1] != vn[1] || vn[2] != vn[2] ||
+          vn[3] != vn[3])
+        atomicOr(status + m.f, PF_ST_DIVERGED);
+      if (obits) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (obits & (1u << e)) {
+            const double d = s_y[n0 + e] - static_cast<double>(un[e]);
+            part = fma(d, d, part);
+          }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if (lane == 0) {
+      mbar_arrive(&empty[k]);  // this warp is done with stage k
+      if (logw) {
+        s_part[k][warp] = part;
+        __threadfence_block();
+        if (atomicAdd(&s_cnt[k], 1) == CW - 1) {  // last warp: combine in warp order
+          __threadfence_block();
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < CW; ++w) sum += s_part[k][w];
+          logw[m.p] = static_cast<float>(c.obs_coef * sum);
+          s_cnt[k] = 0;
+        }
+      }
+    }
+  }
+}
+
+template <int CW, int S>
+static int launch_net_fast(const NetConsts &c, const void *x_in, const uint32_t *q_in,
+                           const int32_t *anc, void *x_out, uint32_t *q_out, const double *fmask,
+                           const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
+                           int32_t N, const uint32_t *keys, uint32_t t, uint32_t *status,
+                           cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(S) * c.nodes * 12 + static_cast<size_t>(c.nodes) * 8 +
+                      static_cast<size_t>((c.nodes + 31) / 32) * 4;
+  auto kern = fhnnet_fast_kernel<CW, S>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (CW + 1) * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  int sms = kSmCount, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(MN, static_cast<int64_t>(sms) * per_sm);
+  kern<<<static_cast<unsigned>(grid), (CW + 1) * 32, smem, s>>>(
+      static_cast<const float *>(x_in), q_in, anc, static_cast<float *>(x_out), q_out, fmask, y,
+      obs_idx, static_cast<float *>(logw), MN, N, c, keys, t, status);
+  return check_launch("pf_fhnnet_step(fast)");
+}
+
+static int net_fast_warps(const NetConsts &c) {
+  const int groups = c.nodes / 4;
+  return groups <= 32 ? 1 : groups <= 64 ? 2 : groups <= 128 ? 4 : groups <= 256 ? 8 : 0;
+}
+
+// The bulk-copy kernel serves fp32 Philox steps on lattices with J % 4 == 0
+// and J <= 32 (one 4-node group per compute thread).
+// PF_FHNNET_KERNEL=generic forces the generic kernel (comparison tests).
+static bool net_fast_ok(const NetConsts &c, pf_dtype dtype, bool tape) {
+  if (dtype != PF_F32 || tape || !c.stochastic || c.J % 4 != 0 || net_fast_warps(c) == 0)
+    return false;
+  const char *env = std::getenv("PF_FHNNET_KERNEL");
+  return !(env && std::strcmp(env, "generic") == 0);
+}
+
 // Zone log-likelihood of stored rows (fhn.py:199-207), one warp per row:
 // out[r] = -0.5/obs_var * sum_i (y[i] - x[r*stride + idx[i]])^2 in the
 // reference's order (np_rows_sum).
@@ -497,6 +792,18 @@ int pf_fhnnet_step(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
   const int64_t MN = M * N;
   const int32_t n32 = static_cast<int32_t>(N);
   const bool tape = p->stochastic && stim_tape;
+  if (net_fast_ok(c, dtype, tape)) {
+#define PF_NET_FAST(CW)                                                                      \
+  return launch_net_fast<CW, 3>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y, obs_idx, \
+                                logw_out, MN, n32, keys, t, status, s)
+    switch (net_fast_warps(c)) {
+      case 1: PF_NET_FAST(1);
+      case 2: PF_NET_FAST(2);
+      case 4: PF_NET_FAST(4);
+      default: PF_NET_FAST(8);
+    }
+#undef PF_NET_FAST
+  }
   if (dtype == PF_F64)
     return tape ? dispatch_vec<double, 1>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y,
                                           obs_idx, logw_out, MN, n32, keys, t, stim_tape, z_tape,

@@ -249,3 +249,53 @@ def test_production_is_deterministic_and_tracks(golden):
     assert np.array_equal(a.mean_estimates, b.mean_estimates)
     mse = float(np.mean((a.mean_estimates - truth_u) ** 2))
     assert mse < 0.5 * float(np.mean((truth_u - truth_u.mean()) ** 2))
+
+
+@pytest.mark.parametrize("J", [8, 32])
+def test_fast_kernel_matches_generic(golden, monkeypatch, J):
+    """The bulk-copy fp32 kernel and the generic kernel run the same
+    Philox draws and arithmetic order: states within fp32 rounding of each
+    other, identical stimulus decisions (history bits)."""
+    g = golden["fhnnet"]
+    gm = pf.FhnNetworkModel(J=J, n_zones=2, zone_width=2, stim_prob=0.5)
+    M, N = 3, 40
+    if J == 8:
+        x0 = np.tile(g["sim8_states"][80], (M * N, 1))
+        y = g["sim8_obs"][80]
+    else:
+        rng = np.random.default_rng(4)
+        x0 = np.zeros((M * N, gm.dim_x))
+        x0[:, : gm.nodes] = rng.uniform(-2.0, 2.0, size=(M * N, gm.nodes))
+        x0[:, gm.nodes: 2 * gm.nodes] = rng.normal(size=(M * N, gm.nodes))
+        x0[:, 2 * gm.nodes:] = rng.random((M * N, gm.stim_hold * gm.nodes)) < 0.02
+        y = rng.normal(size=gm.dim_y)
+    keys = torch.from_numpy(pf.philox.filter_keys(5, M).view(np.int32)).cuda()
+    anc = torch.from_numpy(np.random.default_rng(1).integers(0, M * N, M * N)
+                           .astype(np.int32)).cuda()
+    dy = torch.from_numpy(np.asarray(y, dtype=np.float64).copy()).cuda()
+    idx = torch.from_numpy(gm.obs_indices.astype(np.int32)).cuda()
+    mask = gm.device_mask()
+    outs = []
+    for kernel in ("fast", "generic"):
+        if kernel == "generic":
+            monkeypatch.setenv("PF_FHNNET_KERNEL", "generic")
+        x, q = gm.to_device(x0, dtype=torch.float32)
+        xo, qo = torch.empty_like(x), torch.empty_like(q)
+        lw = torch.empty(M * N, dtype=torch.float32, device="cuda")
+        st = torch.zeros(M, dtype=torch.int32, device="cuda")
+        for t in (81, 5000):  # forcing on / off
+            pf._lib.call("pf_fhnnet_step", gm.params(), pf._lib.PF_F32, pf._lib.ptr(x),
+                         pf._lib.ptr(q), pf._lib.ptr(anc), pf._lib.ptr(xo), pf._lib.ptr(qo),
+                         pf._lib.ptr(mask), pf._lib.ptr(dy), pf._lib.ptr(idx), pf._lib.ptr(lw),
+                         M, N, pf._lib.ptr(keys), t, None, None, pf._lib.ptr(st),
+                         pf._lib.stream_ptr())
+            torch.cuda.synchronize()
+            outs.append((gm.from_device(xo, qo), lw.cpu().numpy().copy(), st.cpu().numpy()))
+    for a, b in zip(outs[:2], outs[2:]):
+        K = gm.nodes
+        assert norm_rel(a[0][:, : 2 * K], b[0][:, : 2 * K]) < 1e-6
+        assert np.array_equal(a[0][:, 2 * K:], b[0][:, 2 * K:])
+        assert norm_rel(a[1], b[1]) < 1e-6
+        assert np.array_equal(a[2], b[2])
+    # stimuli actually fired somewhere in the fast run
+    assert outs[0][0][:, 2 * gm.nodes: 3 * gm.nodes].sum() > 0
