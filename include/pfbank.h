@@ -103,6 +103,25 @@ typedef struct pf_fhnnet_params {
   double obs_var;
 } pf_fhnnet_params;
 
+/* Finite-state HMM (models/hmm.py:19-77).  Device tables: cum_prior (K),
+ * cum_rows (K*K, row-wise cumsum of the transition matrix), log_emission
+ * (K*S) = log(emission).  States are stored as floating-point indices. */
+typedef struct pf_hmm_params {
+  int32_t K, S;
+  const double *cum_prior, *cum_rows, *log_emission; /* device */
+} pf_hmm_params;
+
+/* Linear-Gaussian model (models/linear_gaussian.py:18-95), dim_x, dim_y <= 8.
+ * Device row-major matrices: A (dx*dx), chol_q (dx*dx), H (dy*dx),
+ * obs_prec (dy*dy), prior_mean (dx), chol_p0 (dx*dx). */
+typedef struct pf_lgm_params {
+  int32_t dx, dy;
+  int32_t noise_free; /* transition_point_prediction (linear_gaussian.py:74-75) */
+  int32_t reserved;
+  const double *A, *chol_q, *H, *obs_prec, *prior_mean, *chol_p0; /* device */
+  double obs_logconst; /* -0.5 (dy log 2pi + log det obs_cov) */
+} pf_lgm_params;
+
 /* ---- library ------------------------------------------------------- */
 const char *pf_last_error(void);
 int pf_version(void);
@@ -249,6 +268,29 @@ int pf_zone_loglik(pf_dtype dtype, const void *x, int64_t n, int64_t row_stride,
 int pf_bits_estimate(const uint32_t *q, int32_t nodes, int32_t nbits, const int32_t *anc,
                      int64_t M, int64_t N, double *est, int64_t est_stride, void *stream);
 
+/* ---- small-state verification models (models/hmm.py, linear_gaussian.py) */
+/* State planes x[d*M*N + p].  HMM draws: one uniform per particle and step
+ * (u_tape (M,N) fp64 in oracle mode); LGM draws: dim_x normals (z_tape
+ * (M,N,dx) fp64).  logw_out NULL skips the weights. */
+int pf_hmm_prior(const pf_hmm_params *h, pf_dtype dtype, void *x, int64_t M, int64_t N,
+                 const uint32_t *keys, const double *u_tape, void *stream);
+int pf_hmm_propagate_weight(const pf_hmm_params *h, pf_dtype dtype, const void *x_in,
+                            const int32_t *anc, void *x_out, const double *y, void *logw_out,
+                            int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                            const double *u_tape, uint32_t *status, void *stream);
+int pf_lgm_prior(const pf_lgm_params *g, pf_dtype dtype, void *x, int64_t M, int64_t N,
+                 const uint32_t *keys, const double *z_tape, void *stream);
+int pf_lgm_propagate_weight(const pf_lgm_params *g, pf_dtype dtype, const void *x_in,
+                            const int32_t *anc, void *x_out, const double *y, void *logw_out,
+                            int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                            const double *z_tape, uint32_t *status, void *stream);
+/* DiscreteHmm.log_likelihood of n stored fp64 states: log_emission[x[r], y[0]]. */
+int pf_hmm_loglik(const pf_hmm_params *h, const double *x, int64_t n, const double *y,
+                  double *out, void *stream);
+/* LinearGaussianModel.log_likelihood of n stored fp64 states (planes x[d*n + r]). */
+int pf_lgm_loglik(const pf_lgm_params *g, const double *x, int64_t n, const double *y,
+                  double *out, void *stream);
+
 /* ---- native bank driver ------------------------------------------------ */
 /* Production-mode (Philox) bootstrap bank: runs observations k0..k0+n-1 back
  * to back (propagate+weight, segmented resample, estimate, lnc/collapse trace
@@ -260,6 +302,8 @@ int pf_bits_estimate(const uint32_t *q, int32_t nodes, int32_t nbits, const int3
 #define PF_MODEL_LORENZ 0
 #define PF_MODEL_FHN 1
 #define PF_MODEL_FHNNET 2
+#define PF_MODEL_HMM 3
+#define PF_MODEL_LGM 4
 typedef struct pf_bank_desc {
   int32_t model; /* PF_MODEL_* */
   pf_dtype dtype;
@@ -291,6 +335,8 @@ typedef struct pf_bank_desc {
   const double *forcing_mask;     /* (J*J) */
   int64_t est_stride_f; /* distance between filters' estimate rows (0 = est_dim) */
   int32_t est_bits;     /* > 0: history bit means written after the est_dim state means */
+  const pf_hmm_params *hmm; /* host */
+  const pf_lgm_params *lgm; /* host */
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);

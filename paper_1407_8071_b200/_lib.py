@@ -53,6 +53,17 @@ class FhnNetParams(ctypes.Structure):
                 ("sig_sqdt", c_f64), ("obs_var", c_f64)]
 
 
+class HmmParams(ctypes.Structure):
+    _fields_ = [("K", c_i32), ("S", c_i32), ("cum_prior", c_vp), ("cum_rows", c_vp),
+                ("log_emission", c_vp)]
+
+
+class LgmParams(ctypes.Structure):
+    _fields_ = [("dx", c_i32), ("dy", c_i32), ("noise_free", c_i32), ("reserved", c_i32),
+                ("A", c_vp), ("chol_q", c_vp), ("H", c_vp), ("obs_prec", c_vp),
+                ("prior_mean", c_vp), ("chol_p0", c_vp), ("obs_logconst", c_f64)]
+
+
 class BankDesc(ctypes.Structure):
     _fields_ = [("model", c_i32), ("dtype", ctypes.c_int), ("M", c_i64), ("N", c_i64),
                 ("lorenz", ctypes.POINTER(LorenzParams)), ("fhn", ctypes.POINTER(FhnParams)),
@@ -63,12 +74,15 @@ class BankDesc(ctypes.Structure):
                 ("est_stride_d", c_i64), ("est_dim", c_i32), ("lnc_trace", c_vp),
                 ("collapsed_trace", c_vp), ("prop_ms", ctypes.POINTER(ctypes.c_float)),
                 ("fhnnet", ctypes.POINTER(FhnNetParams)), ("q", c_vp * 2),
-                ("forcing_mask", c_vp), ("est_stride_f", c_i64), ("est_bits", c_i32)]
+                ("forcing_mask", c_vp), ("est_stride_f", c_i64), ("est_bits", c_i32),
+                ("hmm", ctypes.POINTER(HmmParams)), ("lgm", ctypes.POINTER(LgmParams))]
 
 
 PF_MODEL_LORENZ = 0
 PF_MODEL_FHN = 1
 PF_MODEL_FHNNET = 2
+PF_MODEL_HMM = 3
+PF_MODEL_LGM = 4
 
 # name -> (restype, argtypes); must match include/pfbank.h exactly
 SIGNATURES = {
@@ -113,6 +127,18 @@ SIGNATURES = {
                                       c_vp, c_vp]),
     "pf_bits_estimate": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp, c_i64, c_i64, c_vp, c_i64,
                                         c_vp]),
+    "pf_hmm_prior": (ctypes.c_int, [ctypes.POINTER(HmmParams), ctypes.c_int, c_vp, c_i64, c_i64,
+                                    c_vp, c_vp, c_vp]),
+    "pf_hmm_propagate_weight": (ctypes.c_int, [ctypes.POINTER(HmmParams), ctypes.c_int, c_vp,
+                                               c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_u32,
+                                               c_vp, c_vp, c_vp]),
+    "pf_hmm_loglik": (ctypes.c_int, [ctypes.POINTER(HmmParams), c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "pf_lgm_prior": (ctypes.c_int, [ctypes.POINTER(LgmParams), ctypes.c_int, c_vp, c_i64, c_i64,
+                                    c_vp, c_vp, c_vp]),
+    "pf_lgm_propagate_weight": (ctypes.c_int, [ctypes.POINTER(LgmParams), ctypes.c_int, c_vp,
+                                               c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_u32,
+                                               c_vp, c_vp, c_vp]),
+    "pf_lgm_loglik": (ctypes.c_int, [ctypes.POINTER(LgmParams), c_vp, c_i64, c_vp, c_vp, c_vp]),
     "pf_bank_run": (ctypes.c_int, [ctypes.POINTER(BankDesc), c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pf_apf_first_stage_prepare": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "pf_compose_ancestors": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),

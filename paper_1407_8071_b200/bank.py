@@ -68,7 +68,7 @@ class FilterBank:
             raise ValueError("n_filters and n_particles must be >= 1")
         if n_filters * n_particles > 2**31 - 1:
             raise ValueError("M*N per GPU must fit int32 particle indices")
-        if model.kind not in ("lorenz", "fhn", "fhnnet"):
+        if model.kind not in ("lorenz", "fhn", "fhnnet", "hmm", "lgm"):
             raise ValueError(f"model kind {model.kind!r} has no GPU descriptor")
         if variant not in ("bootstrap", "auxiliary"):
             raise ValueError(f"unknown filter variant {variant!r}")
@@ -90,10 +90,11 @@ class FilterBank:
         self.est_width = estimate_width(model, estimate)
         self.est_bits = 0
         self.q = [None, None]
-        if model.kind == "lorenz":
-            self.x = [torch.empty((3, self.MN), dtype=self.dtype, **kw) for _ in range(2)]
+        if model.kind in ("lorenz", "hmm", "lgm"):  # state planes x[d][p]
+            self.x = [torch.empty((model.dim_x, self.MN), dtype=self.dtype, **kw)
+                      for _ in range(2)]
             self.params = model.params()
-            self.est_dim = 3
+            self.est_dim = model.dim_x
             self.est_strides = (1, self.MN)
         elif model.kind == "fhnnet":
             nodes = model.nodes
@@ -186,6 +187,16 @@ class FilterBank:
                 ztape = torch.from_numpy(z).to(self.device)
             _lib.call("pf_lorenz_prior", self.code, _lib.ptr(self.x[0]), self.M, self.N, mean_p,
                       m.prior_sd(), _lib.ptr(self.keys), _lib.ptr(ztape), s)
+        elif m.kind in ("hmm", "lgm"):
+            ztape = None
+            if self.tape is not None:
+                if self.tape.prior is None:
+                    raise ValueError("tape has no prior draws")
+                z = np.ascontiguousarray(self.tape.prior[self._rows()], dtype=np.float64)
+                ztape = torch.from_numpy(z).to(self.device)
+            fn = "pf_hmm_prior" if m.kind == "hmm" else "pf_lgm_prior"
+            _lib.call(fn, self.params, self.code, _lib.ptr(self.x[0]), self.M, self.N,
+                      _lib.ptr(self.keys), _lib.ptr(ztape), s)
         elif m.kind == "fhnnet":
             self.x[0].zero_()  # quiescent prior, no history (fhn.py:144-147)
             self.q[0].zero_()
@@ -208,6 +219,12 @@ class FilterBank:
                       _lib.ptr(anc), _lib.ptr(xout), _lib.ptr(qout), _lib.ptr(self.fmask),
                       y_ptr, _lib.ptr(self.obs_idx), _lib.ptr(logw), self.M, self.N,
                       _lib.ptr(self.keys), t, _lib.ptr(stim), _lib.ptr(z),
+                      _lib.ptr(self.status), s)
+        elif self.model.kind in ("hmm", "lgm"):
+            fn = "pf_hmm_propagate_weight" if self.model.kind == "hmm" else \
+                "pf_lgm_propagate_weight"
+            _lib.call(fn, params, self.code, _lib.ptr(xin), _lib.ptr(anc), _lib.ptr(xout), y_ptr,
+                      _lib.ptr(logw), self.M, self.N, _lib.ptr(self.keys), t, _lib.ptr(noise),
                       _lib.ptr(self.status), s)
         elif self.model.kind == "lorenz":
             _lib.call("pf_lorenz_propagate_weight", params, self.code, _lib.ptr(xin),
@@ -240,11 +257,16 @@ class FilterBank:
 
         d = _lib.BankDesc()
         d.model = {"lorenz": _lib.PF_MODEL_LORENZ, "fhn": _lib.PF_MODEL_FHN,
-                   "fhnnet": _lib.PF_MODEL_FHNNET}[self.model.kind]
+                   "fhnnet": _lib.PF_MODEL_FHNNET, "hmm": _lib.PF_MODEL_HMM,
+                   "lgm": _lib.PF_MODEL_LGM}[self.model.kind]
         d.dtype = self.code
         d.M, d.N = self.M, self.N
         if self.model.kind == "lorenz":
             d.lorenz = ctypes.pointer(self.params)
+        elif self.model.kind == "hmm":
+            d.hmm = ctypes.pointer(self.params)
+        elif self.model.kind == "lgm":
+            d.lgm = ctypes.pointer(self.params)
         elif self.model.kind == "fhnnet":
             d.fhnnet = ctypes.pointer(self.params)
             d.obs_idx = self.obs_idx.data_ptr()
@@ -386,7 +408,7 @@ class FilterBank:
             anc = self.anc if self.steps_done > 0 else None
             return self.model.from_device(x, self.q[self.cur], anc).reshape(self.M, self.N, -1)
         anc = self.anc.long() if self.steps_done > 0 else torch.arange(self.MN, device=x.device)
-        if self.model.kind == "lorenz":
+        if self.model.kind in ("lorenz", "hmm", "lgm"):
             g = x[:, anc].t()
         else:
             g = x[anc]

@@ -33,8 +33,10 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                  ? d->lorenz != nullptr
                  : d->model == PF_MODEL_FHN
                        ? (d->fhn && d->obs_idx)
-                       : (d->model == PF_MODEL_FHNNET && d->fhnnet && d->obs_idx && d->q[0] &&
-                          d->q[1] && d->forcing_mask),
+                       : d->model == PF_MODEL_FHNNET
+                             ? (d->fhnnet && d->obs_idx && d->q[0] && d->q[1] && d->forcing_mask)
+                             : d->model == PF_MODEL_HMM ? d->hmm != nullptr
+                                                        : (d->model == PF_MODEL_LGM && d->lgm),
              "pf_bank_run: model descriptor missing");
   PF_REQUIRE(d->x[0] && d->x[1] && d->logw && d->anc && d->lnc && d->collapsed && d->status &&
                  d->keys && d->obs && d->est,
@@ -66,6 +68,12 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     if (d->model == PF_MODEL_LORENZ)
       rc = pf_lorenz_propagate_weight(d->lorenz, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
                                       d->keys, t, nullptr, d->status, stream);
+    else if (d->model == PF_MODEL_HMM)
+      rc = pf_hmm_propagate_weight(d->hmm, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
+                                   d->keys, t, nullptr, d->status, stream);
+    else if (d->model == PF_MODEL_LGM)
+      rc = pf_lgm_propagate_weight(d->lgm, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
+                                   d->keys, t, nullptr, d->status, stream);
     else if (d->model == PF_MODEL_FHNNET)
       rc = pf_fhnnet_step(d->fhnnet, d->dtype, xin, d->q[cur], anc, xout, d->q[cur ^ 1],
                           d->forcing_mask, y, d->obs_idx, d->logw, d->M, d->N, d->keys, t,

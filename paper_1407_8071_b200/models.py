@@ -44,8 +44,8 @@ def estimate_width(model, estimate: str) -> int:
     projection (the voltage block of the lattice models)."""
     if estimate not in ("full", "projection"):
         raise ValueError("estimate must be 'full' or 'projection'")
-    if model.kind == "lorenz":
-        return 3
+    if model.kind in ("lorenz", "hmm", "lgm"):
+        return model.dim_x
     return model.dim_x if estimate == "full" else model.nodes
 
 
@@ -502,3 +502,276 @@ def simulate(model, n_steps: int, seed):
     from .simulate import simulate as _simulate
 
     return _simulate(model, n_steps, seed)
+
+
+# ---------------------------------------------------------------------------
+# Verification oracles: finite-state HMM and linear-Gaussian model
+# ---------------------------------------------------------------------------
+
+
+class _DeviceTables:
+    """Per-device fp64 copies of a model's constant tables (not pickled)."""
+
+    def _tables(self):
+        torch = _torch()
+        dev = torch.cuda.current_device()
+        cache = self.__dict__.setdefault("_dev_cache", {})
+        if dev not in cache:
+            cache[dev] = {k: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).cuda()
+                          for k, v in self._host_tables().items()}
+        return cache[dev]
+
+    def __getstate__(self):
+        d = dict(self.__dict__)
+        d.pop("_dev_cache", None)
+        return d
+
+
+@dataclass
+class DiscreteHmm(_DeviceTables, StateSpaceModel):
+    """Drop-in for parpf.models.DiscreteHmm (hmm.py:19-77): prior (K,),
+    row-stochastic transition (K, K), strictly positive emission (K, S).
+    States are carried as (n, 1) float arrays."""
+
+    prior: np.ndarray
+    transition: np.ndarray
+    emission: np.ndarray
+
+    kind = "hmm"
+
+    def __post_init__(self):
+        self.prior = np.asarray(self.prior, dtype=np.float64)
+        self.transition = np.asarray(self.transition, dtype=np.float64)
+        self.emission = np.asarray(self.emission, dtype=np.float64)
+        k = self.prior.shape[0]
+        if self.transition.shape != (k, k):
+            raise ValueError("transition matrix shape mismatch")
+        if not np.allclose(self.transition.sum(axis=1), 1.0, atol=1e-12):
+            raise ValueError("transition rows must sum to 1")
+        if not np.isclose(self.prior.sum(), 1.0, atol=1e-12):
+            raise ValueError("prior must sum to 1")
+        if self.emission.shape[0] != k:
+            raise ValueError("emission table must have one row per state")
+        if np.any(self.emission <= 0.0):
+            raise ValueError("emission probabilities must be strictly positive")
+        self.dim_x = 1
+        self.dim_y = 1
+        self._cum_rows = np.cumsum(self.transition, axis=1)
+        self._cum_prior = np.cumsum(self.prior)
+
+    @property
+    def n_states(self) -> int:
+        return self.prior.shape[0]
+
+    def _host_tables(self):
+        return {"cum_prior": self._cum_prior, "cum_rows": self._cum_rows,
+                "log_emission": np.log(self.emission)}
+
+    def params(self, n_sub=None, noise_free=False) -> _lib.HmmParams:
+        tb = self._tables()
+        return _lib.HmmParams(self.n_states, self.emission.shape[1], tb["cum_prior"].data_ptr(),
+                              tb["cum_rows"].data_ptr(), tb["log_emission"].data_ptr())
+
+    def sample_prior(self, rng, n):
+        torch = _torch()
+        u = torch.from_numpy(rng.random(n)).cuda()
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.call("pf_hmm_prior", self.params(), _lib.PF_F64, _lib.ptr(x), 1, n, None,
+                  _lib.ptr(u), _lib.stream_ptr())
+        return x.cpu().numpy()[:, None]
+
+    def _step(self, x_prev, t, u, y=None):
+        torch = _torch()
+        x_prev = np.atleast_2d(np.asarray(x_prev, dtype=np.float64))
+        n = x_prev.shape[0]
+        xin = torch.from_numpy(np.ascontiguousarray(x_prev[:, 0])).cuda()
+        xout = torch.empty_like(xin)
+        d_u = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).cuda()
+        lw = d_y = None
+        if y is not None:
+            lw = torch.empty(n, dtype=torch.float64, device="cuda")
+            d_y = torch.tensor([float(np.asarray(y).reshape(-1)[0])], dtype=torch.float64,
+                               device="cuda")
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("pf_hmm_propagate_weight", self.params(), _lib.PF_F64, _lib.ptr(xin), None,
+                  _lib.ptr(xout), _lib.ptr(d_y), _lib.ptr(lw), 1, n, None, int(t),
+                  _lib.ptr(d_u), _lib.ptr(st), _lib.stream_ptr())
+        return xout.cpu().numpy()[:, None], (None if lw is None else lw.cpu().numpy())
+
+    def sample_transition(self, x_prev, t, rng):
+        x_prev = np.atleast_2d(np.asarray(x_prev, dtype=np.float64))
+        return self._step(x_prev, t, rng.random(x_prev.shape[0]))[0]
+
+    def log_likelihood(self, y, x, t):
+        """log(emission[state, y]) (hmm.py:70-72), looked up on the device."""
+        torch = _torch()
+        x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+        d_x = torch.from_numpy(np.ascontiguousarray(x[:, 0])).cuda()
+        d_y = torch.tensor([float(np.asarray(y).reshape(-1)[0])], dtype=torch.float64,
+                           device="cuda")
+        out = torch.empty(x.shape[0], dtype=torch.float64, device="cuda")
+        _lib.call("pf_hmm_loglik", self.params(), _lib.ptr(d_x), x.shape[0], _lib.ptr(d_y),
+                  _lib.ptr(out), _lib.stream_ptr())
+        return out.cpu().numpy()
+
+    def sample_observation(self, x, t, rng):
+        state = int(np.asarray(x).reshape(-1)[0])
+        u = rng.random()
+        sym = np.searchsorted(np.cumsum(self.emission[state]), u, side="right")
+        return np.array([float(min(sym, self.emission.shape[1] - 1))])
+
+
+def hmm_exact_filter(model: DiscreteHmm, observations) -> list[tuple[np.ndarray, float]]:
+    """Exact forward recursion (hmm.py:80-97): per step (filter vector,
+    unnormalised mass), accumulated in extended precision.  Host oracle for
+    the verification checks."""
+    obs = [int(np.asarray(y).reshape(-1)[0]) for y in observations]
+    rho = model.prior.astype(np.longdouble)
+    trans = model.transition.astype(np.longdouble)
+    emit = model.emission.astype(np.longdouble)
+    out = []
+    for y in obs:
+        rho = (trans.T @ rho) * emit[:, y]
+        mass = rho.sum()
+        out.append(((rho / mass).astype(np.float64), float(mass)))
+    return out
+
+
+@dataclass
+class LinearGaussianModel(_DeviceTables, StateSpaceModel):
+    """Drop-in for parpf.models.LinearGaussianModel (linear_gaussian.py:18-95):
+    x_t = A x_{t-1} + w, y_t = H x_t + v; the log-likelihood keeps its
+    normalising constant.  The GPU kernels support dim_x, dim_y <= 8."""
+
+    A: np.ndarray
+    trans_cov: np.ndarray
+    H: np.ndarray
+    obs_cov: np.ndarray
+    prior_mean: np.ndarray
+    prior_cov: np.ndarray
+
+    kind = "lgm"
+
+    def __post_init__(self):
+        m = lambda a: np.atleast_2d(np.asarray(a, dtype=np.float64))  # noqa: E731
+        self.A, self.trans_cov, self.H, self.obs_cov = (m(self.A), m(self.trans_cov), m(self.H),
+                                                        m(self.obs_cov))
+        self.prior_mean = np.atleast_1d(np.asarray(self.prior_mean, dtype=np.float64))
+        self.prior_cov = m(self.prior_cov)
+        self.dim_x = self.A.shape[0]
+        self.dim_y = self.H.shape[0]
+        if self.dim_x > 8 or self.dim_y > 8:
+            raise ValueError("the GPU linear-Gaussian kernels support dim_x, dim_y <= 8")
+        self._chol_q = np.linalg.cholesky(self.trans_cov)
+        self._chol_p0 = np.linalg.cholesky(self.prior_cov)
+        sign, logdet = np.linalg.slogdet(self.obs_cov)
+        if sign > 0:
+            self._chol_r = np.linalg.cholesky(self.obs_cov)
+            self._obs_prec = np.linalg.inv(self.obs_cov)
+            self._obs_logconst = -0.5 * (self.dim_y * np.log(2.0 * np.pi) + logdet)
+        else:
+            self._chol_r = None
+            self._obs_prec = None
+            self._obs_logconst = float("nan")
+
+    @classmethod
+    def scalar(cls, a: float = 1.0, q: float = 1.0, h: float = 1.0, r: float = 1.0,
+               prior_mean: float = 0.0, prior_var: float = 1.0) -> "LinearGaussianModel":
+        return cls(A=[[a]], trans_cov=[[q]], H=[[h]], obs_cov=[[r]],
+                   prior_mean=[prior_mean], prior_cov=[[prior_var]])
+
+    def _host_tables(self):
+        t = {"A": self.A, "chol_q": self._chol_q, "H": self.H, "prior_mean": self.prior_mean,
+             "chol_p0": self._chol_p0}
+        if self._obs_prec is not None:
+            t["obs_prec"] = self._obs_prec
+        return t
+
+    def params(self, n_sub=None, noise_free=False) -> _lib.LgmParams:
+        tb = self._tables()
+        p = _lib.LgmParams()
+        p.dx, p.dy, p.noise_free = self.dim_x, self.dim_y, 1 if noise_free else 0
+        p.A, p.chol_q, p.H = tb["A"].data_ptr(), tb["chol_q"].data_ptr(), tb["H"].data_ptr()
+        p.obs_prec = tb["obs_prec"].data_ptr() if "obs_prec" in tb else None
+        p.prior_mean, p.chol_p0 = tb["prior_mean"].data_ptr(), tb["chol_p0"].data_ptr()
+        p.obs_logconst = float(self._obs_logconst)
+        return p
+
+    def _planes(self, x):
+        torch = _torch()
+        x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+        return torch.from_numpy(np.ascontiguousarray(x.T)).cuda(), x.shape[0]
+
+    def sample_prior(self, rng, n):
+        torch = _torch()
+        z = torch.from_numpy(np.ascontiguousarray(rng.standard_normal((n, self.dim_x)))).cuda()
+        x = torch.empty((self.dim_x, n), dtype=torch.float64, device="cuda")
+        _lib.call("pf_lgm_prior", self.params(), _lib.PF_F64, _lib.ptr(x), 1, n, None,
+                  _lib.ptr(z), _lib.stream_ptr())
+        return x.t().contiguous().cpu().numpy()
+
+    def _advance(self, x_prev, z, noise_free):
+        torch = _torch()
+        xin, n = self._planes(x_prev)
+        xout = torch.empty_like(xin)
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        d_z = None if z is None else torch.from_numpy(np.ascontiguousarray(z)).cuda()
+        _lib.call("pf_lgm_propagate_weight", self.params(noise_free=noise_free), _lib.PF_F64,
+                  _lib.ptr(xin), None, _lib.ptr(xout), None, None, 1, n, None, 1,
+                  _lib.ptr(d_z), _lib.ptr(st), _lib.stream_ptr())
+        if int(st.item()) & _lib.PF_ST_DIVERGED:
+            raise NumericalDivergenceError("linear-Gaussian transition produced non-finite states")
+        return xout.t().contiguous().cpu().numpy()
+
+    def sample_transition(self, x_prev, t, rng):
+        x_prev = np.atleast_2d(np.asarray(x_prev, dtype=np.float64))
+        return self._advance(x_prev, rng.standard_normal(x_prev.shape), False)
+
+    def transition_point_prediction(self, x_prev, t):
+        return self._advance(x_prev, None, True)
+
+    def log_likelihood(self, y, x, t):
+        torch = _torch()
+        if self._obs_prec is None:
+            raise ValueError("obs_cov is singular; likelihood is undefined")
+        xin, n = self._planes(x)
+        d_y = torch.from_numpy(np.atleast_1d(np.asarray(y, dtype=np.float64)).copy()).cuda()
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        _lib.call("pf_lgm_loglik", self.params(), _lib.ptr(xin), n, _lib.ptr(d_y),
+                  _lib.ptr(out), _lib.stream_ptr())
+        return out.cpu().numpy()
+
+    def sample_observation(self, x, t, rng):
+        if self._chol_r is None:
+            return np.asarray(x) @ self.H.T
+        z = rng.standard_normal(self.dim_y)
+        return x @ self.H.T + z @ self._chol_r.T
+
+
+def kalman_filter(model: LinearGaussianModel, observations):
+    """Exact Kalman posteriors (linear_gaussian.py:98-125): the prior, then
+    one (mean, cov) per observation.  Host oracle for the verification
+    checks."""
+    observations = np.asarray(observations, dtype=np.float64)
+    if observations.size == 0:
+        observations = observations.reshape(0, model.dim_y)
+    observations = np.atleast_2d(observations)
+    if observations.ndim != 2 or observations.shape[1] != model.dim_y:
+        raise ValueError("observations must have shape (T, dim_y)")
+    mean = model.prior_mean.copy()
+    cov = model.prior_cov.copy()
+    out = [(mean.copy(), cov.copy())]
+    eye = np.eye(model.dim_x)
+    for y in observations:
+        mean = model.A @ mean
+        cov = model.A @ cov @ model.A.T + model.trans_cov
+        innov = y - model.H @ mean
+        s = model.H @ cov @ model.H.T + model.obs_cov
+        try:
+            gain = np.linalg.solve(s, model.H @ cov).T
+        except np.linalg.LinAlgError as exc:
+            raise NumericalDivergenceError(f"singular innovation covariance: {exc}") from exc
+        mean = mean + gain @ innov
+        cov = (eye - gain @ model.H) @ cov
+        out.append((mean.copy(), cov.copy()))
+    return out

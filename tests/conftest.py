@@ -19,4 +19,4 @@ def golden():
 
     base = os.path.join(REPO, "tests", "golden")
     return {name: np.load(os.path.join(base, name + ".npz"))
-            for name in ("kernels", "lorenz", "fhn", "fhnnet")}
+            for name in ("kernels", "lorenz", "fhn", "fhnnet", "small")}

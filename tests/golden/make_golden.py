@@ -353,12 +353,53 @@ def gen_fhnnet():
     np.savez_compressed(os.path.join(HERE, "fhnnet.npz"), **d)
 
 
+def gen_small():
+    """Verification oracle models (models/hmm.py, models/linear_gaussian.py)."""
+    from parpf.models import DiscreteHmm, LinearGaussianModel, hmm_exact_filter, kalman_filter
+    from parpf.models import simulate as ref_simulate
+
+    d = {}
+    hmm = DiscreteHmm(prior=[0.5, 0.5], transition=[[0.9, 0.1], [0.2, 0.8]],
+                      emission=[[0.8, 0.2], [0.3, 0.7]])
+    hobs = np.array([[0.0], [1.0], [0.0], [0.0], [1.0]])
+    out, calls = _filter_with_steps(hmm, hobs, 50, np.random.SeedSequence(7102))
+    d["h_est"], d["h_lnc"] = out.estimates, out.log_norm_const
+    d["h_anc"] = np.stack([c[1] for c in calls])
+    ens = parpf.run_ensemble(hmm, hobs, "bootstrap", 3, 20, 44)
+    d["he_mean"] = ens.mean_estimates
+    d["he_lnc"] = np.stack([fo.log_norm_const for fo in ens.filter_outputs])
+    ex = hmm_exact_filter(hmm, hobs)
+    d["h_exact_filter"] = np.stack([e[0] for e in ex])
+    d["h_exact_mass"] = np.array([e[1] for e in ex])
+    d["h_sim_states"], d["h_sim_obs"] = ref_simulate(hmm, 30, 5)
+    lg = LinearGaussianModel.scalar(a=0.9, q=1.0, h=1.0, r=1.0, prior_mean=0.0, prior_var=1.0)
+    st, ob = ref_simulate(lg, 10, 12)
+    d["l_sim_states"], d["l_obs"] = st, ob
+    out, calls = _filter_with_steps(lg, ob, 64, np.random.SeedSequence(7103))
+    d["l_est"], d["l_lnc"] = out.estimates, out.log_norm_const
+    d["l_anc"] = np.stack([c[1] for c in calls])
+    outa = parpf.run_filter(lg, ob, "auxiliary", 40, np.random.SeedSequence(71))
+    d["la_est"], d["la_lnc"] = outa.estimates, outa.log_norm_const
+    kf = kalman_filter(lg, ob)
+    d["l_kf_mean"] = np.stack([k[0] for k in kf])
+    d["l_kf_cov"] = np.stack([k[1] for k in kf])
+    lg2 = LinearGaussianModel(A=[[0.9, 0.1], [-0.2, 0.8]], trans_cov=[[1.0, 0.3], [0.3, 0.5]],
+                              H=[[1.0, 0.5]], obs_cov=[[0.7]], prior_mean=[0.5, -0.5],
+                              prior_cov=[[1.0, 0.2], [0.2, 2.0]])
+    st2, ob2 = ref_simulate(lg2, 8, 13)
+    d["l2_obs"] = ob2
+    out2 = parpf.run_filter(lg2, ob2, "bootstrap", 32, np.random.SeedSequence(5))
+    d["l2_est"], d["l2_lnc"] = out2.estimates, out2.log_norm_const
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **d)
+
+
 if __name__ == "__main__":
     print("reference backend:", accel.backend_name())
     gen_kernels()
     gen_lorenz()
     gen_fhn()
     gen_fhnnet()
+    gen_small()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
