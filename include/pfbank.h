@@ -291,6 +291,25 @@ int pf_hmm_loglik(const pf_hmm_params *h, const double *x, int64_t n, const doub
 int pf_lgm_loglik(const pf_lgm_params *g, const double *x, int64_t n, const double *y,
                   double *out, void *stream);
 
+/* ---- double bootstrap: islands = the bank's filters (filters.py:201-313) - */
+/* log_weights[m] += lnc[m] - lnc_old[m]  (dbf_step, filters.py:253-256). */
+int pf_island_accumulate(double *log_weights, const double *lnc, const double *lnc_old,
+                         int64_t M, void *stream);
+/* Whole-island resampling (filters.py:258-263): island m takes island
+ * idx[m]'s ancestors (so the next propagate gathers its particles), lnc and
+ * collapse flag; log_weights := 0.  idx comes from a 1-segment
+ * pf_segmented_resample_ex over the M island log-weights; *_tmp are
+ * caller-provided scratch of the same sizes. */
+int pf_island_copy(const int32_t *idx, int32_t *anc, double *lnc, uint8_t *collapsed,
+                   double *log_weights, int64_t M, int64_t N, int32_t *anc_tmp,
+                   double *lnc_tmp, uint8_t *coll_tmp, void *stream);
+/* pooled_estimate (filters.py:229-234): out[d] = sum_m p_m est[m*est_stride+d]
+ * with p = softmax(log_weights) in numpy order; M <= 4096. */
+int pf_island_pool(const double *est, int64_t est_stride, int64_t M, int64_t dim,
+                   const double *log_weights, double *out, void *stream);
+/* out[0] = max + log(sum exp(lnc - max)) - log(M)  (filters.py:301-303). */
+int pf_island_trace(const double *lnc, int64_t M, double *out, void *stream);
+
 /* ---- native bank driver ------------------------------------------------ */
 /* Production-mode (Philox) bootstrap bank: runs observations k0..k0+n-1 back
  * to back (propagate+weight, segmented resample, estimate, lnc/collapse trace

@@ -139,6 +139,11 @@ SIGNATURES = {
                                                c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_u32,
                                                c_vp, c_vp, c_vp]),
     "pf_lgm_loglik": (ctypes.c_int, [ctypes.POINTER(LgmParams), c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "pf_island_accumulate": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pf_island_copy": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
+                                      c_vp, c_vp]),
+    "pf_island_pool": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "pf_island_trace": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "pf_bank_run": (ctypes.c_int, [ctypes.POINTER(BankDesc), c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pf_apf_first_stage_prepare": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp]),
     "pf_compose_ancestors": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),

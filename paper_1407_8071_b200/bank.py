@@ -42,6 +42,7 @@ class DrawTape:
     uniforms: list = field(default_factory=list)
     uniforms_first: list = field(default_factory=list)  # auxiliary filter, first stage
     stim: list = field(default_factory=list)  # FH-N network stimulus uniforms
+    islands: dict = field(default_factory=dict)  # double bootstrap: t -> (1, M) uniforms
 
 
 def _torch_dtype(dtype):
@@ -137,6 +138,9 @@ class FilterBank:
         self.cur = 0
         self.steps_done = 0
         self.kernel_events = None  # optional (start, end) CUDA events around propagate
+        # optional callable(k, t) run after resampling, before the estimate
+        # (double bootstrap island selection, islands.py)
+        self.post_resample = None
         self._desc = None  # cached pf_bank_desc (buffers are fixed for the bank's lifetime)
         # oracle mode builds the CDF in the reference's exact order (bit-exact
         # ancestors); production mode uses the parallel scan
@@ -250,7 +254,7 @@ class FilterBank:
 
     def _native_ok(self):
         return (self.tape is None and self.variant == "bootstrap"
-                and self.kernel_events is None)
+                and self.kernel_events is None and self.post_resample is None)
 
     def _bank_desc(self):
         import ctypes
@@ -347,6 +351,8 @@ class FilterBank:
             if self.kernel_events is not None:
                 self.kernel_events[1].record()
             self._resample(self.logw, uni, t, self.anc)
+        if self.post_resample is not None:
+            self.post_resample(k, t)
         est_base = self.est[k].data_ptr() + self.est_row * self.est_width * 8
         sp, sd = self.est_strides
         _lib.call("pf_filter_estimate_strided", self.code, _lib.ptr(xout), sp, sd, self.est_dim,

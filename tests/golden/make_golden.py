@@ -268,6 +268,12 @@ def gen_lorenz():
     outac = parpf.run_filter(model, obs_c, "auxiliary", 16, 12)
     d["ac_est"], d["ac_lnc"] = outac.estimates, outac.log_norm_const
     d["ac_steps"] = np.array(outac.collapse_steps)
+    # double bootstrap (filters.py:201-313): 4 islands x 30, island period 5
+    from parpf.filters import run_double_bootstrap
+
+    db = run_double_bootstrap(model, obs[:12], 4, 30, 5, np.random.SeedSequence(99))
+    d["db_est"], d["db_lnc"] = db.estimates, db.log_norm_const
+    d["db_coll"] = np.array(db.collapse_steps, dtype=np.int64)
     # ground truth / observation generator (models/simulate.py:10-29), stock model
     from parpf.models import simulate as ref_simulate
 
@@ -390,6 +396,12 @@ def gen_small():
     d["l2_obs"] = ob2
     out2 = parpf.run_filter(lg2, ob2, "bootstrap", 32, np.random.SeedSequence(5))
     d["l2_est"], d["l2_lnc"] = out2.estimates, out2.log_norm_const
+    # double bootstrap (filters.py:201-313) on the HMM: island steps at t = 2, 4
+    from parpf.filters import run_double_bootstrap
+
+    db = run_double_bootstrap(hmm, hobs, 3, 20, 2, np.random.SeedSequence(606))
+    d["db_h_est"], d["db_h_lnc"] = db.estimates, db.log_norm_const
+    d["db_h_coll"] = np.array(db.collapse_steps, dtype=np.int64)
     np.savez_compressed(os.path.join(HERE, "small.npz"), **d)
 
 

@@ -126,3 +126,55 @@ def test_hmm_production_unbiased_normalising_constant():
     gvals = np.exp(bank.lnc_tr[-1].cpu().numpy())
     z = abs(gvals.mean() - mass) / (gvals.std(ddof=1) / np.sqrt(M))
     assert z < 4.0, (gvals.mean(), mass, z)
+
+
+def _island_tape(tr, n):
+    M = len(tr.island_traces)
+    prior = np.stack([it["prior"] for it in tr.island_traces])
+    T = len(tr.island_traces[0]["steps"])
+    noise = [np.stack([it["steps"][k].noise for it in tr.island_traces]) for k in range(T)]
+    uni = [np.stack([(it["steps"][k].u if it["steps"][k].u is not None else np.full(n, np.nan))
+                     for it in tr.island_traces]) for k in range(T)]
+    return pf.DrawTape(prior=prior, noise=noise, uniforms=uni,
+                       islands={t: u[None] for t, u, _ in tr.island_steps})
+
+
+def test_double_bootstrap_oracle_mode(golden):
+    from paper_1407_8071_b200 import islands
+
+    g = golden["small"]
+    om, gm = orc.DiscreteHmmModel(**HMM), models.DiscreteHmm(**HMM)
+    tr = orc.run_double_bootstrap(om, HOBS, 3, 20, 2, np.random.SeedSequence(606),
+                                  keep_steps=True)
+    out = islands.run_double_bootstrap(gm, HOBS, 3, 20, 2, np.random.SeedSequence(606),
+                                       tape=_island_tape(tr, 20))
+    assert norm_rel(out.estimates, g["db_h_est"]) < 1e-12
+    assert norm_rel(out.log_norm_const, g["db_h_lnc"]) < 1e-12
+    assert out.collapse_steps == g["db_h_coll"].tolist()
+    assert out.n_particles == 60 and out.variant == "double-bf"
+    gl = golden["lorenz"]
+    om = orc.LorenzConfigModel(prior_mean=tuple(gl["truth0"]))
+    gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(gl["truth0"]), prior_var=1.0)
+    tr = orc.run_double_bootstrap(om, gl["obs"][:12], 4, 30, 5, np.random.SeedSequence(99),
+                                  keep_steps=True)
+    out = islands.run_double_bootstrap(gm, gl["obs"][:12], 4, 30, 5, np.random.SeedSequence(99),
+                                       tape=_island_tape(tr, 30))
+    assert norm_rel(out.estimates, gl["db_est"]) < 1e-12
+    assert norm_rel(out.log_norm_const, gl["db_lnc"]) < 1e-12
+
+
+def test_double_bootstrap_production():
+    """Philox islands: deterministic; on the HMM the pooled estimate of the
+    final filter probability is unbiased within noise over replicates."""
+    from paper_1407_8071_b200 import islands
+
+    gm = models.DiscreteHmm(**HMM)
+    a = islands.run_double_bootstrap(gm, HOBS, 8, 64, 2, 5)
+    b = islands.run_double_bootstrap(gm, HOBS, 8, 64, 2, 5)
+    assert np.array_equal(a.estimates, b.estimates)
+    exact = models.hmm_exact_filter(gm, HOBS)[-1][0][1]
+    ests = np.array([islands.run_double_bootstrap(gm, HOBS, 8, 64, 2, s).estimates[-1, 0]
+                     for s in range(60)])
+    z = abs(ests.mean() - exact) / (ests.std(ddof=1) / np.sqrt(len(ests)))
+    assert z < 4.0

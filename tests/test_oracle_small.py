@@ -45,3 +45,19 @@ def test_lgm_2d_filter(golden):
     tr = orc.run_filter(m, g["l2_obs"], 32, np.random.SeedSequence(5))
     assert np.allclose(tr.estimates, g["l2_est"], rtol=1e-12, atol=1e-12)
     assert np.allclose(tr.log_norm_const, g["l2_lnc"], rtol=1e-12, atol=1e-12)
+
+
+def test_double_bootstrap_bit_exact(golden):
+    """filters.py:201-313 restated: island selection every period steps."""
+    g = golden["small"]
+    tr = orc.run_double_bootstrap(orc.DiscreteHmmModel(**HMM), HOBS, 3, 20, 2,
+                                  np.random.SeedSequence(606))
+    assert np.array_equal(tr.estimates, g["db_h_est"])
+    assert np.array_equal(tr.log_norm_const, g["db_h_lnc"])
+    assert tr.collapse_steps == g["db_h_coll"].tolist()
+    assert [s[0] for s in tr.island_steps] == [2, 4]
+    gl = golden["lorenz"]
+    m = orc.LorenzConfigModel(prior_mean=tuple(gl["truth0"]))
+    tr = orc.run_double_bootstrap(m, gl["obs"][:12], 4, 30, 5, np.random.SeedSequence(99))
+    assert np.array_equal(tr.estimates, gl["db_est"])
+    assert np.array_equal(tr.log_norm_const, gl["db_lnc"])
