@@ -350,7 +350,10 @@ def run_resample(args, cfg):
     achieved = MN * RESAMPLE_BYTES_PER_PARTICLE / per / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
-            "kernel": "pf_segmented_resample_ex (resample_bank_kernel with fused gather)",
+            "kernel": ("pf_segmented_resample_ex (resample_bank_kernel with fused gather)"
+                       if N <= 8192 else
+                       "pf_segmented_resample_ex (wide pipeline: tile stats, filter totals, "
+                       "tile CDF, partition, merge, fused gather)"),
             "algorithmic": f"{RESAMPLE_BYTES_PER_PARTICLE:.0f} B/particle x {MN} particles",
             "traffic": _ncu_traffic(args.config)}
     # e2e: host logw in (pinned), host ancestors out, through the C ABI
