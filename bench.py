@@ -486,7 +486,13 @@ def run_ours(args, cfg):
     e2e_obs = obs[: args.steps]
     # release the timed bank so the caching allocator can serve the e2e call
     del bank, est_full, exch
+    # one untimed call over the warm-up observations (first-use costs: lazy
+    # module loading of the e2e path, allocator growth), then the timed call
+    warm = pf.run_ensemble(model, obs[: max(args.warmup, 1)], "bootstrap", M, N, 7,
+                           dtype=cfg["dtype"], estimate="projection")
+    del warm
     torch.cuda.synchronize()
+    _barrier(world)
     t0 = time.perf_counter()
     out = pf.run_ensemble(model, e2e_obs, "bootstrap", M, N, 7, dtype=cfg["dtype"],
                           estimate="projection")
@@ -497,7 +503,8 @@ def run_ours(args, cfg):
            "h2d_bytes_per_step": int(model.dim_y * 8),
            "d2h_bytes_per_step": int(M * est_dim * 8 + M * 8 + M * 4),
            "api": "paper_1407_8071_b200.run_ensemble (host numpy observations -> "
-                  "EnsembleOutput), includes bank allocation + prior init"}
+                  "EnsembleOutput), includes bank allocation + prior init; after one "
+                  "untimed warm-up call"}
     del out
 
     line = None

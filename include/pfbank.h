@@ -356,6 +356,7 @@ typedef struct pf_bank_desc {
   int32_t est_bits;     /* > 0: history bit means written after the est_dim state means */
   const pf_hmm_params *hmm; /* host */
   const pf_lgm_params *lgm; /* host */
+  float *step_ms; /* host (n_steps) or NULL: whole-interval durations (waits like prop_ms) */
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);

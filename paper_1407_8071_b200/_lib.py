@@ -75,7 +75,8 @@ class BankDesc(ctypes.Structure):
                 ("collapsed_trace", c_vp), ("prop_ms", ctypes.POINTER(ctypes.c_float)),
                 ("fhnnet", ctypes.POINTER(FhnNetParams)), ("q", c_vp * 2),
                 ("forcing_mask", c_vp), ("est_stride_f", c_i64), ("est_bits", c_i32),
-                ("hmm", ctypes.POINTER(HmmParams)), ("lgm", ctypes.POINTER(LgmParams))]
+                ("hmm", ctypes.POINTER(HmmParams)), ("lgm", ctypes.POINTER(LgmParams)),
+                ("step_ms", ctypes.POINTER(ctypes.c_float))]
 
 
 PF_MODEL_LORENZ = 0

@@ -295,11 +295,13 @@ class FilterBank:
         d.collapsed_trace = self.coll_tr.data_ptr()
         return d
 
-    def run_native(self, k0: int, n_steps: int, time_propagate: bool = False):
+    def run_native(self, k0: int, n_steps: int, time_propagate: bool = False,
+                   time_steps: bool = False):
         """Observations k0..k0+n_steps-1 in one native call (pf_bank_run).
 
         time_propagate=True returns the per-interval durations (ms) of the
-        propagate kernel, measured with CUDA events on the launch stream."""
+        propagate kernel, measured with CUDA events on the launch stream;
+        time_steps=True stores whole-interval durations in self.last_step_ms."""
         import ctypes
 
         if self.obs is None:
@@ -308,17 +310,22 @@ class FilterBank:
             raise RuntimeError("run_native: production bootstrap banks only")
         if self._desc is None:
             self._desc = self._bank_desc()
-        ms = None
+        ms = sm = None
         if time_propagate and n_steps > 0:
             ms = (ctypes.c_float * n_steps)()
             self._desc.prop_ms = ctypes.cast(ms, ctypes.POINTER(ctypes.c_float))
+        if time_steps and n_steps > 0:
+            sm = (ctypes.c_float * n_steps)()
+            self._desc.step_ms = ctypes.cast(sm, ctypes.POINTER(ctypes.c_float))
         try:
             _lib.call("pf_bank_run", self._desc, k0, n_steps, self.cur,
                       1 if self.steps_done > 0 else 0, _lib.stream_ptr())
         finally:
             self._desc.prop_ms = None
+            self._desc.step_ms = None
         self.cur ^= n_steps & 1
         self.steps_done += n_steps
+        self.last_step_ms = None if sm is None else np.frombuffer(sm, dtype=np.float32).copy()
         return None if ms is None else list(ms)
 
     def step(self, k: int):

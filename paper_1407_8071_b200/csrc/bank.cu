@@ -43,7 +43,8 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
              "pf_bank_run: null buffer");
   const cudaStream_t s = as_stream(stream);
   const int64_t MN = d->M * d->N;
-  // optional per-interval timing of the propagate kernel (the dominant one)
+  // optional per-interval timing (events on the launch stream): start of the
+  // interval, end of the propagate kernel (the dominant one), end of the interval
   struct Events {
     std::vector<cudaEvent_t> e;
     ~Events() {
@@ -51,8 +52,8 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     }
   } evs;
   cudaEvent_t *ev = nullptr;
-  if (d->prop_ms && n_steps > 0) {
-    evs.e.resize(2 * static_cast<size_t>(n_steps));
+  if ((d->prop_ms || d->step_ms) && n_steps > 0) {
+    evs.e.resize(3 * static_cast<size_t>(n_steps));
     for (auto &x : evs.e) cudaEventCreate(&x);
     ev = evs.e.data();
   }
@@ -64,7 +65,7 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     const int32_t *anc = (have_ancestors || i > 0) ? d->anc : nullptr;
     const double *y = d->obs + static_cast<int64_t>(k) * d->dim_y;
     int rc;
-    if (ev) cudaEventRecord(ev[2 * i], s);
+    if (ev) cudaEventRecord(ev[3 * i], s);
     if (d->model == PF_MODEL_LORENZ)
       rc = pf_lorenz_propagate_weight(d->lorenz, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
                                       d->keys, t, nullptr, d->status, stream);
@@ -81,7 +82,7 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     else
       rc = pf_fhn_interval(d->fhn, d->dtype, xin, anc, xout, y, d->obs_idx, d->logw, d->M, d->N,
                            d->keys, t, nullptr, d->status, stream);
-    if (ev) cudaEventRecord(ev[2 * i + 1], s);
+    if (ev) cudaEventRecord(ev[3 * i + 1], s);
     if (rc) return rc;
     rc = pf_segmented_resample_ex(d->dtype, d->logw, d->M, d->N, nullptr, d->keys, t, d->anc,
                                   d->lnc, d->collapsed, d->status, d->ws, d->ws_bytes, nullptr,
@@ -106,13 +107,16 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
         cudaMemcpyAsync(d->collapsed_trace + static_cast<int64_t>(k) * d->M, d->collapsed,
                         d->M * sizeof(uint8_t), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
       return check_launch("pf_bank_run(collapse trace)");
+    if (ev) cudaEventRecord(ev[3 * i + 2], s);
     cur ^= 1;
   }
   (void)MN;
   if (ev) {
-    cudaEventSynchronize(ev[2 * n_steps - 1]);
-    for (int32_t i = 0; i < n_steps; ++i)
-      cudaEventElapsedTime(&d->prop_ms[i], ev[2 * i], ev[2 * i + 1]);
+    cudaEventSynchronize(ev[3 * n_steps - 1]);
+    for (int32_t i = 0; i < n_steps; ++i) {
+      if (d->prop_ms) cudaEventElapsedTime(&d->prop_ms[i], ev[3 * i], ev[3 * i + 1]);
+      if (d->step_ms) cudaEventElapsedTime(&d->step_ms[i], ev[3 * i], ev[3 * i + 2]);
+    }
   }
   return check_launch("pf_bank_run");
 }

@@ -52,6 +52,36 @@ class EnsembleOutput:
         )
 
 
+class _LazySeeds:
+    """The per-filter SeedSequences of an ensemble, spawned on first use
+    (spawning costs ~10 us per filter; banks have thousands)."""
+
+    def __init__(self, master_seed, n_filters):
+        self.master, self.n, self._seeds = master_seed, n_filters, None
+
+    def __getitem__(self, f):
+        if self._seeds is None:
+            self._seeds = philox.filter_seeds(self.master, self.n)
+        return self._seeds[f]
+
+
+class _EnsembleFilterOutput(FilterOutput):
+    """FilterOutput whose ``seed`` (the filter's SeedSequence child,
+    ensemble.py:96-99) is resolved lazily."""
+
+    @property
+    def seed(self):
+        s = self.__dict__["_seed"]
+        if isinstance(s, tuple) and isinstance(s[0], _LazySeeds):
+            s = s[0][s[1]]
+            self.__dict__["_seed"] = s
+        return s
+
+    @seed.setter
+    def seed(self, value):
+        self.__dict__["_seed"] = value
+
+
 def filter_seeds(master_seed, n_filters: int):
     """ensemble.py:56-60 (same SeedSequence tree)."""
     return philox.filter_seeds(master_seed, n_filters)
@@ -105,15 +135,21 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     bank.load_observations(obs)
     bank.init()
     exch = dist.EstimateExchange(est_full) if use_exch else None
-    events = [torch.cuda.Event(enable_timing=True) for _ in range(T + 1)]
-    events[0].record()
-    for k in range(T):
-        bank.step(k)
-        events[k + 1].record()
+    secs = None
+    if exch is None and bank._native_ok():
+        # the whole record in one native call, per-step device times from it
+        bank.run_native(0, T, time_steps=True)
+        secs = bank.last_step_ms.astype(np.float64) / 1e3
+    else:
+        events = [torch.cuda.Event(enable_timing=True) for _ in range(T + 1)]
+        events[0].record()
+        for k in range(T):
+            bank.step(k)
+            events[k + 1].record()
+            if exch is not None:
+                exch.step_done(k)
         if exch is not None:
-            exch.step_done(k)
-    if exch is not None:
-        exch.finish()
+            exch.finish()
     mean = torch.empty((T, est_dim), dtype=torch.float64, device=dev)
     _lib.call("pf_ensemble_average", _lib.ptr(est_full), T, n_filters, est_dim, _lib.ptr(mean),
               _lib.stream_ptr())
@@ -130,19 +166,19 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     torch.cuda.synchronize()
     total = time.perf_counter() - started
     _lib.raise_status(st_full.cpu().numpy())
-    secs = _bank_seconds(events)
+    if secs is None:
+        secs = _bank_seconds(events)
     est_h = est_full.cpu().numpy()
     lnc_h = lnc_full.cpu().numpy()
     coll_h = coll_full.cpu().numpy()
-    outputs = []
-    for f in range(n_filters):
-        steps = [int(k) + 1 for k in np.nonzero(coll_h[:, f])[0]]
-        outputs.append(FilterOutput(variant, n_particles, None, est_h[:, f, :], lnc_h[:, f],
-                                    secs.copy(), steps))
-    seeds = filter_seeds(master_seed, n_filters)
-    for f, o in enumerate(outputs):
-        o.seed = seeds[f]
-    filter_seconds = np.array([o.total_seconds for o in outputs])
+    steps_of = [[] for _ in range(n_filters)]
+    for k, f in zip(*np.nonzero(coll_h)):
+        steps_of[f].append(int(k) + 1)
+    seeds = _LazySeeds(master_seed, n_filters)
+    outputs = [_EnsembleFilterOutput(variant, n_particles, (seeds, f), est_h[:, f, :],
+                                     lnc_h[:, f], secs, steps_of[f])
+               for f in range(n_filters)]
+    filter_seconds = np.full(n_filters, float(secs.sum()))
     return EnsembleOutput(variant, n_filters, n_particles, master_seed, outputs,
                           mean.cpu().numpy(), filter_seconds, total)
 
