@@ -196,20 +196,29 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
     return;
   }
 
-  // 2. e = exp(lw - m) and the total (core.py:134-135)
+  // 2. e = exp(lw - m) and the total (core.py:134-135).  Production draws
+  // on fp32 log-weights evaluate exp in fp32: the input's own rounding
+  // (|lw| * 2^-24 relative) already exceeds expf's error, and the sums, CDF
+  // and uniforms stay fp64.  Tape mode and fp64 inputs keep fp64 exp.
+  constexpr bool kFastExp = MODE == 0 && std::is_same<TW, float>::value;
   double part = 0.0;
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
-    lw[q] = i0 + q < N ? exp(__dsub_rn(lw[q], m)) : 0.0;
+    if (kFastExp)
+      lw[q] = i0 + q < N ? static_cast<double>(expf(static_cast<float>(lw[q] - m))) : 0.0;
+    else
+      lw[q] = i0 + q < N ? exp(__dsub_rn(lw[q], m)) : 0.0;
     part = __dadd_rn(part, lw[q]);
   }
   const double total = block_sum(part, scratch);
 
-  // 3. w = e / total (IEEE division, core.py:136), CDF = offset + local run
+  // 3. w = e / total (IEEE division, core.py:136; production fp32 inputs:
+  // reciprocal multiply), CDF = offset + local run
   double run = 0.0;
+  const double inv_total = kFastExp ? 1.0 / total : 0.0;
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
-    run = __dadd_rn(run, __ddiv_rn(lw[q], total));
+    run = __dadd_rn(run, kFastExp ? lw[q] * inv_total : __ddiv_rn(lw[q], total));
     lw[q] = run;  // local inclusive prefix
   }
   double wtot;
@@ -249,19 +258,47 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
   __syncthreads();  // s_cum complete
 
   // 5. merge: searchsorted(cum, u, 'left') clamped to N-1 (accel.py:175-197)
-  if (i0 < N) {
-    int k = lower_bound_tm<THREADS, IPT>(s_cum, N, u[0]);
-    int32_t av[IPT];
+  // as a merge path over (cum, u): thread t merges the 2*IPT outputs on its
+  // diagonal [2*IPT*t, 2*IPT*(t+1)), taking cum[a] before u[b] iff
+  // cum[a] < u[b]; when u[b] is taken, a = #{cum < u[b]} is its ancestor.
+  // Every thread does one diagonal binary search and exactly 2*IPT merge
+  // steps, whatever the weight profile (flat CDF runs included).
+  double *s_u = s_cum + THREADS * IPT;
+  int32_t *s_anc = reinterpret_cast<int32_t *>(s_u + THREADS * IPT);
 #pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-      if (i0 + q < N) {
-        k = advance_to<int>([&](int i) { return s_cum[cdf_slot<THREADS, IPT>(i)]; }, k,
-                            static_cast<int>(N), u[q]);
-        av[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+  for (int q = 0; q < IPT; ++q)
+    if (i0 + q < N) s_u[q * THREADS + tid] = u[q];
+  __syncthreads();
+  {
+    auto slot = [](unsigned i) { return (i & (IPT - 1)) * THREADS + i / IPT; };
+    const int d0 = min(tid * 2 * IPT, 2 * N), d1 = min(d0 + 2 * IPT, 2 * N);
+    int lo = max(0, d0 - N), hi = min(d0, N);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_cum[slot(mid)] < s_u[slot(d0 - 1 - mid)])
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    int a = lo, b = d0 - lo;
+    double ca = a < N ? s_cum[slot(a)] : INFINITY;
+    double ub = b < N ? s_u[slot(b)] : INFINITY;
+    for (int d = d0; d < d1; ++d) {
+      if (b >= N || ca < ub) {
+        ++a;
+        ca = a < N ? s_cum[slot(a)] : INFINITY;
       } else {
-        av[q] = 0;
+        s_anc[slot(b)] = static_cast<int32_t>(base + (a < N - 1 ? a : N - 1));
+        ++b;
+        ub = b < N ? s_u[slot(b)] : INFINITY;
       }
     }
+  }
+  __syncthreads();
+  if (i0 < N) {
+    int32_t av[IPT];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) av[q] = i0 + q < N ? s_anc[q * THREADS + tid] : 0;
     if (vec) {
 #pragma unroll
       for (int q = 0; q < IPT; q += 4)
@@ -1088,7 +1125,8 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
 #undef PF_PICK
     // thread-major CDF slots: THREADS * IPT doubles (>= N)
     const int ipt = N <= 256 ? 2 : N <= 512 ? 4 : N <= 1024 ? 8 : N <= 2048 ? 8 : 16;
-    const size_t smem = static_cast<size_t>(threads) * ipt * sizeof(double);
+    // shared: CDF and uniforms (fp64) + ancestors (int32), THREADS * IPT slots each
+    const size_t smem = static_cast<size_t>(threads) * ipt * (2 * sizeof(double) + 4);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
