@@ -27,7 +27,7 @@ namespace pf {
 
 constexpr int kBankMaxN = 8192;
 constexpr int kBankThreads = 256;
-constexpr int kTile = 4096;          // wide path elements per tile
+constexpr int kTile = 2048;          // wide path elements per tile
 constexpr int kTileThreads = 256;
 
 template <typename TW>
@@ -491,7 +491,7 @@ __global__ void wide_offsets_kernel(int64_t M, int64_t tpf, WideWs ws, int64_t N
 // in registers: one block scan of run totals per tile (instead of one per
 // 256 elements), vector loads, and a padded thread-major shared transpose for
 // coalesced stores.
-constexpr int kRun = kTile / kTileThreads;  // 16
+constexpr int kRun = kTile / kTileThreads;  // 8
 constexpr int kPad = kTileThreads + 1;     // transpose row pitch (conflict-free)
 
 template <typename TW>
@@ -823,19 +823,24 @@ __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) wide2_filter(int64_t N, int64_t tpf, WideWs ws,
-                                                    uint8_t *collapsed, uint32_t *status,
-                                                    double *lnc, const uint32_t *keys,
-                                                    uint32_t t) {
+__global__ void __launch_bounds__(1024) wide2_filter(int64_t N, int64_t tpf, WideWs ws,
+                                                     uint8_t *collapsed, uint32_t *status,
+                                                     double *lnc, const uint32_t *keys,
+                                                     uint32_t t) {
+  // one CTA per filter, 1024 threads; each thread owns runs of kFr
+  // consecutive tiles (weights in registers), so the per-filter max, total
+  // and the two tile-offset scans are one block reduction / scan per 16K
+  // tiles instead of a serial walk
+  constexpr int kFr = 8;
   __shared__ double scratch[33];
-  __shared__ double sw[1024], se[1024];
   const int64_t f = blockIdx.x;
   const double *tmax = ws.tmax + f * tpf, *tsum = ws.tsum + f * tpf, *tes = ws.tesum + f * tpf;
   double mx = -INFINITY;
   int nan = 0;
   for (int64_t i = threadIdx.x; i < tpf; i += blockDim.x) {
-    nan |= isnan(tmax[i]);
-    mx = fmax(mx, tmax[i]);
+    const double v = tmax[i];
+    nan |= isnan(v);
+    mx = fmax(mx, v);
   }
   nan = __syncthreads_or(nan);
   const double m = block_max(mx, scratch);
@@ -851,23 +856,39 @@ __global__ void __launch_bounds__(256) wide2_filter(int64_t N, int64_t tpf, Wide
   for (int64_t i = threadIdx.x; i < tpf; i += blockDim.x)
     part = __dadd_rn(part, __dmul_rn(tsum[i], exp(__dsub_rn(tmax[i], m))));
   const double total = block_sum(part, scratch);
+  const double inv = 1.0 / total;
   double cw = 0.0, ce = 0.0;
-  for (int64_t b0 = 0; b0 < tpf; b0 += 1024) {
-    const int n = static_cast<int>(tpf - b0 < 1024 ? tpf - b0 : 1024);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      sw[i] = __ddiv_rn(__dmul_rn(tsum[b0 + i], exp(__dsub_rn(tmax[b0 + i], m))), total);
-      se[i] = tes[b0 + i];
+  for (int64_t b0 = 0; b0 < tpf; b0 += static_cast<int64_t>(kFr) * blockDim.x) {
+    const int64_t j0 = b0 + static_cast<int64_t>(threadIdx.x) * kFr;
+    double wv[kFr], ev[kFr];
+    double rw = 0.0, re = 0.0;
+#pragma unroll
+    for (int q = 0; q < kFr; ++q) {
+      const int64_t j = j0 + q;
+      const double w = j < tpf
+                           ? (MODE == 1 ? __ddiv_rn(__dmul_rn(tsum[j], exp(__dsub_rn(tmax[j], m))),
+                                                    total)
+                                        : __dmul_rn(tsum[j], exp(__dsub_rn(tmax[j], m))) * inv)
+                           : 0.0;
+      const double e = j < tpf ? tes[j] : 0.0;
+      wv[q] = rw;  // exclusive within the run
+      ev[q] = re;
+      rw = __dadd_rn(rw, w);
+      re = __dadd_rn(re, e);
     }
-    __syncthreads();
-    const double cw_next = block_scan_inplace(sw, n, cw, scratch);
-    const double ce_next = block_scan_inplace(se, n, ce, scratch);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      ws.twoff[f * tpf + b0 + i] = i == 0 ? cw : sw[i - 1];
-      ws.teoff[f * tpf + b0 + i] = i == 0 ? ce : se[i - 1];
+    double tw, te;
+    const double ow = __dadd_rn(cw, block_exclusive_scan(rw, scratch, &tw));
+    const double oe = __dadd_rn(ce, block_exclusive_scan(re, scratch, &te));
+#pragma unroll
+    for (int q = 0; q < kFr; ++q) {
+      const int64_t j = j0 + q;
+      if (j < tpf) {
+        ws.twoff[f * tpf + j] = __dadd_rn(ow, wv[q]);
+        ws.teoff[f * tpf + j] = __dadd_rn(oe, ev[q]);
+      }
     }
-    __syncthreads();
-    cw = cw_next;
-    ce = ce_next;
+    cw = __dadd_rn(cw, tw);
+    ce = __dadd_rn(ce, te);
   }
   if (threadIdx.x == 0) {
     ws.total[f] = total;
@@ -916,14 +937,16 @@ __global__ void wide2_partition(int64_t N, int64_t tpf, int64_t ntiles, WideWs w
 }
 
 template <int MODE, bool GATHER>
-__global__ void __launch_bounds__(kTileThreads, 2) wide2_merge(
+__global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
     int64_t N, int64_t tpf, WideWs ws, const double *__restrict__ u_tape,
     const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
     const float *__restrict__ gx_in, float *__restrict__ gx_out, int gdims, int64_t gMN) {
-  __shared__ double s_c[kWin];  // CDF window, then reused for the ancestor transpose
+  // dynamic shared: CDF window | uniforms (fast path) | ancestor transpose
+  extern __shared__ double s_dyn[];
+  double *s_c = s_dyn;
+  double *s_u = s_dyn + kWin;
+  int32_t *s_a = reinterpret_cast<int32_t *>(s_u + kTile);
   __shared__ double scratch[33];
-  static_assert(kRun * kPad * sizeof(int32_t) <= kWin * sizeof(double), "transpose must fit");
-  int32_t *s_a = reinterpret_cast<int32_t *>(s_c);
   const int64_t tile = blockIdx.x;
   const int64_t f = tile / tpf, tt = tile - f * tpf;
   const int64_t i0 = tt * kTile;
@@ -975,7 +998,47 @@ __global__ void __launch_bounds__(kTileThreads, 2) wide2_merge(
     for (int q = 0; q < kRun; ++q) u[q] = r0 + q < n ? __dadd_rn(off, u[q]) * inv : 2.0;
   }
   int32_t a[kRun];
-  if (chunked) {
+  if (wlen <= kWin) {
+    // fast path: the whole CDF window and the tile's uniforms sit in shared
+    // memory; a merge path gives every thread one diagonal binary search and
+    // a fixed number of merge steps (cum[k] taken before u iff cum[k] < u)
+    auto us = [](unsigned j) { return (j % kRun) * kTileThreads + j / kRun; };
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const int i = r * kTileThreads + threadIdx.x;
+      if (i < len0) s_c[i] = cv[r];
+    }
+#pragma unroll
+    for (int q = 0; q < kRun; ++q)
+      if (r0 + q < n) s_u[q * kTileThreads + threadIdx.x] = u[q];
+    __syncthreads();
+    const int A = static_cast<int>(wlen), L = A + n;
+    const int per = (L + kTileThreads - 1) / kTileThreads;
+    const int d0 = min(static_cast<int>(threadIdx.x) * per, L), d1 = min(d0 + per, L);
+    int lo2 = max(0, d0 - n), hi2 = min(d0, A);
+    while (lo2 < hi2) {
+      const int mid = (lo2 + hi2) >> 1;
+      if (s_c[mid] < s_u[us(d0 - 1 - mid)])
+        lo2 = mid + 1;
+      else
+        hi2 = mid;
+    }
+    int ka = lo2, jb = d0 - lo2;
+    double ca = ka < A ? s_c[ka] : INFINITY;
+    double ub = jb < n ? s_u[us(jb)] : INFINITY;
+    for (int d = d0; d < d1; ++d) {
+      if (jb >= n || ca < ub) {
+        ++ka;
+        ca = ka < A ? s_c[ka] : INFINITY;
+      } else {
+        const int64_t k = lo + ka;
+        s_a[(jb % kRun) * kPad + jb / kRun] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
+        ++jb;
+        ub = jb < n ? s_u[us(jb)] : INFINITY;
+      }
+    }
+    __syncthreads();
+  } else if (chunked) {
     // stream the CDF window through shared memory in kWin chunks; every
     // uniform is placed in the chunk holding its answer (answers are
     // non-decreasing, so each thread resumes from its previous answer)
@@ -1023,10 +1086,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) wide2_merge(
       a[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
     }
   }
-  __syncthreads();  // all window reads done before s_c is reused
+  if (wlen > kWin) {
 #pragma unroll
-  for (int q = 0; q < kRun; ++q) s_a[q * kPad + threadIdx.x] = a[q];
-  __syncthreads();
+    for (int q = 0; q < kRun; ++q) s_a[q * kPad + threadIdx.x] = a[q];
+    __syncthreads();
+  }
   // coalesced write-out (thread-strided elements), gather loads batched 4 deep
   for (int e0 = threadIdx.x; e0 < n; e0 += 4 * kTileThreads) {
     int32_t ai[4];
@@ -1160,11 +1224,11 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
   } else {
     if (u_tape) {
       wide2_tile_stats<TW, 1><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, keys, t);
-      wide2_filter<1><<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, collapsed, status,
+      wide2_filter<1><<<static_cast<unsigned>(M), 1024, 0, s>>>(N, tpf, ws, collapsed, status,
                                                                lnc, keys, t);
     } else {
       wide2_tile_stats<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, keys, t);
-      wide2_filter<0><<<static_cast<unsigned>(M), 256, 0, s>>>(N, tpf, ws, collapsed, status,
+      wide2_filter<0><<<static_cast<unsigned>(M), 1024, 0, s>>>(N, tpf, ws, collapsed, status,
                                                                lnc, keys, t);
     }
     wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
@@ -1175,7 +1239,10 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
     wide2_partition<0><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
   // merge -> ancestors, then the gather as its own high-occupancy pass
   auto mk = u_tape ? wide2_merge<1, false> : wide2_merge<0, false>;
-  mk<<<nt, kTileThreads, 0, s>>>(N, tpf, ws, u_tape, keys, t, anc, nullptr, nullptr, 0, M * N);
+  const size_t msmem = (kWin + kTile) * sizeof(double) + kRun * kPad * sizeof(int32_t);
+  cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem));
+  mk<<<nt, kTileThreads, msmem, s>>>(N, tpf, ws, u_tape, keys, t, anc, nullptr, nullptr, 0,
+                                     M * N);
   if (gx_in) {
     const int64_t MN = M * N;
     if (gdims == 3 && (MN & 3) == 0)
