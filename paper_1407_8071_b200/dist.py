@@ -93,3 +93,63 @@ def allreduce_disjoint(t):
 
 def local_rank() -> int:
     return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def owner_of(i: int, n: int, world_size: int) -> int:
+    """Rank owning global id i under shard_range's block partition."""
+    base, rem = divmod(n, world_size)
+    cut = rem * (base + 1)
+    return i // (base + 1) if i < cut else rem + (i - cut) // max(base, 1)
+
+
+def exchange_islands(idx, n_islands: int, get_island, template):
+    """Whole-island resampling across ranks (double bootstrap, filters.py:258-263,
+    SURVEY §8f #4).  Island m (owned by rank owner_of(m)) becomes a copy of
+    island idx[m]; ``idx`` is the same on every rank (identical selection).
+
+    get_island(src) returns the particle block (tensor or tuple of tensors)
+    of a LOCAL island src; ``template`` gives the block shapes/dtypes for
+    receive buffers.  Returns {m: block} for every local destination m.
+    Sends and receives between any two ranks are issued in increasing m, so
+    they match in order (NCCL groups them with batch_isend_irecv)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world_size = world()
+    lo, hi = shard_range(n_islands, rank, world_size)
+    as_tuple = lambda b: b if isinstance(b, tuple) else (b,)  # noqa: E731
+    ops, out, cache = [], {}, {}
+
+    def local(src):
+        if src not in cache:
+            cache[src] = tuple(x.contiguous() for x in as_tuple(get_island(src)))
+        return cache[src]
+
+    for m in range(n_islands):
+        src = int(idx[m])
+        dst_rank, src_rank = owner_of(m, n_islands, world_size), owner_of(src, n_islands,
+                                                                           world_size)
+        if src_rank == rank and dst_rank != rank:
+            for part in local(src):
+                ops.append(("send", part, dst_rank))
+        elif dst_rank == rank:
+            if src_rank == rank:
+                out[m] = local(src)
+            else:
+                bufs = tuple(torch.empty_like(t) for t in as_tuple(template))
+                for part in bufs:
+                    ops.append(("recv", part, src_rank))
+                out[m] = bufs
+    if ops:
+        if dist.get_backend() == "nccl":
+            p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, t, peer)
+                   for kind, t, peer in ops]
+            for w in dist.batch_isend_irecv(p2p):
+                w.wait()
+        else:
+            works = [(dist.isend if kind == "send" else dist.irecv)(t, peer)
+                     for kind, t, peer in ops]
+            for w in works:
+                w.wait()
+    single = not isinstance(template, tuple)
+    return {m: (b[0] if single else b) for m, b in out.items()}

@@ -7,26 +7,31 @@ resampling the island log-weights accumulate the islands' lnc increments;
 every ``island_period`` steps whole islands are resampled by those weights
 with the island key (``spawn(M + 1)[M]``) through the same segmented
 resampler (one segment of M "particles"), and island m takes over island
-idx[m]'s ancestors, lnc and collapse flag - particle states are never
-copied, the next propagate gathers them.  The pooled estimate and the
+idx[m]'s particles, lnc and collapse flag.  The pooled estimate and the
 normalising-constant trace are computed on the device.
 
-Single GPU: island selection is global, so sharding islands over ranks
-would need a particle exchange every period; not done here.
+One GPU: island m simply takes island idx[m]'s *ancestors* (states are never
+copied; the next propagate gathers them).  Several GPUs (one process per GPU,
+islands block-sharded by id): the island log-weights, lnc and collapse flags
+are combined with disjoint-support all-reduces, every rank draws the same
+island selection, and islands that change rank move as particle blocks over
+NCCL point-to-point (dist.exchange_islands); each rank then materialises its
+new islands and continues with identity ancestors.  Results are identical
+for any number of GPUs.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-from . import _lib, philox
+from . import _lib, dist, philox
 from .bank import DrawTape, FilterBank
-from .filters import FilterOutput, _bank_seconds
+from .filters import FilterOutput
 
 
 class IslandBank:
     def __init__(self, model, n_islands: int, n_particles: int, island_period: int, seed,
-                 n_steps: int, *, dtype=None, tape: DrawTape | None = None):
+                 n_steps: int, *, dtype=None, tape: DrawTape | None = None, shard=None):
         import torch
 
         if n_islands < 1:
@@ -40,18 +45,29 @@ class IslandBank:
         keys = np.stack([philox.seed_key(c) for c in children[:n_islands]]).astype(np.uint32)
         self.M, self.N, self.period, self.T = n_islands, n_particles, island_period, n_steps
         self.tape = tape
-        self.bank = FilterBank(model, n_islands, n_particles, keys, n_steps, dtype=dtype,
-                               tape=tape, estimate="full")
-        dev = self.bank.device
+        rank, world = dist.world()
+        self.sharded = (world > 1 and shard is not False) or (shard is True and dist.initialized())
+        if not self.sharded:
+            rank, world = 0, 1
+        self.lo, self.hi = dist.shard_range(n_islands, rank, world)
+        dev = torch.device("cuda", torch.cuda.current_device())
         kw = dict(device=dev)
+        # per-island estimates of every island (rows of other ranks arrive by all-reduce)
+        self.est_isl = torch.zeros((n_steps, n_islands, model.dim_x), dtype=torch.float64, **kw)
+        self.bank = FilterBank(model, self.hi - self.lo, n_particles, keys[self.lo:self.hi],
+                               n_steps, dtype=dtype, tape=tape, estimate="full",
+                               filter_offset=self.lo, est_buffer=self.est_isl,
+                               est_row_offset=self.lo)
         ik = philox.seed_key(children[n_islands]).astype(np.uint32)[None, :]
         self.island_key = torch.from_numpy(ik.view(np.int32)).to(dev)
-        self.lw = torch.zeros(n_islands, dtype=torch.float64, **kw)
-        self.lnc_old = torch.empty(n_islands, dtype=torch.float64, **kw)
+        Ml = self.hi - self.lo
+        self.lw = torch.zeros(n_islands, dtype=torch.float64, **kw)  # full; local slice updated
+        self.lnc_old = torch.empty(Ml, dtype=torch.float64, **kw)
         self.idx = torch.empty(n_islands, dtype=torch.int32, **kw)
         self.anc_tmp = torch.empty_like(self.bank.anc)
         self.lnc_tmp = torch.empty_like(self.bank.lnc)
         self.coll_tmp = torch.empty_like(self.bank.collapsed)
+        self.lnc_all = torch.zeros(n_islands, dtype=torch.float64, **kw)
         # scratch outputs of the island-level resample (1 segment of M)
         self.s_lnc = torch.zeros(1, dtype=torch.float64, **kw)
         self.s_coll = torch.zeros(1, dtype=torch.uint8, **kw)
@@ -64,15 +80,10 @@ class IslandBank:
         self.bank.post_resample = self._islands
         self.island_steps = []
 
-    def _islands(self, k, t):
+    # -- island selection -------------------------------------------------------
+    def _select(self, t):
         import torch
 
-        b = self.bank
-        s = _lib.stream_ptr()
-        _lib.call("pf_island_accumulate", _lib.ptr(self.lw), _lib.ptr(b.lnc),
-                  _lib.ptr(self.lnc_old), self.M, s)
-        if t % self.period:
-            return
         uni = None
         flags = 0
         if self.tape is not None:
@@ -80,18 +91,90 @@ class IslandBank:
             if u is None:
                 raise ValueError(f"tape has no island uniforms for t={t}")
             uni = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64).reshape(1, -1)) \
-                .to(b.device)
+                .to(self.bank.device)
             self._keep = uni
             flags = _lib.PF_RS_REFERENCE_ORDER
         _lib.call("pf_segmented_resample_ex", _lib.PF_F64, _lib.ptr(self.lw), 1, self.M,
                   _lib.ptr(uni), _lib.ptr(self.island_key), t, _lib.ptr(self.idx),
                   _lib.ptr(self.s_lnc), _lib.ptr(self.s_coll), _lib.ptr(self.s_status),
-                  _lib.ptr(self.ws), self.ws_bytes, None, None, 0, flags, s)
-        _lib.call("pf_island_copy", _lib.ptr(self.idx), _lib.ptr(b.anc), _lib.ptr(b.lnc),
-                  _lib.ptr(b.collapsed), _lib.ptr(self.lw), self.M, self.N,
-                  _lib.ptr(self.anc_tmp), _lib.ptr(self.lnc_tmp), _lib.ptr(self.coll_tmp), s)
+                  _lib.ptr(self.ws), self.ws_bytes, None, None, 0, flags, _lib.stream_ptr())
+
+    def _islands(self, k, t):
+        b = self.bank
+        s = _lib.stream_ptr()
+        Ml = self.hi - self.lo
+        lw_local = self.lw[self.lo:self.hi]
+        _lib.call("pf_island_accumulate", _lib.ptr(lw_local), _lib.ptr(b.lnc),
+                  _lib.ptr(self.lnc_old), Ml, s)
+        if t % self.period:
+            return
+        if not self.sharded:
+            self._select(t)
+            _lib.call("pf_island_copy", _lib.ptr(self.idx), _lib.ptr(b.anc), _lib.ptr(b.lnc),
+                      _lib.ptr(b.collapsed), _lib.ptr(self.lw), self.M, self.N,
+                      _lib.ptr(self.anc_tmp), _lib.ptr(self.lnc_tmp), _lib.ptr(self.coll_tmp), s)
+        else:
+            self._islands_sharded(t)
         self.island_steps.append(t)
 
+    def _islands_sharded(self, t):
+        """Cross-rank island resampling: full log-weights by a disjoint
+        all-reduce, the same selection on every rank, particle blocks moved
+        with NCCL point-to-point, new islands materialised locally."""
+        import torch
+
+        b = self.bank
+        lo, hi, N = self.lo, self.hi, self.N
+        others = torch.ones(self.M, dtype=torch.bool, device=self.lw.device)
+        others[lo:hi] = False
+        self.lw[others] = 0.0
+        dist.allreduce_disjoint(self.lw)
+        self._select(t)
+        idx = self.idx.cpu().numpy()
+        # every island's lnc and collapse flag (disjoint all-reduce)
+        self.lnc_all.zero_()
+        self.lnc_all[lo:hi] = b.lnc
+        dist.allreduce_disjoint(self.lnc_all)
+        coll_all = torch.zeros(self.M, dtype=torch.int32, device=self.lw.device)
+        coll_all[lo:hi] = b.collapsed.to(torch.int32)
+        dist.allreduce_disjoint(coll_all)
+        # current particles of a local island: propagated rows through the ancestors
+        xprop = b.x[1 - b.cur]  # the step's output buffer (cur flips after the step)
+        planes = b.model.kind in ("lorenz", "hmm", "lgm")
+
+        def get_island(src):
+            rows = b.anc[(src - lo) * N:(src - lo + 1) * N].long()
+            if planes:
+                blk = xprop.index_select(1, rows)
+            else:
+                blk = xprop.index_select(0, rows)
+            if b.q[0] is not None:
+                return blk, b.q[1 - b.cur].index_select(0, rows)
+            return blk
+
+        template = get_island(lo) if hi > lo else None
+        out = dist.exchange_islands(idx, self.M, get_island, template)
+        new = torch.empty_like(xprop)
+        newq = torch.empty_like(b.q[1 - b.cur]) if b.q[0] is not None else None
+        for m, blk in out.items():
+            j = m - lo
+            if newq is not None:
+                blk, qb = blk
+                newq[j * N:(j + 1) * N] = qb
+            if planes:
+                new[:, j * N:(j + 1) * N] = blk
+            else:
+                new[j * N:(j + 1) * N] = blk
+        xprop.copy_(new)
+        if newq is not None:
+            b.q[1 - b.cur].copy_(newq)
+        torch.arange(0, (hi - lo) * N, dtype=torch.int32, out=b.anc)  # local rows
+        sel = torch.from_numpy(idx[lo:hi].astype(np.int64)).to(self.lw.device)
+        b.lnc.copy_(self.lnc_all[sel])
+        b.collapsed.copy_(coll_all[sel].to(torch.uint8))
+        self.lw.zero_()
+
+    # -- driver ----------------------------------------------------------------------
     def run(self, observations):
         import torch
 
@@ -105,33 +188,57 @@ class IslandBank:
         for k in range(self.T):
             self.lnc_old.copy_(b.lnc)
             b.step(k)
-            _lib.call("pf_island_pool", _lib.ptr(b.est[k]), b.est_width, self.M,
-                      self.bank.model.dim_x, _lib.ptr(self.lw),
+            self.lnc_all.zero_()
+            self.lnc_all[self.lo:self.hi] = b.lnc
+            lw_full = self.lw
+            if self.sharded:
+                # rows / entries of other ranks' islands arrive by disjoint all-reduce
+                dist.allreduce_disjoint(self.est_isl[k])
+                dist.allreduce_disjoint(self.lnc_all)
+                lw_full = self.lw.clone()
+                mask = torch.ones(self.M, dtype=torch.bool, device=lw_full.device)
+                mask[self.lo:self.hi] = False
+                lw_full[mask] = 0.0
+                dist.allreduce_disjoint(lw_full)
+            _lib.call("pf_island_pool", _lib.ptr(self.est_isl[k]), self.est_isl.stride(1),
+                      self.M, b.model.dim_x, _lib.ptr(lw_full),
                       _lib.c_vp(self.est.data_ptr() + k * self.est.stride(0) * 8), s)
-            _lib.call("pf_island_trace", _lib.ptr(b.lnc), self.M,
+            _lib.call("pf_island_trace", _lib.ptr(self.lnc_all), self.M,
                       _lib.c_vp(self.trace.data_ptr() + k * 8), s)
             events[k + 1].record()
         torch.cuda.synchronize()
-        b.check_status()
-        return _bank_seconds(events)
+        st = torch.zeros(self.M, dtype=torch.int32, device=b.device)
+        st[self.lo:self.hi] = b.status
+        if self.sharded:
+            dist.allreduce_disjoint(st)
+        _lib.raise_status(st.cpu().numpy())
+        return np.array([events[i].elapsed_time(events[i + 1]) / 1e3 for i in range(self.T)])
 
     def collapse_steps(self) -> list[int]:
-        c = self.bank.coll_tr.cpu().numpy()
+        import torch
+
+        c = torch.zeros((self.T, self.M), dtype=torch.int32, device=self.bank.device)
+        c[:, self.lo:self.hi] = self.bank.coll_tr.to(torch.int32)
+        if self.sharded:
+            dist.allreduce_disjoint(c)
+        c = c.cpu().numpy()
         return [int(k) + 1 for k in np.nonzero(c.any(axis=1))[0]]
 
 
 def run_double_bootstrap(model, observations, n_islands: int, n_particles: int,
                          island_period: int, seed, *, dtype=None,
-                         tape: DrawTape | None = None) -> FilterOutput:
+                         tape: DrawTape | None = None, shard=None) -> FilterOutput:
     """filters.py:274-313 on the GPU bank; same seeding tree, estimates
-    (pooled island posterior means) and diagnostic lnc trace."""
+    (pooled island posterior means) and diagnostic lnc trace.  Under
+    torch.distributed the islands are sharded over ranks (shard=None: when
+    the world size is > 1); every rank returns the same FilterOutput."""
     obs = np.atleast_2d(np.asarray(observations, dtype=np.float64))
     if obs.shape[0] == 0:
         raise ValueError("observation sequence must be non-empty")
     if getattr(model, "dim_y", obs.shape[1]) == 1 and obs.shape[1] != 1:
         obs = obs.reshape(-1, 1)
     ib = IslandBank(model, n_islands, n_particles, island_period, seed, obs.shape[0],
-                    dtype=dtype, tape=tape)
+                    dtype=dtype, tape=tape, shard=shard)
     secs = ib.run(obs)
     return FilterOutput("double-bf", n_islands * n_particles, seed, ib.est.cpu().numpy(),
                         ib.trace.cpu().numpy(), secs, ib.collapse_steps())

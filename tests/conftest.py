@@ -11,6 +11,10 @@ if REPO not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running statistical test")
+    # the CPU oracle's fork pool (the reference's ensemble workers) in a
+    # process that also runs CUDA threads
+    config.addinivalue_line("filterwarnings",
+                            "ignore:This process .* is multi-threaded:DeprecationWarning")
 
 
 @pytest.fixture(scope="session")

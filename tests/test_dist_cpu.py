@@ -82,3 +82,51 @@ def test_disjoint_allreduce_two_ranks_bit_identical():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_owner_of_matches_shard_range():
+    for n in (1, 5, 7, 64):
+        for w in (1, 2, 3, 4):
+            if n < w:
+                continue
+            for r in range(w):
+                lo, hi = pdist.shard_range(n, r, w)
+                assert all(pdist.owner_of(i, n, w) == r for i in range(lo, hi))
+
+
+def _island_worker(rank, world, port, M, idx, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = pdist.shard_range(M, rank, world)
+        # island i's particle block: (3, 4) values 100*i + j, plus a tuple member
+        blocks = {i: (torch.arange(12, dtype=torch.float32).reshape(3, 4) + 100 * i,
+                      torch.full((4,), i, dtype=torch.int32)) for i in range(lo, hi)}
+        tmpl = (torch.zeros(3, 4), torch.zeros(4, dtype=torch.int32))
+        out = pdist.exchange_islands(idx, M, lambda s: blocks[s], tmpl)
+        assert sorted(out) == list(range(lo, hi))
+        for m, (a, b) in out.items():
+            src = idx[m]
+            assert torch.equal(a, torch.arange(12, dtype=torch.float32).reshape(3, 4) + 100 * src)
+            assert torch.equal(b, torch.full((4,), src, dtype=torch.int32))
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_island_exchange_two_ranks():
+    """Double-bootstrap island copies across ranks (gloo, world size 2)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    idx = [4, 4, 0, 2, 1]  # cross-rank copies in both directions, duplicates
+    procs = [ctx.Process(target=_island_worker, args=(r, 2, port, 5, idx, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res

@@ -31,6 +31,15 @@ a = pf.run_ensemble(m, obs, "bootstrap", 6, 256, 3, shard=True)
 b = pf.run_ensemble(m, obs, "bootstrap", 6, 256, 3, shard=False)
 assert a.same_result(b), "exchange path changed the result"
 assert a.mean_estimates.tobytes() == b.mean_estimates.tobytes()
+# double bootstrap: the sharded island path (disjoint all-reduces, island
+# materialisation, point-to-point exchange) equals the single-GPU path
+from paper_1407_8071_b200 import islands
+for model, ob in ((m, obs), (pf.FhnNetworkModel(J=8, n_zones=2, zone_width=2, stim_prob=0.05),
+                             pf.simulate.simulate(pf.FhnNetworkModel(J=8, n_zones=2,
+                                                  zone_width=2, stim_prob=0.05), 12, 4)[1])):
+    da = islands.run_double_bootstrap(model, ob, 5, 128, 3, 9, shard=True)
+    db = islands.run_double_bootstrap(model, ob, 5, 128, 3, 9, shard=False)
+    assert da.same_result(db), "sharded island path changed the result"
 dist.destroy_process_group()
 print("OK")
 """
