@@ -1023,19 +1023,24 @@ __global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
       else
         hi2 = mid;
     }
-    int ka = lo2, jb = d0 - lo2;
-    double ca = ka < A ? s_c[ka] : INFINITY;
-    double ub = jb < n ? s_u[us(jb)] : INFINITY;
+    // branch-free merge: lanes differ only in which list they advance; one
+    // shared load per step from the selected list (no divergent paths)
+    unsigned ka = lo2, jb = d0 - lo2;
+    const unsigned uA = A, un = n;
+    const unsigned kcap = static_cast<unsigned>(N - 1 - lo);  // clamp to N-1 (accel.py:183)
+    const int32_t row0 = static_cast<int32_t>(base + lo);
+    double ca = ka < uA ? s_c[ka] : INFINITY;
+    double ub = jb < un ? s_u[us(jb)] : INFINITY;
     for (int d = d0; d < d1; ++d) {
-      if (jb >= n || ca < ub) {
-        ++ka;
-        ca = ka < A ? s_c[ka] : INFINITY;
-      } else {
-        const int64_t k = lo + ka;
-        s_a[(jb % kRun) * kPad + jb / kRun] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
-        ++jb;
-        ub = jb < n ? s_u[us(jb)] : INFINITY;
-      }
+      const bool take_c = jb >= un || ca < ub;
+      if (!take_c) s_a[(jb & (kRun - 1)) * kPad + jb / kRun] =
+          row0 + static_cast<int32_t>(ka < kcap ? ka : kcap);
+      ka += take_c;
+      jb += !take_c;
+      const double *src = take_c ? s_c + (ka < uA ? ka : uA - 1) : s_u + us(jb < un ? jb : un - 1);
+      const double v = *src;
+      ca = take_c ? (ka < uA ? v : INFINITY) : ca;
+      ub = take_c ? ub : (jb < un ? v : INFINITY);
     }
     __syncthreads();
   } else if (chunked) {
