@@ -54,6 +54,18 @@ CONFIGS = {
                  desc="Lorenz-63, M=4 x N=1000, 40 Euler steps/obs, fp64"),
     # the paper's own lattice (models/fhn.py:85-207): not a
     # BASELINE config; same metric, one Euler step per observation
+    # SURVEY §8f rows on the same metric: the auxiliary filter (two-stage
+    # resampling with a noise-free lookahead propagate; filter particle-steps
+    # counted, the lookahead is extra work) and the double bootstrap (islands)
+    "cfg4apf": dict(kind="fhn", variant="auxiliary", M=64, N=4096, dtype="float32",
+                    desc="FH-N 30x50 lattice, auxiliary PF, M=64 x N=4096, 50 Euler steps/obs "
+                         "(+50 lookahead steps not counted), fp32"),
+    "cfg2apf": dict(kind="lorenz", variant="auxiliary", M=4096, N=1024, dtype="float32",
+                    desc="Lorenz-63 auxiliary PF, M=4096 x N=1024, 40 Euler steps/obs "
+                         "(+40 lookahead steps not counted), fp32"),
+    "dbf": dict(kind="lorenz", variant="double-bf", M=64, N=65536, dtype="float32", period=5,
+                desc="Lorenz-63 double bootstrap, 64 islands x 65536 particles, island "
+                     "resampling every 5 observations, fp32"),
     "net": dict(kind="fhnnet", M=64, N=4096, dtype="float32",
                 desc="paper FH-N network 32x32 (stimuli, forcing, 25-step history), "
                      "M=64 x N=4096, 1 Euler step/obs, fp32"),
@@ -202,9 +214,12 @@ def cpu_baseline(cfg, budget_s=12.0, steps=1):
         model = orc.LorenzConfigModel(prior_mean=tuple(truth0))
         n_part = 1024 if cfg["N"] >= 1024 else cfg["N"]
         n_sub = model.substeps
+    variant = cfg.get("variant", "bootstrap")
+    if variant == "double-bf":
+        return _cpu_baseline_dbf(cfg, model, obs, n_sub, budget_s)
     # calibrate: one filter, one step
     t0 = time.perf_counter()
-    orc.run_filter(model, obs[:1], n_part, 0)
+    orc.run_filter(model, obs[:1], n_part, 0, variant=variant)
     one = max(time.perf_counter() - t0, 1e-6)
     per_worker = max(1, int(budget_s / max(steps, 1) / one))
     # never more filters than the workload has (cfg0 has M=4): the reference
@@ -220,14 +235,37 @@ def cpu_baseline(cfg, budget_s=12.0, steps=1):
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=workers, mp_context=get_context("fork")) as pool:
         list(pool.map(orc._filter_task,
-                      [(model, obs[:steps], n_part, s, False)
+                      [(model, obs[:steps], n_part, s, False, variant)
                        for s in orc.filter_seeds(1, n_filters)]))
     wall = time.perf_counter() - t0
     ps = n_filters * n_part * n_sub * steps
     return {"value": ps / wall, "unit": "particle-steps/s", "cores": workers, "kind": "port",
-            "sample": (f"{n_filters} filters x {n_part} particles x {steps} obs x {n_sub} Euler "
-                       f"steps of the {cfg['kind']} config model, fp64 numpy driver + C kernels "
-                       f"(oracle/), fork pool of {workers} workers; {wall:.1f} s wall")}
+            "sample": (f"{n_filters} {variant} filters x {n_part} particles x {steps} obs x "
+                       f"{n_sub} Euler steps of the {cfg['kind']} config model, fp64 numpy "
+                       f"driver + C kernels (oracle/), fork pool of {workers} workers; "
+                       f"{wall:.1f} s wall")}
+
+
+def _cpu_baseline_dbf(cfg, model, obs, n_sub, budget_s):
+    """The reference's double bootstrap runs its islands in one process
+    (filters.py:274-313): one core, a bounded island count / size."""
+    from oracle import parpf_oracle as orc
+
+    M, period = min(cfg["M"], 16), cfg.get("period", 5)
+    n_part, steps = 256, max(period, 1)
+    obs_s = np.resize(obs, (steps, obs.shape[1]))
+    t0 = time.perf_counter()
+    orc.run_double_bootstrap(model, obs_s[:1], M, n_part, period, 0)
+    one = max(time.perf_counter() - t0, 1e-6)
+    n_part = max(64, min(cfg["N"], int(n_part * budget_s / (one * steps))))
+    t0 = time.perf_counter()
+    orc.run_double_bootstrap(model, obs_s, M, n_part, period, 1)
+    wall = time.perf_counter() - t0
+    ps = M * n_part * n_sub * steps
+    return {"value": ps / wall, "unit": "particle-steps/s", "cores": 1, "kind": "port",
+            "sample": (f"double bootstrap, {M} islands x {n_part} particles x {steps} obs "
+                       f"(one island resampling) x {n_sub} Euler steps, fp64 numpy driver + C "
+                       f"kernels, single process; {wall:.1f} s wall")}
 
 
 def run_reference_arm(args, cfg):
@@ -534,6 +572,115 @@ def run_ours(args, cfg):
     return 0
 
 
+def run_variant(args, cfg):
+    """Auxiliary PF / double bootstrap on one GPU: W untimed steps, K timed
+    steps bracketed by CUDA events (synchronised), the propagate kernel
+    timed with events around its launch."""
+    import torch
+
+    import paper_1407_8071_b200 as pf
+    from paper_1407_8071_b200 import islands, philox
+
+    rank, world, local = _dist_setup()
+    if world > 1:
+        raise SystemExit(f"{args.config}: single-GPU workload")
+    M, N, variant = cfg["M"], cfg["N"], cfg["variant"]
+    T = args.warmup + args.steps
+    model, obs = _make_model_and_obs(cfg, T)
+    n_sub = getattr(model, "substeps", 1)
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    if variant == "double-bf":
+        runner = islands.IslandBank(model, M, N, cfg["period"], 7, T, dtype=cfg["dtype"])
+        runner.start(obs)
+        bank, step = runner.bank, runner.step
+    else:
+        bank = pf.FilterBank(model, M, N, philox.filter_keys(7, M), T, dtype=cfg["dtype"],
+                             estimate="projection", variant=variant)
+        bank.load_observations(obs)
+        bank.init()
+        step = bank.step
+    bank.kernel_events = ev
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        start.record()
+        for i in range(args.steps):
+            bank.kernel_events = evs[i]  # events around this step's propagate launch
+            step(args.warmup + i)
+        end.record()
+        torch.cuda.synchronize()
+    elapsed = start.elapsed_time(end) / 1e3
+    bank.check_status()
+    ps_total = M * N * n_sub * args.steps
+    value = ps_total / elapsed
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    peaks, peak_src = _peaks()
+    if cfg["kind"] == "fhn":
+        ach = M * N * n_sub * FHN_BYTES_PER_PS / (kern_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "peak_source": peak_src,
+                "kernel": "fhn_fast_kernel (second-stage propagate)",
+                "algorithmic": f"{FHN_BYTES_PER_PS:.0f} B/particle-step x {M * N * n_sub}"}
+    else:
+        ach = M * N * n_sub * LORENZ_FLOP_PER_PS / (kern_ms / 1e3) / 1e12
+        roof = {"bound": "fp32", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP32_PEAK_TFLOPS,
+                "peak_source": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (SURVEY §8d)",
+                "kernel": "lorenz_fast_kernel (propagate)",
+                "algorithmic": f"{LORENZ_FLOP_PER_PS:.0f} flop/particle-step x {M * N * n_sub}"}
+    roof["kernel_ms"] = kern_ms
+    roof["kernel_share_of_step"] = kern_ms * args.steps / (elapsed * 1e3)
+    roof["traffic"] = None
+    if args.profile:
+        print(json.dumps({"profile_run": args.config, "value": value, "kernel_ms": kern_ms}))
+        return 0
+    del bank, step
+    if variant == "double-bf":
+        del runner
+    e2e_obs = obs[: args.steps]
+    call = (lambda o: islands.run_double_bootstrap(model, o, M, N, cfg["period"], 7,
+                                                   dtype=cfg["dtype"])) \
+        if variant == "double-bf" else \
+        (lambda o: pf.run_ensemble(model, o, variant, M, N, 7, dtype=cfg["dtype"],
+                                   estimate="projection"))
+    call(obs[: max(args.warmup, 1)])  # untimed warm-up call
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = call(e2e_obs)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    est_dim = model.dim_x if variant == "double-bf" else (3 if cfg["kind"] == "lorenz"
+                                                          else model.nodes)
+    e2e = {"value": ps_total / e2e_s, "unit": "particle-steps/s",
+           "h2d_bytes_per_step": int(model.dim_y * 8),
+           "d2h_bytes_per_step": int((1 if variant == "double-bf" else M) * est_dim * 8 + M * 9),
+           "api": ("paper_1407_8071_b200.islands.run_double_bootstrap" if variant == "double-bf"
+                   else "paper_1407_8071_b200.run_ensemble(variant='auxiliary')") +
+                  " (host numpy observations -> host outputs), after one untimed warm-up call"}
+    del out
+    cb = None if args.no_cpu_baseline else cpu_baseline(cfg)
+    line = {"metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"], "M": M, "N": N,
+                       "variant": variant, "euler_steps_per_obs": n_sub,
+                       "parallelism": "single GPU"},
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+            # APF: 2 propagates, 2 resamples, prepare, compose, weights, finish, estimate;
+            # double bootstrap: propagate, resample, accumulate, estimate, pool, trace
+            # (+ island select and copy every period)
+            "gpu_launches": args.steps * 9 if variant == "auxiliary" else
+            args.steps * 6 + 2 * (T // cfg["period"] - args.warmup // cfg["period"]),
+            "clocks": clocks.summary()}
+    print(json.dumps(line))
+    return 0
+
+
 def _state_bytes(model):
     """Device bytes of one fp32 particle."""
     if model.kind == "fhnnet":
@@ -566,6 +713,8 @@ def main():
         return run_reference_arm(args, cfg)
     if cfg["kind"] == "resample":
         return run_resample(args, cfg)
+    if cfg.get("variant", "bootstrap") != "bootstrap":
+        return run_variant(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -175,43 +175,61 @@ class IslandBank:
         self.lw.zero_()
 
     # -- driver ----------------------------------------------------------------------
-    def run(self, observations):
-        import torch
-
+    def start(self, observations):
+        """dbf_init (filters.py:237-242) for every island."""
         b = self.bank
         b.load_observations(observations)
         b.init()
         self.lw.zero_()
+
+    def step(self, k: int):
+        """dbf_step (filters.py:245-265) for observation k, then the pooled
+        estimate and the lnc trace of step k."""
+        import torch
+
+        b = self.bank
         s = _lib.stream_ptr()
-        events = [torch.cuda.Event(enable_timing=True) for _ in range(self.T + 1)]
-        events[0].record()
-        for k in range(self.T):
-            self.lnc_old.copy_(b.lnc)
-            b.step(k)
-            self.lnc_all.zero_()
-            self.lnc_all[self.lo:self.hi] = b.lnc
-            lw_full = self.lw
-            if self.sharded:
-                # rows / entries of other ranks' islands arrive by disjoint all-reduce
-                dist.allreduce_disjoint(self.est_isl[k])
-                dist.allreduce_disjoint(self.lnc_all)
-                lw_full = self.lw.clone()
-                mask = torch.ones(self.M, dtype=torch.bool, device=lw_full.device)
-                mask[self.lo:self.hi] = False
-                lw_full[mask] = 0.0
-                dist.allreduce_disjoint(lw_full)
-            _lib.call("pf_island_pool", _lib.ptr(self.est_isl[k]), self.est_isl.stride(1),
-                      self.M, b.model.dim_x, _lib.ptr(lw_full),
-                      _lib.c_vp(self.est.data_ptr() + k * self.est.stride(0) * 8), s)
-            _lib.call("pf_island_trace", _lib.ptr(self.lnc_all), self.M,
-                      _lib.c_vp(self.trace.data_ptr() + k * 8), s)
-            events[k + 1].record()
-        torch.cuda.synchronize()
+        self.lnc_old.copy_(b.lnc)
+        b.step(k)
+        self.lnc_all.zero_()
+        self.lnc_all[self.lo:self.hi] = b.lnc
+        lw_full = self.lw
+        if self.sharded:
+            # rows / entries of other ranks' islands arrive by disjoint all-reduce
+            dist.allreduce_disjoint(self.est_isl[k])
+            dist.allreduce_disjoint(self.lnc_all)
+            lw_full = self.lw.clone()
+            mask = torch.ones(self.M, dtype=torch.bool, device=lw_full.device)
+            mask[self.lo:self.hi] = False
+            lw_full[mask] = 0.0
+            dist.allreduce_disjoint(lw_full)
+        _lib.call("pf_island_pool", _lib.ptr(self.est_isl[k]), self.est_isl.stride(1),
+                  self.M, b.model.dim_x, _lib.ptr(lw_full),
+                  _lib.c_vp(self.est.data_ptr() + k * self.est.stride(0) * 8), s)
+        _lib.call("pf_island_trace", _lib.ptr(self.lnc_all), self.M,
+                  _lib.c_vp(self.trace.data_ptr() + k * 8), s)
+
+    def check_status(self):
+        import torch
+
+        b = self.bank
         st = torch.zeros(self.M, dtype=torch.int32, device=b.device)
         st[self.lo:self.hi] = b.status
         if self.sharded:
             dist.allreduce_disjoint(st)
         _lib.raise_status(st.cpu().numpy())
+
+    def run(self, observations):
+        import torch
+
+        self.start(observations)
+        events = [torch.cuda.Event(enable_timing=True) for _ in range(self.T + 1)]
+        events[0].record()
+        for k in range(self.T):
+            self.step(k)
+            events[k + 1].record()
+        torch.cuda.synchronize()
+        self.check_status()
         return np.array([events[i].elapsed_time(events[i + 1]) / 1e3 for i in range(self.T)])
 
     def collapse_steps(self) -> list[int]:
