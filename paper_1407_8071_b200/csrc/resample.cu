@@ -527,7 +527,7 @@ __device__ __forceinline__ void spacing_run(Key2 key, uint32_t t, int64_t i0, in
   }
 }
 
-template <typename TW>
+template <typename TW, bool FAST = false>
 __global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restrict__ logw,
                                                               int64_t N, int64_t tpf,
                                                               WideWs ws) {
@@ -543,11 +543,24 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restri
   double v[kRun];
   load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, v);
   double run = 0.0;
+  if (FAST) {
+    // w = expf(lw - tile max) * exp(tile max - max) / total (see wide2_tile_stats)
+    const double mt = ws.tmax[tile];
+    const double scale = exp(__dsub_rn(mt, m)) / total;
 #pragma unroll
-  for (int q = 0; q < kRun; ++q) {
-    const double w = r0 + q < n ? __ddiv_rn(exp(__dsub_rn(v[q], m)), total) : 0.0;
-    run = __dadd_rn(run, w);
-    v[q] = run;
+    for (int q = 0; q < kRun; ++q) {
+      const double w =
+          r0 + q < n ? static_cast<double>(expf(static_cast<float>(v[q] - mt))) * scale : 0.0;
+      run = __dadd_rn(run, w);
+      v[q] = run;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      const double w = r0 + q < n ? __ddiv_rn(exp(__dsub_rn(v[q], m)), total) : 0.0;
+      run = __dadd_rn(run, w);
+      v[q] = run;
+    }
   }
   double tot;
   const double off = __dadd_rn(ws.twoff[tile], block_exclusive_scan(run, scratch, &tot));
@@ -802,8 +815,14 @@ __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
   const double m = block_max(mx, scratch);
   double part = 0.0;
   if (m != -INFINITY) {
+    // production fp32 log-weights: fp32 exp against the TILE max; the CDF
+    // pass (wide_tile_cum<.., true>) recomputes exactly these values, so the
+    // tile totals and the in-tile CDF stay consistent to fp64 rounding
 #pragma unroll
-    for (int q = 0; q < kRun; ++q) part = __dadd_rn(part, exp(__dsub_rn(lv[q], m)));
+    for (int q = 0; q < kRun; ++q)
+      part = __dadd_rn(part, (MODE == 0 && std::is_same<TW, float>::value)
+                                 ? static_cast<double>(expf(static_cast<float>(lv[q] - m)))
+                                 : exp(__dsub_rn(lv[q], m)));
   }
   const double ssum = block_sum(part, scratch);
   double se = 0.0;
@@ -1236,7 +1255,10 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
       wide2_filter<0><<<static_cast<unsigned>(M), 1024, 0, s>>>(N, tpf, ws, collapsed, status,
                                                                lnc, keys, t);
     }
-    wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+    if (!u_tape && std::is_same<TW, float>::value)
+      wide_tile_cum<TW, true><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+    else
+      wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
   }
   if (u_tape)
     wide2_partition<1><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
