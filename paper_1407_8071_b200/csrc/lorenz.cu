@@ -16,6 +16,9 @@
 #include "common.cuh"
 #include "philox.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace pf {
 
 struct LorenzConsts {
@@ -229,6 +232,62 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
   }
 }
 
+// fp64 production kernel for SMALL banks (BASELINE cfg0: 4 x 1000 particles):
+// one warp per particle.  The Gaussian increments do not depend on the
+// state, so the 32 lanes generate a chunk of substeps' normals in parallel
+// (same Philox counters and fp64 Box-Muller as lorenz_pw_kernel<double,0>:
+// block b of a substep pair yields normals 2b, 2b+1 of the flat sequence)
+// into shared memory, and lane 0 runs the exact-order substep chain.  With
+// one thread per particle the 4000-particle bank occupied 16 SMs and was
+// bound by the serial RNG latency.  Results are bit-identical.
+constexpr int kSmallChunk = 64;  // substeps per generated chunk (even)
+constexpr int64_t kSmallBank = 1 << 15;  // particles: below this, a warp per particle
+
+__global__ void __launch_bounds__(256) lorenz_small_kernel(
+    const double *__restrict__ xin, const int32_t *__restrict__ anc, double *__restrict__ xout,
+    const double *__restrict__ y, double *__restrict__ logw, int64_t MN, int32_t N, int obs_dim,
+    LorenzConsts c, const uint32_t *__restrict__ keys, uint32_t t,
+    uint32_t *__restrict__ status) {
+  __shared__ double s_z[8][3 * kSmallChunk];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t p = blockIdx.x * 8 + w;
+  if (p >= MN) return;
+  const int64_t f = p / N;
+  const uint32_t j = static_cast<uint32_t>(p - f * N);
+  const Key2 key = load_key(keys, f);
+  double x1 = 0.0, x2 = 0.0, x3 = 0.0;
+  if (lane == 0) {
+    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+    x1 = xin[src];
+    x2 = xin[MN + src];
+    x3 = xin[2 * MN + src];
+  }
+  double *z = s_z[w];
+  for (int k0 = 0; k0 < c.n_sub; k0 += kSmallChunk) {
+    const int nk = c.n_sub - k0 < kSmallChunk ? c.n_sub - k0 : kSmallChunk;
+    const int nblocks = ((nk + 1) / 2) * 3;  // 3 Philox blocks per substep pair
+    __syncwarp();
+    for (int b = lane; b < nblocks; b += 32) {
+      const uint32_t gb = static_cast<uint32_t>((k0 >> 1) * 3 + b);  // global block index
+      const uint4 rr = philox10(make_uint4(j, t, gb, kPurposeLorenz), key);
+      const double2 g = box_muller_f64(rr.x, rr.y, rr.z, rr.w);
+      z[2 * b] = g.x;
+      z[2 * b + 1] = g.y;
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int k = 0; k < nk; ++k)
+        lorenz_substep<double>(x1, x2, x3, z[3 * k], z[3 * k + 1], z[3 * k + 2], c);
+  }
+  if (lane == 0) {
+    if (!(finite_val(x1) && finite_val(x2) && finite_val(x3))) atomicOr(status + f, PF_ST_DIVERGED);
+    xout[p] = x1;
+    xout[MN + p] = x2;
+    xout[2 * MN + p] = x3;
+    logw[p] = lorenz_loglik<double>(x1, x3, y, obs_dim, c.two_obs_var);
+  }
+}
+
 // accel.lorenz_euler_block: states (n,3) row-major, noise (n_sub, n, 3)
 __global__ void lorenz_block_op_kernel(const double *__restrict__ st,
                                        const double *__restrict__ nz, int64_t n,
@@ -243,6 +302,13 @@ __global__ void lorenz_block_op_kernel(const double *__restrict__ st,
   out[3 * i] = x1;
   out[3 * i + 1] = x2;
   out[3 * i + 2] = x3;
+}
+
+// PF_LORENZ_KERNEL=thread keeps one thread per particle for small banks too
+// (comparison tests)
+static bool force_thread_kernel() {
+  const char *e = std::getenv("PF_LORENZ_KERNEL");
+  return e && std::strcmp(e, "thread") == 0;
 }
 
 static LorenzConsts make_consts(const pf_lorenz_params *p) {
@@ -312,6 +378,9 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
     if (z_tape)
       lorenz_pw_kernel<double, 1><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
                                                        c, keys, t, z_tape, status);
+    else if (MN <= kSmallBank && !force_thread_kernel())
+      lorenz_small_kernel<<<grid_for(MN, 8), 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32,
+                                                          p->obs_dim, c, keys, t, status);
     else
       lorenz_pw_kernel<double, 0><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
                                                        c, keys, t, z_tape, status);
