@@ -57,6 +57,9 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     for (auto &x : evs.e) cudaEventCreate(&x);
     ev = evs.e.data();
   }
+  // planar states (x[d*MN + p]): the estimate is fused into the resampler
+  const bool planar = d->model == PF_MODEL_LORENZ || d->model == PF_MODEL_HMM ||
+                      d->model == PF_MODEL_LGM;
   for (int32_t i = 0; i < n_steps; ++i) {
     const int32_t k = k0 + i;
     const uint32_t t = static_cast<uint32_t>(k + 1);
@@ -84,15 +87,24 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                            d->keys, t, nullptr, d->status, stream);
     if (ev) cudaEventRecord(ev[3 * i + 1], s);
     if (rc) return rc;
-    rc = pf_segmented_resample_ex(d->dtype, d->logw, d->M, d->N, nullptr, d->keys, t, d->anc,
-                                  d->lnc, d->collapsed, d->status, d->ws, d->ws_bytes, nullptr,
-                                  nullptr, 0, 0u, stream);
-    if (rc) return rc;
     double *est = d->est + static_cast<int64_t>(k) * d->est_step_stride + d->est_offset;
-    const int64_t est_f = d->est_stride_f ? d->est_stride_f : d->est_dim;
-    rc = pf_filter_estimate_strided(d->dtype, xout, d->est_stride_p, d->est_stride_d, d->est_dim,
-                                    d->anc, d->M, d->N, est, est_f, stream);
+    const int64_t est_f0 = d->est_stride_f ? d->est_stride_f : d->est_dim;
+    bool fused = false;
+    if (planar && d->est_stride_p == 1 && d->est_stride_d == MN)
+      rc = segmented_resample_fused(d->dtype, d->logw, d->M, d->N, d->keys, t, d->anc, d->lnc,
+                                    d->collapsed, d->status, d->ws, d->ws_bytes, xout,
+                                    d->est_dim, est, est_f0, s, &fused);
+    else
+      rc = pf_segmented_resample_ex(d->dtype, d->logw, d->M, d->N, nullptr, d->keys, t, d->anc,
+                                    d->lnc, d->collapsed, d->status, d->ws, d->ws_bytes, nullptr,
+                                    nullptr, 0, 0u, stream);
     if (rc) return rc;
+    const int64_t est_f = est_f0;
+    if (!fused) {
+      rc = pf_filter_estimate_strided(d->dtype, xout, d->est_stride_p, d->est_stride_d,
+                                      d->est_dim, d->anc, d->M, d->N, est, est_f, stream);
+      if (rc) return rc;
+    }
     if (d->model == PF_MODEL_FHNNET && d->est_bits > 0) {
       const int32_t nodes = d->fhnnet->J * d->fhnnet->J;
       rc = pf_bits_estimate(d->q[cur ^ 1], nodes, d->est_bits, d->anc, d->M, d->N,

@@ -61,6 +61,14 @@ template <> struct Ar<float> {
 __device__ __forceinline__ bool finite_val(float x) { return isfinite(x); }
 __device__ __forceinline__ bool finite_val(double x) { return isfinite(x); }
 
+// production resample + fused posterior mean of planar states (resample.cu,
+// used by the native bank driver bank.cu)
+int segmented_resample_fused(pf_dtype dtype, const void *logw, int64_t M, int64_t N,
+                             const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
+                             uint8_t *collapsed, uint32_t *status, void *ws, size_t ws_bytes,
+                             const void *x, int dim, double *est, int64_t est_stride,
+                             cudaStream_t s, bool *fused);
+
 inline unsigned grid_for(int64_t n, int block) {
   return static_cast<unsigned>((n + block - 1) / block);
 }

@@ -137,14 +137,52 @@ __device__ __forceinline__ I advance_to(F c, I k, I n, double x) {
   return lo;
 }
 
+// Fused posterior mean of the resampled set (filters.py:188) for planar
+// states (Lorenz, HMM, linear-Gaussian; dim <= 8): the resampler already
+// holds every particle's ancestor, so it sums x[d][anc] and writes the
+// estimate - no separate pass over the particles.  Fixed order: per thread
+// in particle order, warps by shuffle tree, warps in index order.
+struct EstFuse {
+  const void *x;  // planes x[d*mn + row] of the propagated particles (NULL: off)
+  int dim;
+  int64_t mn;
+  double *est;  // filter f's row at est + f*stride
+  int64_t stride;
+};
+constexpr int kEstMaxDim = 8;
+
+template <int THREADS>
+__device__ __forceinline__ void est_block_write(double (&acc)[kEstMaxDim], int dim,
+                                                double *s_red, double *dst, double invN) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 0; d < kEstMaxDim; ++d) {
+    if (d >= dim) continue;
+    double v = acc[d];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+    if (lane == 0) s_red[warp * kEstMaxDim + d] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < dim) {
+    double sum = s_red[threadIdx.x];
+    for (int w = 1; w < THREADS / 32; ++w) sum = __dadd_rn(sum, s_red[w * kEstMaxDim + threadIdx.x]);
+    dst[threadIdx.x] = __dmul_rn(sum, invN);
+  }
+}
+
 template <typename TW, int MODE, int THREADS, int IPT, bool GATHER>
 __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
     const TW *__restrict__ logw, int32_t N, const double *__restrict__ u_tape,
     const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
     double *__restrict__ lnc, uint8_t *__restrict__ collapsed, uint32_t *__restrict__ status,
-    const float *__restrict__ gx_in, float *__restrict__ gx_out, int gdims, int64_t gMN) {
+    const float *__restrict__ gx_in, float *__restrict__ gx_out, int gdims, int64_t gMN,
+    EstFuse ef) {
   extern __shared__ double s_cum[];  // THREADS * IPT slots, thread-major
   __shared__ double scratch[33];
+  __shared__ double s_red[(THREADS / 32) * kEstMaxDim];
+  const TW *ex = static_cast<const TW *>(ef.x);
+  const double invN = 1.0 / static_cast<double>(N);
   const int tid = threadIdx.x;
   const int64_t f = blockIdx.x;
   const int64_t base = f * N;
@@ -184,11 +222,18 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
   if (nan || m == -INFINITY) {
     // NaN -> ValueError on the host; total underflow -> collapse: identity
     // ancestors, lnc unchanged (filters.py:105-109)
+    double acc[kEstMaxDim] = {};
     for (int i = tid; i < N; i += blockDim.x) {
       anc[base + i] = static_cast<int32_t>(base + i);
       if (GATHER)
         for (int d = 0; d < gdims; ++d) gx_out[d * gMN + base + i] = gx_in[d * gMN + base + i];
+      if (ex) {
+#pragma unroll
+        for (int d = 0; d < kEstMaxDim; ++d)
+          if (d < ef.dim) acc[d] = __dadd_rn(acc[d], static_cast<double>(ex[d * ef.mn + base + i]));
+      }
     }
+    if (ex) est_block_write<THREADS>(acc, ef.dim, s_red, ef.est + f * ef.stride, invN);
     if (tid == 0) {
       collapsed[f] = nan ? 0 : 1;
       if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
@@ -326,6 +371,18 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
         }
       }
     }
+  }
+  if (ex) {
+    double acc[kEstMaxDim] = {};
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+      if (i0 + q < N) {
+        const int64_t row = s_anc[q * THREADS + tid];
+#pragma unroll
+        for (int d = 0; d < kEstMaxDim; ++d)
+          if (d < ef.dim) acc[d] = __dadd_rn(acc[d], static_cast<double>(ex[d * ef.mn + row]));
+      }
+    est_block_write<THREADS>(acc, ef.dim, s_red, ef.est + f * ef.stride, invN);
   }
   if (tid == 0) {
     collapsed[f] = 0;
@@ -1175,8 +1232,10 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
                            const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
                            uint8_t *collapsed, uint32_t *status, void *ws_v, size_t ws_bytes,
                            cudaStream_t s, const float *gx_in = nullptr,
-                           float *gx_out = nullptr, int gdims = 0, uint32_t flags = 0) {
+                           float *gx_out = nullptr, int gdims = 0, uint32_t flags = 0,
+                           const EstFuse *ef = nullptr, bool *fused = nullptr) {
   const TW *logw = static_cast<const TW *>(logw_v);
+  if (fused) *fused = false;
   const bool exact = flags & PF_RS_REFERENCE_ORDER;
   if (N <= kBankMaxN && exact) {
     auto kern = u_tape ? resample_bank_exact_kernel<TW, 1> : resample_bank_exact_kernel<TW, 0>;
@@ -1192,7 +1251,8 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
   }
   if (N <= kBankMaxN) {
     using K = void (*)(const TW *, int32_t, const double *, const uint32_t *, uint32_t, int32_t *,
-                       double *, uint8_t *, uint32_t *, const float *, float *, int, int64_t);
+                       double *, uint8_t *, uint32_t *, const float *, float *, int, int64_t,
+                       EstFuse);
     K kern;
     int threads;
     const bool g = gx_in != nullptr;
@@ -1218,9 +1278,14 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
+    EstFuse e{};
+    if (ef && ef->x && ef->dim >= 1 && ef->dim <= kEstMaxDim) {
+      e = *ef;
+      if (fused) *fused = true;
+    }
     kern<<<static_cast<unsigned>(M), threads, smem, s>>>(logw, static_cast<int32_t>(N), u_tape,
                                                          keys, t, anc, lnc, collapsed, status,
-                                                         gx_in, gx_out, gdims, M * N);
+                                                         gx_in, gx_out, gdims, M * N, e);
     return check_launch("pf_segmented_resample(bank)");
   }
   WideWs ws;
@@ -1326,6 +1391,24 @@ __global__ void resample_indices_kernel(const double *__restrict__ cum, int64_t 
   if (j >= m) return;
   const int64_t k = lower_bound_f64_64(cum, n, u[j]);
   idx[j] = k < n - 1 ? k : n - 1;
+}
+
+// Production resample that also writes the posterior mean of the resampled
+// set of planar states when the bank kernel serves (N <= kBankMaxN, dim <= 8);
+// *fused reports whether it did (bank.cu runs the standalone pass otherwise).
+int segmented_resample_fused(pf_dtype dtype, const void *logw, int64_t M, int64_t N,
+                             const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
+                             uint8_t *collapsed, uint32_t *status, void *ws, size_t ws_bytes,
+                             const void *x, int dim, double *est, int64_t est_stride,
+                             cudaStream_t s, bool *fused) {
+  PF_REQUIRE(logw && anc && lnc && collapsed && status && keys && fused,
+             "segmented_resample_fused: null");
+  const EstFuse ef{x, dim, M * N, est, est_stride};
+  if (dtype == PF_F64)
+    return launch_resample<double>(logw, M, N, nullptr, keys, t, anc, lnc, collapsed, status, ws,
+                                   ws_bytes, s, nullptr, nullptr, 0, 0u, &ef, fused);
+  return launch_resample<float>(logw, M, N, nullptr, keys, t, anc, lnc, collapsed, status, ws,
+                                ws_bytes, s, nullptr, nullptr, 0, 0u, &ef, fused);
 }
 
 }  // namespace pf

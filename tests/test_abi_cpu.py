@@ -138,3 +138,13 @@ def test_ctypes_struct_layouts_match_c(tmp_path):
         assert int(got[cname]) == ctypes.sizeof(cls), cname
         for fname, _ in cls._fields_:
             assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, (cname, fname)
+
+
+def test_library_binds_every_symbol_now(lib):
+    """RTLD_NOW load: every symbol the library references resolves (catches an
+    internal C++ entry point declared but not linked in)."""
+    import ctypes
+
+    from paper_1407_8071_b200 import _lib
+
+    ctypes.CDLL(_lib.LIB_PATH, mode=os.RTLD_NOW)

@@ -551,3 +551,27 @@ def test_small_bank_warp_kernel_bit_identical(monkeypatch):
     monkeypatch.setenv("PF_LORENZ_KERNEL", "thread")
     b = pf.run_filter(gm3, obs[:, :1], "bootstrap", 100, 2)
     assert a.same_result(b)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_native_fused_estimate_matches_separate_pass(dtype):
+    """pf_bank_run fuses the planar-state posterior mean into the resampler;
+    it agrees with the standalone pf_filter_estimate pass of the per-step
+    path to fp64 rounding, and states / lnc are identical."""
+    truth0, _, obs = orc.lorenz_truth(seed=12, n_obs=6)
+    gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(truth0), prior_var=1.0)
+    keys = pf.philox.filter_keys(3, 5)
+    res = []
+    for native in (True, False):
+        bank = pf.FilterBank(gm, 5, 333, keys, len(obs), dtype=dtype)
+        bank.load_observations(obs)
+        bank.init()
+        if not native:
+            bank.kernel_events = (torch.cuda.Event(), torch.cuda.Event())
+        bank.run()
+        torch.cuda.synchronize()
+        res.append((bank.est.cpu().numpy(), bank.lnc_tr.cpu().numpy(), bank.particles()))
+    assert norm_rel(res[0][0], res[1][0]) < 1e-13
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][2], res[1][2])
