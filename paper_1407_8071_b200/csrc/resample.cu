@@ -85,28 +85,10 @@ __device__ __forceinline__ double block_exclusive_scan(double v, double *scratch
 // ---- bank path: one CTA per filter --------------------------------------
 // Thread t owns the IPT consecutive particles [t*IPT, t*IPT+IPT): weights,
 // CDF and sorted uniforms live in registers, per-thread sums are combined
-// with one block scan, and only the CDF goes to shared memory for the merge
-// (binary search for the thread's first uniform, then a forward walk over
-// its sorted run).  Shared CDF layout is "thread-major" (element i at
-// (i % IPT) * THREADS + i / IPT) so the per-thread stores are conflict-free.
+// with one block scan; the CDF and the uniforms go to shared memory in a
+// "thread-major" layout (element i at (i % IPT) * THREADS + i / IPT, so the
+// per-thread stores are conflict-free) for the merge path.
 // GATHER fuses the ancestor gather of a fp32 planar state (cfg1).
-template <int THREADS, int IPT>
-__device__ __forceinline__ int cdf_slot(int i) {
-  return (i % IPT) * THREADS + i / IPT;
-}
-
-template <int THREADS, int IPT>
-__device__ __forceinline__ int lower_bound_tm(const double *c, int n, double x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (c[cdf_slot<THREADS, IPT>(mid)] < x)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
 
 // Forward search from k for the first index >= k with c(i) >= x (n if none):
 // a short linear probe, then galloping + binary search.  Keeps the merge
