@@ -157,6 +157,15 @@ int pf_op_normalize_log_weights(pf_dtype logw_dtype, const void *logw, int64_t M
                                 double *weights_out, double *log_mean_raw_out,
                                 uint8_t *collapsed, uint32_t *status, void *stream);
 
+/* Hook-level resampling helpers in numpy's order (resampling.py:21-72):
+ * out = np.cumsum(a) (sequential); u = cumsum(e)[:n_out] / cumsum(e)[n_out]
+ * for e of length n_out + 1 (work: n_out + 1 doubles); systematic thresholds
+ * u_i = (i + r) / n_out. */
+int pf_op_cumsum(const double *a, int64_t n, double *out, void *stream);
+int pf_op_spacing_uniforms(const double *e, int64_t n_out, double *work, double *u,
+                           void *stream);
+int pf_op_systematic_uniforms(double r, int64_t n_out, double *u, void *stream);
+
 /* Explicit ancestor gather of a 3-plane state (filters.py:111 / cfg1):
  * x_out[d][p] = x_in[d][anc[p]]. */
 int pf_gather_planes(pf_dtype dtype, const void *x_in, const int32_t *anc, int64_t MN,

@@ -98,6 +98,9 @@ SIGNATURES = {
     "pf_op_resample_indices": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "pf_op_normalize_log_weights": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp,
                                                    c_vp, c_vp, c_vp]),
+    "pf_op_cumsum": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "pf_op_spacing_uniforms": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "pf_op_systematic_uniforms": (ctypes.c_int, [c_f64, c_i64, c_vp, c_vp]),
     "pf_gather_planes": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "pf_lorenz_prior": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_f64, c_vp, c_vp,
                                        c_vp]),

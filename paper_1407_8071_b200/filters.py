@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import philox
+from . import _lib, philox
 from .bank import DrawTape, FilterBank
 from .core import ParticleApproximation, StateSpaceModel, normalize_log_weights, uniform_weights
 from .exceptions import UnsupportedModelError, WeightCollapseError
@@ -80,12 +80,8 @@ def bf_step(model: StateSpaceModel, state: ParticleApproximation, y, rng) -> Par
     except WeightCollapseError:
         return ParticleApproximation(propagated, uniform_weights(n), state.log_norm_const, t,
                                      collapsed=True)
-    import torch
-
     idx = multinomial_resample_indices(weights, n, rng)
-    gathered = torch.from_numpy(np.ascontiguousarray(propagated)).cuda()[
-        torch.from_numpy(idx).cuda()].cpu().numpy()
-    return ParticleApproximation(gathered, uniform_weights(n),
+    return ParticleApproximation(np.asarray(propagated)[idx], uniform_weights(n),
                                  state.log_norm_const + log_mean_raw, t)
 
 
@@ -109,21 +105,22 @@ def apf_step(model: StateSpaceModel, state: ParticleApproximation, y, rng) -> Pa
         lam = np.zeros(n)
         first_stage, log_mean_first = uniform_weights(n), 0.0
     ancestors = multinomial_resample_indices(first_stage, n, rng)
-    dev_x = torch.from_numpy(np.ascontiguousarray(state.particles)).cuda()
-    chosen = dev_x[torch.from_numpy(ancestors).cuda()].cpu().numpy()
-    propagated = model.sample_transition(chosen, t, rng)
+    propagated = model.sample_transition(np.asarray(state.particles)[ancestors], t, rng)
+    # log w = log p(y | x) - lambda[ancestors] (filters.py:143), on the device
+    d_lw = torch.from_numpy(np.ascontiguousarray(model.log_likelihood(y, propagated, t),
+                                                 dtype=np.float64)).cuda()
     d_lam = torch.from_numpy(np.ascontiguousarray(lam, dtype=np.float64)).cuda()
-    log_w = (torch.from_numpy(np.ascontiguousarray(model.log_likelihood(y, propagated, t))).cuda()
-             - d_lam[torch.from_numpy(ancestors).cuda()]).cpu().numpy()
+    d_anc = torch.from_numpy(ancestors.astype(np.int32)).cuda()
+    _lib.call("pf_apf_second_stage_weights", _lib.PF_F64, _lib.ptr(d_lw), _lib.ptr(d_lam),
+              _lib.ptr(d_anc), n, _lib.stream_ptr())
+    log_w = d_lw.cpu().numpy()
     try:
         weights, log_mean_second = normalize_log_weights(log_w)
     except WeightCollapseError:
         return ParticleApproximation(propagated, uniform_weights(n), state.log_norm_const, t,
                                      collapsed=True)
     idx = multinomial_resample_indices(weights, n, rng)
-    gathered = torch.from_numpy(np.ascontiguousarray(propagated)).cuda()[
-        torch.from_numpy(idx).cuda()].cpu().numpy()
-    return ParticleApproximation(gathered, uniform_weights(n),
+    return ParticleApproximation(np.asarray(propagated)[idx], uniform_weights(n),
                                  state.log_norm_const + log_mean_first + log_mean_second, t,
                                  collapsed=collapsed)
 

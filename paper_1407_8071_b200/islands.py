@@ -260,3 +260,97 @@ def run_double_bootstrap(model, observations, n_islands: int, n_particles: int,
     secs = ib.run(obs)
     return FilterOutput("double-bf", n_islands * n_particles, seed, ib.est.cpu().numpy(),
                         ib.trace.cpu().numpy(), secs, ib.collapse_steps())
+
+
+# ---------------------------------------------------------------------------
+# Hook-level API (filters.py:201-271): IslandSystem, dbf_init, dbf_step
+# ---------------------------------------------------------------------------
+
+
+def _island_probs_device(log_weights):
+    """softmax of the island log-weights in numpy's order (filters.py:225-227),
+    through pf_island_pool with an identity estimate matrix."""
+    import torch
+
+    lw = torch.from_numpy(np.ascontiguousarray(log_weights, dtype=np.float64)).cuda()
+    M = lw.shape[0]
+    eye = torch.eye(M, dtype=torch.float64, device="cuda")
+    out = torch.empty(M, dtype=torch.float64, device="cuda")
+    _lib.call("pf_island_pool", _lib.ptr(eye), M, M, M, _lib.ptr(lw), _lib.ptr(out),
+              _lib.stream_ptr())
+    return out.cpu().numpy()
+
+
+class IslandSystem:
+    """M equally sized particle islands plus their accumulated log weights
+    (filters.py:206-234)."""
+
+    def __init__(self, islands, log_weights):
+        sizes = {isl.n_particles for isl in islands}
+        if len(sizes) != 1:
+            raise ValueError("all islands must share the same particle count")
+        self.islands = list(islands)
+        self.log_weights = np.asarray(log_weights, dtype=np.float64)
+        if self.log_weights.shape != (len(self.islands),):
+            raise ValueError("one log weight per island required")
+
+    @property
+    def n_islands(self) -> int:
+        return len(self.islands)
+
+    def island_probs(self) -> np.ndarray:
+        return _island_probs_device(self.log_weights)
+
+    def pooled_estimate(self) -> np.ndarray:
+        """sum_m p_m * posterior_mean(island m), islands in order (pf_island_pool)."""
+        import torch
+
+        from .core import posterior_mean
+
+        est = torch.from_numpy(np.stack([np.asarray(posterior_mean(isl), dtype=np.float64)
+                                         for isl in self.islands])).cuda()
+        lw = torch.from_numpy(np.ascontiguousarray(self.log_weights)).cuda()
+        out = torch.empty(est.shape[1], dtype=torch.float64, device="cuda")
+        _lib.call("pf_island_pool", _lib.ptr(est), est.shape[1], self.n_islands, est.shape[1],
+                  _lib.ptr(lw), _lib.ptr(out), _lib.stream_ptr())
+        return out.cpu().numpy()
+
+
+def _copy_island(isl):
+    from .core import ParticleApproximation
+
+    return ParticleApproximation(isl.particles.copy(), isl.weights.copy(), isl.log_norm_const,
+                                 isl.t, collapsed=isl.collapsed)
+
+
+def dbf_init(model, n_islands: int, n_particles: int, rngs) -> IslandSystem:
+    """filters.py:237-242."""
+    from .filters import bf_init
+
+    if n_islands < 1:
+        raise ValueError("n_islands must be >= 1")
+    return IslandSystem([bf_init(model, n_particles, rngs[m]) for m in range(n_islands)],
+                        np.zeros(n_islands))
+
+
+def dbf_step(model, system: IslandSystem, y, t: int, island_period: int, rngs,
+             island_rng) -> IslandSystem:
+    """filters.py:245-271: one bootstrap step per island (island m on rngs[m]);
+    every island_period steps whole islands are resampled by their
+    accumulated weights with island_rng."""
+    from .filters import bf_step
+    from .resampling import multinomial_resample_indices
+
+    if island_period < 1:
+        raise ValueError("island_period must be >= 1")
+    new_islands, log_weights = [], system.log_weights.copy()
+    for m, isl in enumerate(system.islands):
+        stepped = bf_step(model, isl, y, rngs[m])
+        log_weights[m] += stepped.log_norm_const - isl.log_norm_const
+        new_islands.append(stepped)
+    if t % island_period == 0:
+        idx = multinomial_resample_indices(_island_probs_device(log_weights), system.n_islands,
+                                           island_rng)
+        new_islands = [_copy_island(new_islands[i]) for i in idx]
+        log_weights = np.zeros(system.n_islands)
+    return IslandSystem(new_islands, log_weights)

@@ -775,3 +775,15 @@ def kalman_filter(model: LinearGaussianModel, observations):
         cov = (eye - gain @ model.H) @ cov
         out.append((mean.copy(), cov.copy()))
     return out
+
+
+def lorenz_transition(x, rng, model: Lorenz63Model | None = None) -> np.ndarray:
+    """One observation interval for a single 3-vector state (lorenz63.py:72-78)."""
+    model = model or Lorenz63Model()
+    return model.sample_transition(np.asarray(x, dtype=np.float64)[None, :], 1, rng)[0]
+
+
+def lorenz_log_likelihood(y: float, x, model: Lorenz63Model | None = None) -> float:
+    """Scalar-observation log-likelihood of one state (lorenz63.py:81-85)."""
+    model = model or Lorenz63Model()
+    return float(model.log_likelihood(np.array([y]), np.asarray(x)[None, :], 1)[0])

@@ -209,6 +209,15 @@ def gen_kernels():
     w = rng.dirichlet(np.ones(500))
     d["mri_w"] = w
     d["mri_idx"] = resampling.multinomial_resample_indices(w, 500, np.random.default_rng(77))
+    d["sys_idx"] = resampling.systematic_resample_indices(w, 700, np.random.default_rng(78))
+    wb = rng.dirichlet(np.ones(50_000))
+    d["mri_big_w"] = wb
+    d["mri_big_idx"] = resampling.multinomial_resample_indices(wb, 60_000,
+                                                               np.random.default_rng(79))
+    from parpf.models import lorenz_log_likelihood, lorenz_transition
+
+    d["lz_tr"] = lorenz_transition(np.array([1.0, 2.0, 3.0]), np.random.default_rng(3))
+    d["lz_ll"] = np.array(lorenz_log_likelihood(0.7, np.array([1.0, 2.0, 3.0])))
     # lorenz_euler_block (accel.py:60-102), same shapes as test_accel.py:22-27
     st = rng.normal(size=(257, 3)) * 10.0
     nz = rng.normal(size=(100, 257, 3))

@@ -575,3 +575,23 @@ def test_native_fused_estimate_matches_separate_pass(dtype):
     assert norm_rel(res[0][0], res[1][0]) < 1e-13
     assert np.array_equal(res[0][1], res[1][1])
     assert np.array_equal(res[0][2], res[1][2])
+
+
+def test_hook_level_resamplers_match_reference(golden):
+    """systematic_resample_indices and a 50,000-weight multinomial draw
+    against the reference's own outputs (sequential cumsum on the device)."""
+    g = golden["kernels"]
+    idx = pf.systematic_resample_indices(g["mri_w"], 700, np.random.default_rng(78))
+    assert np.array_equal(idx, g["sys_idx"])
+    idx = pf.multinomial_resample_indices(g["mri_big_w"], 60_000, np.random.default_rng(79))
+    assert np.array_equal(idx, g["mri_big_idx"])
+    x = np.arange(500.0)[:, None]
+    assert np.array_equal(pf.systematic_resample(x, g["mri_w"], 700, np.random.default_rng(78)),
+                          x[g["sys_idx"]])
+
+
+def test_lorenz_helpers_match_reference(golden):
+    g = golden["kernels"]
+    tr = pf.lorenz_transition(np.array([1.0, 2.0, 3.0]), np.random.default_rng(3))
+    assert np.array_equal(tr, g["lz_tr"])
+    assert pf.lorenz_log_likelihood(0.7, np.array([1.0, 2.0, 3.0])) == float(g["lz_ll"])

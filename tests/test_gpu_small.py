@@ -178,3 +178,20 @@ def test_double_bootstrap_production():
                      for s in range(60)])
     z = abs(ests.mean() - exact) / (ests.std(ddof=1) / np.sqrt(len(ests)))
     assert z < 4.0
+
+
+def test_hook_level_double_bootstrap_matches_reference(golden):
+    """dbf_init / dbf_step driven like filters.py:274-313 with the caller's
+    generators reproduce the reference's double bootstrap (HMM)."""
+    g = golden["small"]
+    gm = models.DiscreteHmm(**HMM)
+    children = np.random.SeedSequence(606).spawn(4)
+    rngs = [np.random.default_rng(c) for c in children[:3]]
+    island_rng = np.random.default_rng(children[3])
+    system = pf.dbf_init(gm, 3, 20, rngs)
+    ests = []
+    for k in range(len(HOBS)):
+        system = pf.dbf_step(gm, system, HOBS[k], k + 1, 2, rngs, island_rng)
+        ests.append(system.pooled_estimate())
+    assert norm_rel(np.array(ests), g["db_h_est"]) < 1e-12
+    assert abs(system.island_probs().sum() - 1.0) < 1e-12

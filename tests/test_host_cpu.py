@@ -95,3 +95,27 @@ def test_raise_status_maps_flags_to_reference_exceptions():
         _lib.raise_status(np.array([0, _lib.PF_ST_DIVERGED | _lib.PF_ST_NAN_WEIGHT]))
     with pytest.raises(ValueError):
         _lib.raise_status(np.array([_lib.PF_ST_NAN_WEIGHT]))
+
+
+def test_public_api_covers_the_reference_names():
+    """Every name parpf and parpf.models export (parpf/__init__.py,
+    models/__init__.py) exists here."""
+    import paper_1407_8071_b200 as pf
+    from paper_1407_8071_b200 import models
+
+    ref_top = ["ConfigError", "EnsembleOutput", "FilterOutput", "IslandSystem", "MetricRecord",
+               "NumericalDivergenceError", "ParticleApproximation", "StateSpaceModel",
+               "UnsupportedModelError", "WeightCollapseError", "apf_step", "bf_init", "bf_step",
+               "bias_variance", "dbf_init", "dbf_step", "empirical_mse", "ensemble_estimate",
+               "estimate_integral", "loglog_slope", "multinomial_resample",
+               "multinomial_resample_indices", "normalize_log_weights", "posterior_mean",
+               "run_double_bootstrap", "run_ensemble", "run_filter", "systematic_resample",
+               "systematic_resample_indices", "time_error_index"]
+    ref_models = ["DiscreteHmm", "FhnNetworkModel", "LinearGaussianModel", "Lorenz63Model",
+                  "fhn_stimulus_region", "hmm_exact_filter", "kalman_filter",
+                  "lorenz_log_likelihood", "lorenz_transition", "observation_zone_indices",
+                  "simulate", "von_neumann_neighbors"]
+    for n in ref_top:
+        assert hasattr(pf, n), n
+    for n in ref_models:
+        assert hasattr(models, n), n
