@@ -556,10 +556,12 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   fc.sig_w = float(c.sig_w);
   fc.obs_coef = c.obs_coef;
   if (tape)
-    return launch_fhn_fast_t<30, 50, true, 3, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+    return launch_fhn_fast_t<30, 50, true, 3, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                  keys, t, tape, status, s);
   // production: 2 particles per CTA iteration, 3 resident CTAs/SM (80 regs)
-  return launch_fhn_fast_t<30, 50, false, 3, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+  // one particle per CTA, 3 CTAs/SM: measured 46.1 ms vs 46.5 ms for two
+  // particles per CTA and 46.9-48.4 ms for 4-5 CTAs/SM (cfg4)
+  return launch_fhn_fast_t<30, 50, false, 3, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                 keys, t, tape, status, s);
 }
 

@@ -221,8 +221,7 @@ def test_fhn_filter_matches_golden(golden):
 
 @pytest.mark.parametrize("M,N", [(2, 16), (1, 7)])
 def test_fhn_one_interval_fp32_within_1e4(golden, M, N):
-    """The fp32 production kernel (tape-fed), incl. an odd particle count
-    (the 2-particles-per-CTA tail)."""
+    """The fp32 production kernel (tape-fed), incl. an odd particle count."""
     g = golden["fhn"]
     om = orc.FhnConfigModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
     gm = pf.FhnLatticeModel(stim_row=int(g["stim"][0]), stim_col=int(g["stim"][1]))
