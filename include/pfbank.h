@@ -366,6 +366,9 @@ typedef struct pf_bank_desc {
   const pf_hmm_params *hmm; /* host */
   const pf_lgm_params *lgm; /* host */
   float *step_ms; /* host (n_steps) or NULL: whole-interval durations (waits like prop_ms) */
+  void **events;  /* host array of 3*n_steps caller-created timing cudaEvent_t, or NULL:
+                     recorded at each interval's start, after its propagate kernel and at
+                     its end; nothing waits (the caller reads the times) */
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);

@@ -76,7 +76,7 @@ class BankDesc(ctypes.Structure):
                 ("fhnnet", ctypes.POINTER(FhnNetParams)), ("q", c_vp * 2),
                 ("forcing_mask", c_vp), ("est_stride_f", c_i64), ("est_bits", c_i32),
                 ("hmm", ctypes.POINTER(HmmParams)), ("lgm", ctypes.POINTER(LgmParams)),
-                ("step_ms", ctypes.POINTER(ctypes.c_float))]
+                ("step_ms", ctypes.POINTER(ctypes.c_float)), ("events", c_vp)]
 
 
 PF_MODEL_LORENZ = 0

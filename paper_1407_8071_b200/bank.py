@@ -310,23 +310,61 @@ class FilterBank:
             raise RuntimeError("run_native: production bootstrap banks only")
         if self._desc is None:
             self._desc = self._bank_desc()
+        timed = (time_propagate or time_steps) and n_steps > 0
+        pool = self.__dict__.get("_event_pools", {}).get(3 * n_steps) if timed else None
         ms = sm = None
-        if time_propagate and n_steps > 0:
-            ms = (ctypes.c_float * n_steps)()
-            self._desc.prop_ms = ctypes.cast(ms, ctypes.POINTER(ctypes.c_float))
-        if time_steps and n_steps > 0:
-            sm = (ctypes.c_float * n_steps)()
-            self._desc.step_ms = ctypes.cast(sm, ctypes.POINTER(ctypes.c_float))
+        if pool is not None:  # prepared events: recorded by the driver, no host wait
+            evs, handles = pool
+            self._desc.events = ctypes.cast(handles, ctypes.c_void_p)
+        elif timed:  # the driver creates the events and waits for the last one
+            if time_propagate:
+                ms = (ctypes.c_float * n_steps)()
+                self._desc.prop_ms = ctypes.cast(ms, ctypes.POINTER(ctypes.c_float))
+            if time_steps:
+                sm = (ctypes.c_float * n_steps)()
+                self._desc.step_ms = ctypes.cast(sm, ctypes.POINTER(ctypes.c_float))
         try:
             _lib.call("pf_bank_run", self._desc, k0, n_steps, self.cur,
                       1 if self.steps_done > 0 else 0, _lib.stream_ptr())
         finally:
+            self._desc.events = None
             self._desc.prop_ms = None
             self._desc.step_ms = None
         self.cur ^= n_steps & 1
         self.steps_done += n_steps
-        self.last_step_ms = None if sm is None else np.frombuffer(sm, dtype=np.float32).copy()
-        return None if ms is None else list(ms)
+        self.last_step_ms = None
+        if not timed:
+            return None
+        if pool is None:
+            if sm is not None:
+                self.last_step_ms = np.frombuffer(sm, dtype=np.float32).copy()
+            return list(ms) if ms is not None else None
+        evs[3 * n_steps - 1].synchronize()
+        if time_steps:
+            self.last_step_ms = np.array([evs[3 * i].elapsed_time(evs[3 * i + 2])
+                                          for i in range(n_steps)], dtype=np.float32)
+        return [evs[3 * i].elapsed_time(evs[3 * i + 1]) for i in range(n_steps)] \
+            if time_propagate else None
+
+    def prepare_timing(self, n_steps: int):
+        """Create the timing events of an n_steps run_native call ahead of time
+        (keeps their creation out of a timed region)."""
+        self._event_pool(3 * n_steps)
+
+    def _event_pool(self, n):
+        """n timing events and their raw handles (ctypes array), created once
+        per bank and size (each recorded once so the driver handle exists)."""
+        import ctypes
+
+        import torch
+
+        pools = self.__dict__.setdefault("_event_pools", {})
+        if n not in pools:
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+            for e in evs:
+                e.record()
+            pools[n] = (evs, (ctypes.c_void_p * n)(*[e.cuda_event for e in evs]))
+        return pools[n]
 
     def step(self, k: int):
         if self.obs is None:

@@ -52,7 +52,10 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     }
   } evs;
   cudaEvent_t *ev = nullptr;
-  if ((d->prop_ms || d->step_ms) && n_steps > 0) {
+  if (d->events && n_steps > 0) {
+    // caller-owned, pre-created timing events: record only, no host wait
+    ev = reinterpret_cast<cudaEvent_t *>(d->events);
+  } else if ((d->prop_ms || d->step_ms) && n_steps > 0) {
     evs.e.resize(3 * static_cast<size_t>(n_steps));
     for (auto &x : evs.e) cudaEventCreate(&x);
     ev = evs.e.data();
@@ -123,7 +126,7 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     cur ^= 1;
   }
   (void)MN;
-  if (ev) {
+  if (ev && !d->events) {
     cudaEventSynchronize(ev[3 * n_steps - 1]);
     for (int32_t i = 0; i < n_steps; ++i) {
       if (d->prop_ms) cudaEventElapsedTime(&d->prop_ms[i], ev[3 * i], ev[3 * i + 1]);
