@@ -566,6 +566,30 @@ __device__ __forceinline__ void spacing_run(Key2 key, uint32_t t, int64_t i0, in
   }
 }
 
+// Gamma(a, 1) by Marsaglia & Tsang (a >= 1), fp64, counter-based: attempt
+// `it` of tile `tile` uses Philox blocks (tile, t, it | {0, 2^31}).  In
+// production mode the sum of a tile's a = n exponential spacings is drawn
+// directly from Gamma(n) - S ~ Gamma(n) is independent of the normalised
+// spacings E/S ~ Dirichlet(1..1) - so the pre-pass over every element's
+// exponential disappears; the merge regenerates the tile's exponentials and
+// rescales them to S (same joint law of the order statistics).
+constexpr uint32_t kPurposeGamma = 0x47414D4Du;  // 'GAMM'
+
+__device__ double gamma_tile_sum(Key2 key, uint32_t t, uint32_t tile, double a) {
+  const double d = a - 1.0 / 3.0;
+  const double c = 1.0 / sqrt(9.0 * d);
+  for (uint32_t it = 0;; ++it) {
+    const uint4 r = philox10(make_uint4(tile, t, it, kPurposeGamma), key);
+    const double x = box_muller_f64(r.x, r.y, r.z, r.w).x;
+    double v = 1.0 + c * x;
+    if (v <= 0.0) continue;
+    v = v * v * v;
+    const uint4 r2 = philox10(make_uint4(tile, t, it | 0x80000000u, kPurposeGamma), key);
+    const double u = u53_open0(r2.x, r2.y);
+    if (log(u) < 0.5 * x * x + d - d * v + d * log(v)) return d * v;
+  }
+}
+
 template <typename TW, bool FAST = false>
 __global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restrict__ logw,
                                                               int64_t N, int64_t tpf,
@@ -864,19 +888,13 @@ __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
                                  : exp(__dsub_rn(lv[q], m)));
   }
   const double ssum = block_sum(part, scratch);
-  double se = 0.0;
-  if (MODE == 0) {
-    double e[kRun];
-    spacing_run(load_key(keys, f), t, i0 + r0, N, e);
-    double pe = 0.0;
-#pragma unroll
-    for (int q = 0; q < kRun; ++q) pe = __dadd_rn(pe, e[q]);
-    se = block_sum(pe, scratch);
-  }
   if (threadIdx.x == 0) {
     ws.tmax[tile] = nan ? NAN : m;
     ws.tsum[tile] = m == -INFINITY ? 0.0 : ssum;
-    ws.tesum[tile] = se;
+    // production: the tile's exponential-spacing sum S ~ Gamma(n) (gamma_tile_sum)
+    ws.tesum[tile] = MODE == 0 ? gamma_tile_sum(load_key(keys, f), t, static_cast<uint32_t>(tt),
+                                                static_cast<double>(n))
+                               : 0.0;
   }
 }
 
@@ -980,8 +998,8 @@ __global__ void wide2_partition(int64_t N, int64_t tpf, int64_t ntiles, WideWs w
   if (MODE == 1) {
     u = u_tape[f * N + i0 + (last ? n - 1 : 0)];
   } else {
-    const double c = last ? __dadd_rn(ws.teoff[tile], ws.tesum[tile])
-                          : __dadd_rn(ws.teoff[tile], spacing_exp_fast(load_key(keys, f), t, i0));
+    // first uniform of the tile >= teoff / cN; last = (teoff + S_tile) / cN
+    const double c = last ? __dadd_rn(ws.teoff[tile], ws.tesum[tile]) : ws.teoff[tile];
     u = c / ws.cN[f];
   }
   const double x = last ? u * (1.0 + 1e-12) : u * (1.0 - 1e-12);
@@ -1050,10 +1068,13 @@ __global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
       u[q] = run;
     }
     double tot;
-    const double off = __dadd_rn(ws.teoff[tile], block_exclusive_scan(run, scratch, &tot));
+    const double eoff = block_exclusive_scan(run, scratch, &tot);
+    // rescale the tile's spacings to its Gamma-drawn sum S (wide2_filter)
+    const double scale = ws.tesum[tile] / tot, teoff = ws.teoff[tile];
     const double inv = 1.0 / ws.cN[f];
 #pragma unroll
-    for (int q = 0; q < kRun; ++q) u[q] = r0 + q < n ? __dadd_rn(off, u[q]) * inv : 2.0;
+    for (int q = 0; q < kRun; ++q)
+      u[q] = r0 + q < n ? fma(__dadd_rn(eoff, u[q]), scale, teoff) * inv : 2.0;
   }
   int32_t a[kRun];
   if (wlen <= kWin) {
