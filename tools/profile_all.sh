@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round profile capture (run on the GPU box after the plain bench has exited 0):
+# one `ncu --set full` capture of each workload's dominant kernel plus the
+# launch lists (gpu__time_duration, cold-cache, serialised) of cfg4 and cfg2.
+set -u
+out=gpurun_out/prof
+mkdir -p $out
+cap() {  # name regex config [extra]
+  ncu --set full --clock-control none --import-source on -k "regex:$2" -s 2 -c 1 -o $out/$1 \
+    python bench.py --config $3 --steps 2 --warmup 2 --no-cpu-baseline --profile $4 \
+    > $out/$1.log 2>&1
+}
+cap fhn_fast_cfg4 fhn_fast_kernel cfg4 ""
+cap lorenz_fast_cfg2 lorenz_fast_kernel cfg2 ""
+cap resample_bank_cfg1b resample_bank_kernel cfg1b ""
+cap wide2_merge_cfg1c wide2_merge cfg1c ""
+cap fhnnet_fast_net fhnnet_fast_kernel net ""
+for c in cfg4 cfg2 cfg1c net; do
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    --clock-control none -c 80 --csv --log-file $out/launches_$c.csv \
+    python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline --profile \
+    > $out/launches_$c.log 2>&1
+done
+echo done
