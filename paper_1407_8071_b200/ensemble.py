@@ -11,6 +11,7 @@ keeps its meaning of "affects wall time only" and is validated but unused.
 from __future__ import annotations
 
 import time
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -80,6 +81,36 @@ class _EnsembleFilterOutput(FilterOutput):
     @seed.setter
     def seed(self, value):
         self.__dict__["_seed"] = value
+
+
+class _FilterOutputs(Sequence):
+    """EnsembleOutput.filter_outputs as a read-only sequence whose
+    FilterOutput records are built on first access (a bank has thousands of
+    filters; most callers only read the averaged estimates)."""
+
+    def __init__(self, variant, n_particles, seeds, est, lnc, coll, secs):
+        self._args = (variant, n_particles, seeds, est, lnc, coll, secs)
+        self._cache = {}
+
+    def __len__(self):
+        return self._args[3].shape[1]
+
+    def __getitem__(self, f):
+        if isinstance(f, slice):
+            return [self[i] for i in range(*f.indices(len(self)))]
+        if f < 0:
+            f += len(self)
+        if not 0 <= f < len(self):
+            raise IndexError(f)
+        if f not in self._cache:
+            variant, n_particles, seeds, est, lnc, coll, secs = self._args
+            steps = [int(k) + 1 for k in np.nonzero(coll[:, f])[0]]
+            self._cache[f] = _EnsembleFilterOutput(variant, n_particles, (seeds, f), est[:, f, :],
+                                                   lnc[:, f], secs, steps)
+        return self._cache[f]
+
+    def __eq__(self, other):
+        return list(self) == list(other)
 
 
 def filter_seeds(master_seed, n_filters: int):
@@ -171,13 +202,8 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     est_h = est_full.cpu().numpy()
     lnc_h = lnc_full.cpu().numpy()
     coll_h = coll_full.cpu().numpy()
-    steps_of = [[] for _ in range(n_filters)]
-    for k, f in zip(*np.nonzero(coll_h)):
-        steps_of[f].append(int(k) + 1)
-    seeds = _LazySeeds(master_seed, n_filters)
-    outputs = [_EnsembleFilterOutput(variant, n_particles, (seeds, f), est_h[:, f, :],
-                                     lnc_h[:, f], secs, steps_of[f])
-               for f in range(n_filters)]
+    outputs = _FilterOutputs(variant, n_particles, _LazySeeds(master_seed, n_filters), est_h,
+                             lnc_h, coll_h, secs)
     filter_seconds = np.full(n_filters, float(secs.sum()))
     return EnsembleOutput(variant, n_filters, n_particles, master_seed, outputs,
                           mean.cpu().numpy(), filter_seconds, total)
