@@ -366,9 +366,20 @@ typedef struct pf_bank_desc {
   const pf_hmm_params *hmm; /* host */
   const pf_lgm_params *lgm; /* host */
   float *step_ms; /* host (n_steps) or NULL: whole-interval durations (waits like prop_ms) */
-  void **events;  /* host array of 3*n_steps caller-created timing cudaEvent_t, or NULL:
-                     recorded at each interval's start, after its propagate kernel and at
-                     its end; nothing waits (the caller reads the times) */
+  void **events;  /* host array of 4*n_steps caller-created timing cudaEvent_t, or NULL:
+                     recorded at each interval's start, around its (main) propagate kernel
+                     and at its end; nothing waits (the caller reads the times) */
+  /* auxiliary particle filter (filters.py:115-154): variant = 1 runs apf_step per
+   * interval with the noise-free params0 (same struct type as the model's) */
+  int32_t variant;
+  const void *params0;
+  void *lam;           /* (M*N) first-stage log weights, logw dtype */
+  int32_t *anc1;       /* (M*N) first-stage ancestors */
+  int32_t *anc_comp;   /* (M*N) composed state rows */
+  void *x_tmp;         /* lookahead states, like x[0] */
+  uint32_t *q_tmp;     /* FH-N network lookahead history */
+  double *lnc_before;  /* (M) */
+  uint8_t *coll1;      /* (M) first-stage collapse flags */
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);

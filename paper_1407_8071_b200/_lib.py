@@ -76,7 +76,10 @@ class BankDesc(ctypes.Structure):
                 ("fhnnet", ctypes.POINTER(FhnNetParams)), ("q", c_vp * 2),
                 ("forcing_mask", c_vp), ("est_stride_f", c_i64), ("est_bits", c_i32),
                 ("hmm", ctypes.POINTER(HmmParams)), ("lgm", ctypes.POINTER(LgmParams)),
-                ("step_ms", ctypes.POINTER(ctypes.c_float)), ("events", c_vp)]
+                ("step_ms", ctypes.POINTER(ctypes.c_float)), ("events", c_vp),
+                ("variant", c_i32), ("params0", c_vp), ("lam", c_vp), ("anc1", c_vp),
+                ("anc_comp", c_vp), ("x_tmp", c_vp), ("q_tmp", c_vp), ("lnc_before", c_vp),
+                ("coll1", c_vp)]
 
 
 PF_MODEL_LORENZ = 0

@@ -253,8 +253,8 @@ class FilterBank:
         return torch.from_numpy(a).to(self.device)
 
     def _native_ok(self):
-        return (self.tape is None and self.variant == "bootstrap"
-                and self.kernel_events is None and self.post_resample is None)
+        return (self.tape is None and self.kernel_events is None
+                and self.post_resample is None)
 
     def _bank_desc(self):
         import ctypes
@@ -293,6 +293,14 @@ class FilterBank:
         d.est_dim = self.est_dim
         d.lnc_trace = self.lnc_tr.data_ptr()
         d.collapsed_trace = self.coll_tr.data_ptr()
+        if self.variant == "auxiliary":
+            d.variant = 1
+            d.params0 = ctypes.cast(ctypes.pointer(self.params0), ctypes.c_void_p)
+            d.lam, d.anc1, d.anc_comp = (self.lam.data_ptr(), self.anc1.data_ptr(),
+                                         self.anc_comp.data_ptr())
+            d.x_tmp = self.x_tmp.data_ptr()
+            d.q_tmp = self.q_tmp.data_ptr() if self.q_tmp is not None else None
+            d.lnc_before, d.coll1 = self.lnc_before.data_ptr(), self.coll1.data_ptr()
         return d
 
     def run_native(self, k0: int, n_steps: int, time_propagate: bool = False,
@@ -307,11 +315,11 @@ class FilterBank:
         if self.obs is None:
             raise RuntimeError("load_observations() first")
         if not self._native_ok():
-            raise RuntimeError("run_native: production bootstrap banks only")
+            raise RuntimeError("run_native: production banks only (no tape, no per-step hooks)")
         if self._desc is None:
             self._desc = self._bank_desc()
         timed = (time_propagate or time_steps) and n_steps > 0
-        pool = self.__dict__.get("_event_pools", {}).get(3 * n_steps) if timed else None
+        pool = self.__dict__.get("_event_pools", {}).get(4 * n_steps) if timed else None
         ms = sm = None
         if pool is not None:  # prepared events: recorded by the driver, no host wait
             evs, handles = pool
@@ -339,17 +347,17 @@ class FilterBank:
             if sm is not None:
                 self.last_step_ms = np.frombuffer(sm, dtype=np.float32).copy()
             return list(ms) if ms is not None else None
-        evs[3 * n_steps - 1].synchronize()
+        evs[4 * n_steps - 1].synchronize()
         if time_steps:
-            self.last_step_ms = np.array([evs[3 * i].elapsed_time(evs[3 * i + 2])
+            self.last_step_ms = np.array([evs[4 * i].elapsed_time(evs[4 * i + 3])
                                           for i in range(n_steps)], dtype=np.float32)
-        return [evs[3 * i].elapsed_time(evs[3 * i + 1]) for i in range(n_steps)] \
+        return [evs[4 * i + 1].elapsed_time(evs[4 * i + 2]) for i in range(n_steps)] \
             if time_propagate else None
 
     def prepare_timing(self, n_steps: int):
         """Create the timing events of an n_steps run_native call ahead of time
         (keeps their creation out of a timed region)."""
-        self._event_pool(3 * n_steps)
+        self._event_pool(4 * n_steps)
 
     def _event_pool(self, n):
         """n timing events and their raw handles (ctypes array), created once

@@ -24,6 +24,46 @@ extern "C" int pf_fhn_interval(const pf_fhn_params *, pf_dtype, const void *, co
 
 using namespace pf;
 
+// One propagate+weight launch of the descriptor's model with the given
+// (host) parameter struct - the bank's params or the auxiliary filter's
+// noise-free params0.
+static int bank_propagate(const pf_bank_desc *d, const void *params, const void *xin,
+                          const uint32_t *qin, const int32_t *anc, void *xout, uint32_t *qout,
+                          const double *y, void *logw, uint32_t t, void *stream) {
+  switch (d->model) {
+    case PF_MODEL_LORENZ:
+      return pf_lorenz_propagate_weight(static_cast<const pf_lorenz_params *>(params), d->dtype,
+                                        xin, anc, xout, y, logw, d->M, d->N, d->keys, t, nullptr,
+                                        d->status, stream);
+    case PF_MODEL_HMM:
+      return pf_hmm_propagate_weight(static_cast<const pf_hmm_params *>(params), d->dtype, xin,
+                                     anc, xout, y, logw, d->M, d->N, d->keys, t, nullptr,
+                                     d->status, stream);
+    case PF_MODEL_LGM:
+      return pf_lgm_propagate_weight(static_cast<const pf_lgm_params *>(params), d->dtype, xin,
+                                     anc, xout, y, logw, d->M, d->N, d->keys, t, nullptr,
+                                     d->status, stream);
+    case PF_MODEL_FHNNET:
+      return pf_fhnnet_step(static_cast<const pf_fhnnet_params *>(params), d->dtype, xin, qin,
+                            anc, xout, qout, d->forcing_mask, y, d->obs_idx, logw, d->M, d->N,
+                            d->keys, t, nullptr, nullptr, d->status, stream);
+    default:
+      return pf_fhn_interval(static_cast<const pf_fhn_params *>(params), d->dtype, xin, anc,
+                             xout, y, d->obs_idx, logw, d->M, d->N, d->keys, t, nullptr,
+                             d->status, stream);
+  }
+}
+
+static const void *bank_params(const pf_bank_desc *d) {
+  switch (d->model) {
+    case PF_MODEL_LORENZ: return d->lorenz;
+    case PF_MODEL_HMM: return d->hmm;
+    case PF_MODEL_LGM: return d->lgm;
+    case PF_MODEL_FHNNET: return d->fhnnet;
+    default: return d->fhn;
+  }
+}
+
 extern "C" {
 
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
@@ -44,7 +84,8 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
   const cudaStream_t s = as_stream(stream);
   const int64_t MN = d->M * d->N;
   // optional per-interval timing (events on the launch stream): start of the
-  // interval, end of the propagate kernel (the dominant one), end of the interval
+  // interval, around the (main) propagate kernel - the dominant one - and the
+  // end of the interval: 4 events per interval
   struct Events {
     std::vector<cudaEvent_t> e;
     ~Events() {
@@ -56,10 +97,15 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     // caller-owned, pre-created timing events: record only, no host wait
     ev = reinterpret_cast<cudaEvent_t *>(d->events);
   } else if ((d->prop_ms || d->step_ms) && n_steps > 0) {
-    evs.e.resize(3 * static_cast<size_t>(n_steps));
+    evs.e.resize(4 * static_cast<size_t>(n_steps));
     for (auto &x : evs.e) cudaEventCreate(&x);
     ev = evs.e.data();
   }
+  const bool apf = d->variant == 1;
+  PF_REQUIRE(!apf || (d->params0 && d->lam && d->anc1 && d->anc_comp && d->x_tmp &&
+                      d->lnc_before && d->coll1 &&
+                      (d->model != PF_MODEL_FHNNET || d->q_tmp)),
+             "pf_bank_run: auxiliary variant needs params0 and the APF scratch buffers");
   // planar states (x[d*MN + p]): the estimate is fused into the resampler
   const bool planar = d->model == PF_MODEL_LORENZ || d->model == PF_MODEL_HMM ||
                       d->model == PF_MODEL_LGM;
@@ -71,24 +117,33 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     const int32_t *anc = (have_ancestors || i > 0) ? d->anc : nullptr;
     const double *y = d->obs + static_cast<int64_t>(k) * d->dim_y;
     int rc;
-    if (ev) cudaEventRecord(ev[3 * i], s);
-    if (d->model == PF_MODEL_LORENZ)
-      rc = pf_lorenz_propagate_weight(d->lorenz, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
-                                      d->keys, t, nullptr, d->status, stream);
-    else if (d->model == PF_MODEL_HMM)
-      rc = pf_hmm_propagate_weight(d->hmm, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
-                                   d->keys, t, nullptr, d->status, stream);
-    else if (d->model == PF_MODEL_LGM)
-      rc = pf_lgm_propagate_weight(d->lgm, d->dtype, xin, anc, xout, y, d->logw, d->M, d->N,
-                                   d->keys, t, nullptr, d->status, stream);
-    else if (d->model == PF_MODEL_FHNNET)
-      rc = pf_fhnnet_step(d->fhnnet, d->dtype, xin, d->q[cur], anc, xout, d->q[cur ^ 1],
-                          d->forcing_mask, y, d->obs_idx, d->logw, d->M, d->N, d->keys, t,
-                          nullptr, nullptr, d->status, stream);
-    else
-      rc = pf_fhn_interval(d->fhn, d->dtype, xin, anc, xout, y, d->obs_idx, d->logw, d->M, d->N,
-                           d->keys, t, nullptr, d->status, stream);
-    if (ev) cudaEventRecord(ev[3 * i + 1], s);
+    if (ev) cudaEventRecord(ev[4 * i], s);
+    uint32_t *qin = d->q[cur], *qout = d->q[cur ^ 1];
+    const int32_t *src_anc = anc;
+    if (apf) {
+      // first stage (filters.py:126-141): lambda = log p(y | noise-free prediction),
+      // all -inf -> lambda = 0 (flagged), resample by lambda with a distinct
+      // Philox time word, compose with the previous ancestors
+      rc = bank_propagate(d, d->params0, xin, qin, anc, d->x_tmp, d->q_tmp, y, d->lam, t, stream);
+      if (rc) return rc;
+      rc = pf_apf_first_stage_prepare(d->dtype, d->lam, d->M, d->N, d->coll1, stream);
+      if (rc) return rc;
+      if (cudaMemcpyAsync(d->lnc_before, d->lnc, d->M * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return check_launch("pf_bank_run(apf lnc)");
+      rc = pf_segmented_resample_ex(d->dtype, d->lam, d->M, d->N, nullptr, d->keys,
+                                    t | 0x80000000u, d->anc1, d->lnc, d->collapsed, d->status,
+                                    d->ws, d->ws_bytes, nullptr, nullptr, 0, 0u, stream);
+      if (rc) return rc;
+      rc = pf_compose_ancestors(d->anc1, anc, MN, d->anc_comp, stream);
+      if (rc) return rc;
+      src_anc = d->anc_comp;
+    }
+    if (ev) cudaEventRecord(ev[4 * i + 1], s);
+    rc = bank_propagate(d, bank_params(d), xin, qin, src_anc, xout, qout, y, d->logw, t, stream);
+    if (!rc && apf)  // second stage weights log w - lambda[anc1] (filters.py:143)
+      rc = pf_apf_second_stage_weights(d->dtype, d->logw, d->lam, d->anc1, MN, stream);
+    if (ev) cudaEventRecord(ev[4 * i + 2], s);
     if (rc) return rc;
     double *est = d->est + static_cast<int64_t>(k) * d->est_step_stride + d->est_offset;
     const int64_t est_f0 = d->est_stride_f ? d->est_stride_f : d->est_dim;
@@ -102,6 +157,10 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                                     d->lnc, d->collapsed, d->status, d->ws, d->ws_bytes, nullptr,
                                     nullptr, 0, 0u, stream);
     if (rc) return rc;
+    if (apf) {  // a second-stage collapse restores the pre-step lnc (filters.py:146-148)
+      rc = pf_apf_finish(d->lnc, d->lnc_before, d->collapsed, d->coll1, d->M, stream);
+      if (rc) return rc;
+    }
     const int64_t est_f = est_f0;
     if (!fused) {
       rc = pf_filter_estimate_strided(d->dtype, xout, d->est_stride_p, d->est_stride_d,
@@ -122,15 +181,15 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
         cudaMemcpyAsync(d->collapsed_trace + static_cast<int64_t>(k) * d->M, d->collapsed,
                         d->M * sizeof(uint8_t), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
       return check_launch("pf_bank_run(collapse trace)");
-    if (ev) cudaEventRecord(ev[3 * i + 2], s);
+    if (ev) cudaEventRecord(ev[4 * i + 3], s);
     cur ^= 1;
   }
   (void)MN;
   if (ev && !d->events) {
-    cudaEventSynchronize(ev[3 * n_steps - 1]);
+    cudaEventSynchronize(ev[4 * n_steps - 1]);
     for (int32_t i = 0; i < n_steps; ++i) {
-      if (d->prop_ms) cudaEventElapsedTime(&d->prop_ms[i], ev[3 * i], ev[3 * i + 1]);
-      if (d->step_ms) cudaEventElapsedTime(&d->step_ms[i], ev[3 * i], ev[3 * i + 2]);
+      if (d->prop_ms) cudaEventElapsedTime(&d->prop_ms[i], ev[4 * i + 1], ev[4 * i + 2]);
+      if (d->step_ms) cudaEventElapsedTime(&d->step_ms[i], ev[4 * i], ev[4 * i + 3]);
     }
   }
   return check_launch("pf_bank_run");

@@ -261,7 +261,7 @@ struct FhnFast {
 // PP particles are advanced together by the same threads (independent
 // dependency chains -> more ILP per warp, one barrier per Euler step for
 // all PP particles).
-template <int ROWS, int COLS, int R, bool TAPE, int MINB, int PP>
+template <int ROWS, int COLS, int R, bool TAPE, int MINB, int PP, bool NF = false>
 __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
     const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
       const float *xs = xin + src * 2 * static_cast<int64_t>(NODES);
       if (tid == 0) bad[e] = 0;
       key[e] = Key2{0u, 0u};
-      if (!TAPE) key[e] = load_key(keys, fe[e]);
+      if (!TAPE && !NF) key[e] = load_key(keys, fe[e]);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         v[e][r] = 0.f;
@@ -342,6 +342,8 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
               zw0 = float(tape[b0 + wo]);
               zv1 = ok1 ? float(tape[b0 + COLS]) : 0.f;
               zw1 = ok1 ? float(tape[b0 + wo + COLS]) : 0.f;
+            } else if (NF) {  // noise-free lookahead: no draws (sig * 0 adds an exact 0)
+              zv0 = zw0 = zv1 = zw1 = 0.f;
             } else {
               const uint32_t node_pair = static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col);
               const uint4 rr =
@@ -499,7 +501,7 @@ static int launch_fhn(const FhnConsts &c, const void *x_in, const int32_t *anc, 
   return check_launch("pf_fhn_interval");
 }
 
-template <int ROWS, int COLS, bool TAPE, int MINB, int PP, int R = kFhnRows>
+template <int ROWS, int COLS, bool TAPE, int MINB, int PP, bool NF = false, int R = kFhnRows>
 static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
                              const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                              int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
@@ -507,7 +509,7 @@ static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t 
   constexpr int threads = (((ROWS + R - 1) / R * COLS) + 31) / 32 * 32;
   static_assert(threads <= 256, "lattice too large for the fast kernel");
   const size_t smem = PP * 2 * static_cast<size_t>((ROWS + 2) * (COLS + 2)) * sizeof(float);
-  auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE, MINB, PP>;
+  auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE, MINB, PP, NF>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int per_sm = 0;
@@ -558,9 +560,11 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   if (tape)
     return launch_fhn_fast_t<30, 50, true, 3, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                  keys, t, tape, status, s);
-  // production: 2 particles per CTA iteration, 3 resident CTAs/SM (80 regs)
   // one particle per CTA, 3 CTAs/SM: measured 46.1 ms vs 46.5 ms for two
   // particles per CTA and 46.9-48.4 ms for 4-5 CTAs/SM (cfg4)
+  if (c.sig_v == 0.0 && c.sig_w == 0.0)  // the auxiliary filter's point prediction
+    return launch_fhn_fast_t<30, 50, false, 3, 1, true>(fc, x_in, anc, x_out, y, obs_idx, logw,
+                                                        MN, N, keys, t, tape, status, s);
   return launch_fhn_fast_t<30, 50, false, 3, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                 keys, t, tape, status, s);
 }

@@ -232,6 +232,34 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
   }
 }
 
+// Noise-free interval (the auxiliary filter's point prediction,
+// lorenz63.py:57-60): the same substep arithmetic with zero increments and no
+// draws at all.  FAST=true uses the fp32 production substep (bit-identical
+// to lorenz_fast_kernel with zero noise scale: fma(0, z, v) == v), else the
+// exact-order substep of lorenz_pw_kernel.
+template <typename T, bool FAST>
+__global__ void __launch_bounds__(256) lorenz_det_kernel(
+    const T *__restrict__ xin, const int32_t *__restrict__ anc, T *__restrict__ xout,
+    const double *__restrict__ y, T *__restrict__ logw, int64_t MN, int32_t N, int obs_dim,
+    LorenzConsts c, uint32_t *__restrict__ status) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= MN) return;
+  const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+  T x1 = xin[src], x2 = xin[MN + src], x3 = xin[2 * MN + src];
+  for (int k = 0; k < c.n_sub; ++k) {
+    if constexpr (FAST)
+      lorenz_substep_fast(x1, x2, x3, 0.f, 0.f, 0.f, c.f_dt, c.f_ndts, c.f_r, c.f_nb, c.f_cz);
+    else
+      lorenz_substep<T>(x1, x2, x3, T(0), T(0), T(0), c);
+  }
+  if (!(finite_val(x1) && finite_val(x2) && finite_val(x3)))
+    atomicOr(status + p / N, PF_ST_DIVERGED);
+  xout[p] = x1;
+  xout[MN + p] = x2;
+  xout[2 * MN + p] = x3;
+  logw[p] = lorenz_loglik<T>(x1, x3, y, obs_dim, c.two_obs_var);
+}
+
 // fp64 production kernel for SMALL banks (BASELINE cfg0: 4 x 1000 particles):
 // one warp per particle.  The Gaussian increments do not depend on the
 // state, so the 32 lanes generate a chunk of substeps' normals in parallel
@@ -371,6 +399,21 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
   const cudaStream_t s = as_stream(stream);
   const unsigned grid = grid_for(MN, 256);
   const int32_t n32 = static_cast<int32_t>(N);
+  if (p->noise_scale == 0.0 && p->n_sub > 0) {  // point prediction: no draws
+    if (dtype == PF_F64)
+      lorenz_det_kernel<double, false><<<grid, 256, 0, s>>>(
+          static_cast<const double *>(x_in), anc, static_cast<double *>(x_out), y,
+          static_cast<double *>(logw_out), MN, n32, p->obs_dim, c, status);
+    else if (z_tape)
+      lorenz_det_kernel<float, false><<<grid, 256, 0, s>>>(
+          static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y,
+          static_cast<float *>(logw_out), MN, n32, p->obs_dim, c, status);
+    else
+      lorenz_det_kernel<float, true><<<grid, 256, 0, s>>>(
+          static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y,
+          static_cast<float *>(logw_out), MN, n32, p->obs_dim, c, status);
+    return check_launch("pf_lorenz_propagate_weight(noise-free)");
+  }
   if (dtype == PF_F64) {
     auto *xi = static_cast<const double *>(x_in);
     auto *xo = static_cast<double *>(x_out);

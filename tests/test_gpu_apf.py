@@ -143,3 +143,36 @@ def test_apf_hook_level_step_matches_oracle(golden):
                                 steps)
     assert norm_rel(st1.particles, x1) < 1e-12
     assert abs(st1.log_norm_const - lnc1) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["lorenz", "fhnnet"])
+def test_native_apf_driver_matches_stepwise(kind):
+    """pf_bank_run's auxiliary variant (the whole apf_step sequence in C++)
+    equals the per-step Python path: states, lnc, collapse flags identical,
+    estimates to fp64 rounding (the planar estimate is fused natively)."""
+    if kind == "lorenz":
+        truth0, _, obs = orc.lorenz_truth(seed=21, n_obs=6)
+        gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                              prior_mean=tuple(truth0), prior_var=1.0)
+        dtypes = (torch.float64, torch.float32)
+    else:
+        gm = pf.FhnNetworkModel(J=8, n_zones=2, zone_width=2, stim_prob=0.05)
+        _, obs = pf.simulate.simulate(gm, 6, 3)
+        dtypes = (torch.float32,)
+    keys = pf.philox.filter_keys(9, 3)
+    for dtype in dtypes:
+        res = []
+        for native in (True, False):
+            bank = pf.FilterBank(gm, 3, 256, keys, len(obs), dtype=dtype, variant="auxiliary")
+            bank.load_observations(obs)
+            bank.init()
+            if not native:
+                bank.kernel_events = (torch.cuda.Event(), torch.cuda.Event())
+            bank.run()
+            torch.cuda.synchronize()
+            res.append((bank.est.cpu().numpy(), bank.lnc_tr.cpu().numpy(),
+                        bank.coll_tr.cpu().numpy(), bank.particles()))
+        a, b = res
+        assert np.linalg.norm(a[0] - b[0]) <= 1e-13 * np.linalg.norm(b[0])
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+        assert np.array_equal(a[3], b[3])
