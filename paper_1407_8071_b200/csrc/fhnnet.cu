@@ -396,7 +396,9 @@ struct NetMeta {
   double sel;
 };
 
-template <int CW, int S>
+// NF: noise-free transition (transition_point_prediction, fhn.py:191-197): no
+// new stimulus, zero increments, no draws.
+template <int CW, int S, bool NF = false>
 __global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW >= 2 ? 8 : 12) fhnnet_fast_kernel(
     const float *__restrict__ xin, const uint32_t *__restrict__ qin,
     const int32_t *__restrict__ anc, float *__restrict__ xout, uint32_t *__restrict__ qout,
@@ -444,17 +446,23 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW 
         const int64_t p = first + i * stride;
         const int64_t f = p / N;
         const uint32_t j = static_cast<uint32_t>(p - f * N);
-        const Key2 key = load_key(keys, f);
-        // stimulus draws (fhn.py:158-159): fire, then cell select
-        const uint4 r = philox10(make_uint4(j, t, 0u, kPurposeNetStim), key);
         NetMeta &m = meta[k];
         m.p = p;
         m.f = f;
         m.j = j;
-        m.fire = u53_closed0(r.x, r.y) < c.stim_prob;
-        m.sel = u53_closed0(r.z, r.w);
-        m.k0 = key.k0;
-        m.k1 = key.k1;
+        if (NF) {
+          m.fire = 0;
+          m.sel = 0.0;
+          m.k0 = m.k1 = 0u;
+        } else {
+          const Key2 key = load_key(keys, f);
+          // stimulus draws (fhn.py:158-159): fire, then cell select
+          const uint4 r = philox10(make_uint4(j, t, 0u, kPurposeNetStim), key);
+          m.fire = u53_closed0(r.x, r.y) < c.stim_prob;
+          m.sel = u53_closed0(r.z, r.w);
+          m.k0 = key.k0;
+          m.k1 = key.k1;
+        }
         const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
         unsigned char *st = smem_raw + k * stage_bytes;
         mbar_arrive_expect_tx(&full[k], stage_bytes);  // release: meta visible with the data
@@ -559,10 +567,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW 
       const float4 dn = has_dn ? *reinterpret_cast<const float4 *>(su + n0 + J) : zero4;
       const float left = has_l ? su[n0 - 1] : 0.f;
       const float right = has_r ? su[n0 + 4] : 0.f;
-      const uint4 rr = philox10(make_uint4(m.j, t, static_cast<uint32_t>(g), kPurposeNetNoise),
-                                Key2{m.k0, m.k1});
-      const float2 za = box_muller_fast_unscaled(rr.x, rr.y);
-      const float2 zb = box_muller_fast_unscaled(rr.z, rr.w);
+      float2 za = make_float2(0.f, 0.f), zb = za;
+      if (!NF) {
+        const uint4 rr = philox10(make_uint4(m.j, t, static_cast<uint32_t>(g), kPurposeNetNoise),
+                                  Key2{m.k0, m.k1});
+        za = box_muller_fast_unscaled(rr.x, rr.y);
+        zb = box_muller_fast_unscaled(rr.z, rr.w);
+      }
       const float uu[6] = {left, u4.x, u4.y, u4.z, u4.w, right};
       const float upv[4] = {up.x, up.y, up.z, up.w}, dnv[4] = {dn.x, dn.y, dn.z, dn.w};
       const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -630,7 +641,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW 
   }
 }
 
-template <int CW, int S>
+template <int CW, int S, bool NF = false>
 static int launch_net_fast(const NetConsts &c, const void *x_in, const uint32_t *q_in,
                            const int32_t *anc, void *x_out, uint32_t *q_out, const double *fmask,
                            const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
@@ -638,7 +649,7 @@ static int launch_net_fast(const NetConsts &c, const void *x_in, const uint32_t 
                            cudaStream_t s) {
   const size_t smem = static_cast<size_t>(S) * c.nodes * 12 + static_cast<size_t>(c.nodes) * 8 +
                       static_cast<size_t>((c.nodes + 31) / 32) * 4;
-  auto kern = fhnnet_fast_kernel<CW, S>;
+  auto kern = fhnnet_fast_kernel<CW, S, NF>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (CW + 1) * 32, smem);
@@ -662,7 +673,7 @@ static int net_fast_warps(const NetConsts &c) {
 // and J <= 32 (one 4-node group per compute thread).
 // PF_FHNNET_KERNEL=generic forces the generic kernel (comparison tests).
 static bool net_fast_ok(const NetConsts &c, pf_dtype dtype, bool tape) {
-  if (dtype != PF_F32 || tape || !c.stochastic || c.J % 4 != 0 || net_fast_warps(c) == 0)
+  if (dtype != PF_F32 || tape || c.J % 4 != 0 || net_fast_warps(c) == 0)
     return false;
   const char *env = std::getenv("PF_FHNNET_KERNEL");
   return !(env && std::strcmp(env, "generic") == 0);
@@ -793,9 +804,12 @@ int pf_fhnnet_step(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
   const int32_t n32 = static_cast<int32_t>(N);
   const bool tape = p->stochastic && stim_tape;
   if (net_fast_ok(c, dtype, tape)) {
-#define PF_NET_FAST(CW)                                                                      \
-  return launch_net_fast<CW, 3>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y, obs_idx, \
-                                logw_out, MN, n32, keys, t, status, s)
+#define PF_NET_FAST(CW)                                                                       \
+  return c.stochastic                                                                        \
+             ? launch_net_fast<CW, 3>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y,      \
+                                      obs_idx, logw_out, MN, n32, keys, t, status, s)        \
+             : launch_net_fast<CW, 3, true>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y, \
+                                            obs_idx, logw_out, MN, n32, keys, t, status, s)
     switch (net_fast_warps(c)) {
       case 1: PF_NET_FAST(1);
       case 2: PF_NET_FAST(2);

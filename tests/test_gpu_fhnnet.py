@@ -251,11 +251,13 @@ def test_production_is_deterministic_and_tracks(golden):
     assert mse < 0.5 * float(np.mean((truth_u - truth_u.mean()) ** 2))
 
 
+@pytest.mark.parametrize("noise_free", [False, True])
 @pytest.mark.parametrize("J", [8, 12, 20, 28, 32])
-def test_fast_kernel_matches_generic(golden, monkeypatch, J):
+def test_fast_kernel_matches_generic(golden, monkeypatch, J, noise_free):
     """The bulk-copy fp32 kernel and the generic kernel run the same
     Philox draws and arithmetic order: states within fp32 rounding of each
-    other, identical stimulus decisions (history bits)."""
+    other, identical stimulus decisions (history bits).  noise_free: the
+    auxiliary filter's lookahead transition (fhn.py:191-197)."""
     g = golden["fhnnet"]
     gm = pf.FhnNetworkModel(J=J, n_zones=2, zone_width=2, stim_prob=0.5)
     M, N = 3, 40
@@ -284,7 +286,8 @@ def test_fast_kernel_matches_generic(golden, monkeypatch, J):
         lw = torch.empty(M * N, dtype=torch.float32, device="cuda")
         st = torch.zeros(M, dtype=torch.int32, device="cuda")
         for t in (81, 5000):  # forcing on / off
-            pf._lib.call("pf_fhnnet_step", gm.params(), pf._lib.PF_F32, pf._lib.ptr(x),
+            pf._lib.call("pf_fhnnet_step", gm.params(noise_free=noise_free), pf._lib.PF_F32,
+                         pf._lib.ptr(x),
                          pf._lib.ptr(q), pf._lib.ptr(anc), pf._lib.ptr(xo), pf._lib.ptr(qo),
                          pf._lib.ptr(mask), pf._lib.ptr(dy), pf._lib.ptr(idx), pf._lib.ptr(lw),
                          M, N, pf._lib.ptr(keys), t, None, None, pf._lib.ptr(st),
@@ -297,5 +300,10 @@ def test_fast_kernel_matches_generic(golden, monkeypatch, J):
         assert np.array_equal(a[0][:, 2 * K:], b[0][:, 2 * K:])
         assert norm_rel(a[1], b[1]) < 1e-6
         assert np.array_equal(a[2], b[2])
-    # stimuli actually fired somewhere in the fast run
-    assert outs[0][0][:, 2 * gm.nodes: 3 * gm.nodes].sum() > 0
+    if noise_free:  # no new stimulus: the history just shifts
+        K, H = gm.nodes, gm.stim_hold
+        x_anc = x0[anc.cpu().numpy()]
+        assert not outs[0][0][:, 2 * K: 3 * K].any()
+        assert np.array_equal(outs[0][0][:, 3 * K:], x_anc[:, 2 * K: (H + 1) * K])
+    else:  # stimuli actually fired somewhere in the fast run
+        assert outs[0][0][:, 2 * gm.nodes: 3 * gm.nodes].sum() > 0
