@@ -30,14 +30,12 @@ __device__ __forceinline__ double block_sum(double v, double *scratch) {
   v = warp_sum(v);
   if (lane == 0) scratch[warp] = v;
   __syncthreads();
-  if (warp == 0) {
-    double x = lane < nw ? scratch[lane] : 0.0;
-    x = warp_sum(x);
-    if (lane == 0) scratch[32] = x;
-  }
-  __syncthreads();
-  const double r = scratch[32];
-  __syncthreads();
+  // every warp reduces the warp partials (same order as a single warp would):
+  // no divergent shuffle section, no second barrier
+  double x = lane < nw ? scratch[lane] : 0.0;
+  x = warp_sum(x);
+  const double r = __shfl_sync(0xffffffffu, x, 0);
+  __syncthreads();  // scratch reusable
   return r;
 }
 
@@ -47,13 +45,9 @@ __device__ __forceinline__ double block_max(double v, double *scratch) {
   v = warp_max(v);
   if (lane == 0) scratch[warp] = v;
   __syncthreads();
-  if (warp == 0) {
-    double x = lane < nw ? scratch[lane] : -INFINITY;
-    x = warp_max(x);
-    if (lane == 0) scratch[32] = x;
-  }
-  __syncthreads();
-  const double r = scratch[32];
+  double x = lane < nw ? scratch[lane] : -INFINITY;
+  x = warp_max(x);
+  const double r = __shfl_sync(0xffffffffu, x, 0);
   __syncthreads();
   return r;
 }
@@ -79,19 +73,17 @@ __device__ __forceinline__ double block_scan_inplace(double *s, int n, double ca
     }
     if (lane == 31) scratch[warp] = v;
     __syncthreads();
-    if (warp == 0) {
-      double x = lane < nw ? scratch[lane] : 0.0;
+    double x = lane < nw ? scratch[lane] : 0.0;  // every warp scans the warp totals
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double u = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x = __dadd_rn(x, u);
-      }
-      scratch[lane] = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = __dadd_rn(x, u);
     }
-    __syncthreads();
-    const double off = warp > 0 ? __dadd_rn(carry, scratch[warp - 1]) : carry;
+    const double wprev = __shfl_sync(0xffffffffu, x, warp > 0 ? warp - 1 : 0);
+    const double wtot = __shfl_sync(0xffffffffu, x, nw - 1);
+    const double off = warp > 0 ? __dadd_rn(carry, wprev) : carry;
     if (i < n) s[i] = __dadd_rn(off, v);
-    carry = __dadd_rn(carry, scratch[nw - 1]);
+    carry = __dadd_rn(carry, wtot);
     __syncthreads();
   }
   return carry;

@@ -16,6 +16,8 @@
 //    merge), workspace from pf_resample_workspace_bytes().
 // Everything is fp64 (the reference upcasts: core.py:126, resampling.py:11);
 // fp32 CDFs lose ~94% of ancestors at N=2^26 (SURVEY §7 hard part 1).
+#include <cstring>
+#include <cstdlib>
 #include "block_ops.cuh"
 #include "common.cuh"
 #include "npsum.cuh"
@@ -64,18 +66,16 @@ __device__ __forceinline__ double block_exclusive_scan(double v, double *scratch
   }
   if (lane == 31) scratch[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    double wv = lane < nw ? scratch[lane] : 0.0;
+  // every warp scans the warp totals itself (no divergent single-warp
+  // section, one barrier fewer); same association order
+  double wv = lane < nw ? scratch[lane] : 0.0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, wv, o);
-      if (lane >= o) wv = __dadd_rn(wv, y);
-    }
-    scratch[lane] = wv;  // inclusive warp-total prefix
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, wv, o);
+    if (lane >= o) wv = __dadd_rn(wv, y);
   }
-  __syncthreads();
-  const double woff = warp > 0 ? scratch[warp - 1] : 0.0;
-  *total = scratch[nw - 1];
+  const double woff = __shfl_sync(0xffffffffu, wv, warp > 0 ? warp - 1 : 0);
+  *total = __shfl_sync(0xffffffffu, wv, nw - 1);
   const double prev = __shfl_up_sync(0xffffffffu, x, 1);
   const double excl = lane > 0 ? prev : 0.0;  // sum of lower lanes in this warp
   __syncthreads();
@@ -387,7 +387,10 @@ struct WideWs {
   int32_t *n_leaves;
   int64_t max_leaves;
   int64_t *klo, *khi;  // per u-tile CDF window (merge partition)
+  double *cst;         // per (filter, tile chunk): max, weight sum, spacing sum, nan
 };
+
+constexpr int64_t kFilterChunk = 1024;  // tiles per CTA of the chunked filter pass (256 x 4)
 
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
@@ -419,6 +422,7 @@ static size_t wide_ws_layout(int64_t M, int64_t N, WideWs *w, char *base) {
   ws.n_leaves = reinterpret_cast<int32_t *>(take(M * 4));
   ws.klo = reinterpret_cast<int64_t *>(take(nt * 8));
   ws.khi = reinterpret_cast<int64_t *>(take(nt * 8));
+  ws.cst = reinterpret_cast<double *>(take(static_cast<size_t>(M) * (tpf / kFilterChunk + 1) * 32));
   if (w) *w = ws;
   return off;
 }
@@ -550,6 +554,24 @@ __device__ __forceinline__ void load_run(const TW *p, int64_t avail, bool aligne
   }
 }
 
+// fp32 production log weights stay fp32 in registers (no fp64 conversions on
+// the 16-lane XU pipe): -inf padding past `avail`
+__device__ __forceinline__ void load_run_f(const float *p, int64_t avail, bool aligned, float *v) {
+  if (aligned && avail >= kRun) {
+#pragma unroll
+    for (int q = 0; q < kRun; q += 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4 *>(p + q));
+      v[q] = x.x;
+      v[q + 1] = x.y;
+      v[q + 2] = x.z;
+      v[q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) v[q] = q < avail ? __ldg(p + q) : -INFINITY;
+  }
+}
+
 // kRun exponential spacings E_i, i = i0 .. i0+kRun-1 (i0 % 4 == 0): 4 Philox
 // blocks, one 32-bit word per draw (same stream as spacing_exp_fast).
 __device__ __forceinline__ void spacing_run(Key2 key, uint32_t t, int64_t i0, int64_t limit,
@@ -604,20 +626,42 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restri
   const int n = static_cast<int>((N - i0 < kTile ? N - i0 : kTile));
   const int r0 = threadIdx.x * kRun;
   double v[kRun];
-  load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, v);
   double run = 0.0;
-  if (FAST) {
-    // w = expf(lw - tile max) * exp(tile max - max) / total (see wide2_tile_stats)
+  if constexpr (FAST && std::is_same<TW, float>::value) {
+    // production fp32: w = expf(lw - tile max), an fp32 running sum over the
+    // thread's run (the same association wide2_tile_stats sums in), scaled by
+    // exp(tile max - max) / total in fp64 (see wide2_tile_stats)
+    float lf[kRun];
+    load_run_f(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, lf);
     const double mt = ws.tmax[tile];
-    const double scale = exp(__dsub_rn(mt, m)) / total;
+    const bool live = mt != -INFINITY;  // an all -inf tile has weight 0
+    const float mtf = static_cast<float>(mt);
+    const double scale = live ? exp(__dsub_rn(mt, m)) / total : 0.0;
+    float pf = 0.f;
 #pragma unroll
     for (int q = 0; q < kRun; ++q) {
-      const double w =
-          r0 + q < n ? static_cast<double>(expf(static_cast<float>(v[q] - mt))) * scale : 0.0;
+      if (live) pf += expf(lf[q] - mtf);  // padding: expf(-inf) = 0
+      v[q] = static_cast<double>(pf) * scale;
+    }
+    run = v[kRun - 1];
+  } else if (FAST) {
+    load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, v);
+    // w = expf(lw - tile max) * exp(tile max - max) / total (see wide2_tile_stats)
+    // a tile of -inf log weights has tmax = -inf: all its weights are 0
+    // (expf(-inf - -inf) would be NaN)
+    const double mt = ws.tmax[tile];
+    const bool live = mt != -INFINITY;
+    const double scale = live ? exp(__dsub_rn(mt, m)) / total : 0.0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      const double w = (live && r0 + q < n)
+                           ? static_cast<double>(expf(static_cast<float>(v[q] - mt))) * scale
+                           : 0.0;
       run = __dadd_rn(run, w);
       v[q] = run;
     }
   } else {
+    load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, v);
 #pragma unroll
     for (int q = 0; q < kRun; ++q) {
       const double w = r0 + q < n ? __ddiv_rn(exp(__dsub_rn(v[q], m)), total) : 0.0;
@@ -854,7 +898,7 @@ __global__ void __launch_bounds__(32) wide_exact_cumsum(int64_t N, WideWs ws) {
 // D: per u-tile: sorted uniforms, the CDF window they fall into is staged in
 //    shared memory when it fits (galloping search in global memory when it
 //    does not), ancestors and the fused gather written coalesced.
-template <typename TW, int MODE>
+template <typename TW, int MODE, bool GAMMA = true>
 __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
     const TW *__restrict__ logw, int64_t N, int64_t tpf, WideWs ws,
     const uint32_t *__restrict__ keys, uint32_t t) {
@@ -864,6 +908,36 @@ __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
   const int64_t i0 = tt * kTile;
   const int n = static_cast<int>(N - i0 < kTile ? N - i0 : kTile);
   const int r0 = threadIdx.x * kRun;
+  if constexpr (MODE == 0 && std::is_same<TW, float>::value) {
+    // production fp32: max, expf and the run sums in fp32 (wide_tile_cum<float,
+    // true> recomputes exactly these run sums), one fp64 conversion per thread
+    float lf[kRun];
+    load_run_f(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, lf);
+    float mxf = -INFINITY;
+    int nanf = 0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      nanf |= isnan(lf[q]);
+      mxf = fmaxf(mxf, lf[q]);
+    }
+    nanf = __syncthreads_or(nanf);
+    const double mt = block_max(static_cast<double>(mxf), scratch);
+    float pf = 0.f;
+    if (mt != -INFINITY) {
+      const float mtf = static_cast<float>(mt);
+#pragma unroll
+      for (int q = 0; q < kRun; ++q) pf += expf(lf[q] - mtf);
+    }
+    const double ssum = block_sum(static_cast<double>(pf), scratch);
+    if (threadIdx.x == 0) {
+      ws.tmax[tile] = nanf ? NAN : mt;
+      ws.tsum[tile] = mt == -INFINITY ? 0.0 : ssum;
+      if (GAMMA)
+        ws.tesum[tile] = gamma_tile_sum(load_key(keys, f), t, static_cast<uint32_t>(tt),
+                                        static_cast<double>(n));
+    }
+    return;
+  }
   double lv[kRun];
   load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, lv);
   double mx = -INFINITY;
@@ -892,9 +966,157 @@ __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
     ws.tmax[tile] = nan ? NAN : m;
     ws.tsum[tile] = m == -INFINITY ? 0.0 : ssum;
     // production: the tile's exponential-spacing sum S ~ Gamma(n) (gamma_tile_sum)
-    ws.tesum[tile] = MODE == 0 ? gamma_tile_sum(load_key(keys, f), t, static_cast<uint32_t>(tt),
-                                                static_cast<double>(n))
-                               : 0.0;
+    if (GAMMA)
+      ws.tesum[tile] = MODE == 0 ? gamma_tile_sum(load_key(keys, f), t, static_cast<uint32_t>(tt),
+                                                  static_cast<double>(n))
+                                 : 0.0;
+  }
+}
+
+// Production tile spacing sums S_tile ~ Gamma(n_tile) (gamma_tile_sum), one
+// thread per tile: the rejection sampler's fp64 latency no longer sits at the
+// end of every stats CTA (same values, same counters).
+__global__ void __launch_bounds__(128) wide2_gamma(int64_t M, int64_t N, int64_t tpf, WideWs ws,
+                                                   const uint32_t *__restrict__ keys,
+                                                   uint32_t t) {
+  const int64_t tile = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (tile >= M * tpf) return;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  const int64_t n = N - tt * kTile < kTile ? N - tt * kTile : kTile;
+  ws.tesum[tile] = gamma_tile_sum(load_key(keys, f), t, static_cast<uint32_t>(tt),
+                                  static_cast<double>(n));
+}
+
+// Production filter totals for very wide filters (tpf > kFilterChunk tiles):
+// the single-CTA wide2_filter walks 32K tiles on one SM (88 us at N = 2^26).
+// A: one 256-thread CTA per (chunk, filter): chunk max, weight sum relative
+//    to it, spacing sum, chunk-local exclusive scans into twoff / teoff.
+// B: one warp per filter combines the chunks (online max rescaling).
+// C: per (chunk, filter): rescale the local scans to global offsets.
+__global__ void __launch_bounds__(256) wide2_chunk_scan(int64_t tpf, WideWs ws) {
+  constexpr int kFr = kFilterChunk / 256;
+  __shared__ double scratch[33];
+  const int64_t f = blockIdx.y, c = blockIdx.x, nch = gridDim.x;
+  const int64_t j0 = c * kFilterChunk + static_cast<int64_t>(threadIdx.x) * kFr;
+  const double *tmax = ws.tmax + f * tpf, *tsum = ws.tsum + f * tpf, *tes = ws.tesum + f * tpf;
+  double mv[kFr];
+  double mx = -INFINITY;
+  int nan = 0;
+#pragma unroll
+  for (int q = 0; q < kFr; ++q) {
+    mv[q] = j0 + q < tpf ? tmax[j0 + q] : -INFINITY;
+    nan |= isnan(mv[q]);
+    mx = fmax(mx, mv[q]);
+  }
+  nan = __syncthreads_or(nan);
+  const double cm = block_max(mx, scratch);
+  double wv[kFr], ev[kFr];
+  double rw = 0.0, re = 0.0;
+#pragma unroll
+  for (int q = 0; q < kFr; ++q) {
+    const int64_t j = j0 + q;
+    const double w = (j < tpf && cm != -INFINITY && !nan) ? tsum[j] * exp(mv[q] - cm) : 0.0;
+    const double e = j < tpf ? tes[j] : 0.0;
+    wv[q] = rw;
+    ev[q] = re;
+    rw += w;
+    re += e;
+  }
+  double tw, te;
+  const double ow = block_exclusive_scan(rw, scratch, &tw);
+  const double oe = block_exclusive_scan(re, scratch, &te);
+#pragma unroll
+  for (int q = 0; q < kFr; ++q) {
+    const int64_t j = j0 + q;
+    if (j < tpf) {
+      ws.twoff[f * tpf + j] = ow + wv[q];
+      ws.teoff[f * tpf + j] = oe + ev[q];
+    }
+  }
+  if (threadIdx.x == 0) {
+    double *cs = ws.cst + (f * nch + c) * 4;
+    cs[0] = cm;
+    cs[1] = tw;
+    cs[2] = te;
+    cs[3] = nan ? 1.0 : 0.0;
+  }
+}
+
+// one warp per filter: lanes take chunks 32 at a time (max, then an
+// in-order scan of the rescaled chunk sums with a running carry)
+__global__ void __launch_bounds__(128) wide2_chunk_combine(int64_t M, int64_t N, int64_t nch,
+                                                           WideWs ws, uint8_t *collapsed,
+                                                           uint32_t *status, double *lnc,
+                                                           const uint32_t *keys, uint32_t t) {
+  const int64_t f = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (f >= M) return;  // whole warps
+  double *cs = ws.cst + f * nch * 4;
+  double m = -INFINITY;
+  int nan = 0;
+  for (int64_t c = lane; c < nch; c += 32) {
+    nan |= cs[4 * c + 3] != 0.0;
+    m = fmax(m, cs[4 * c]);
+  }
+  m = warp_max(m);
+  m = __shfl_sync(0xffffffffu, m, 0);
+  nan = __any_sync(0xffffffffu, nan);
+  const int fl = nan ? 2 : (m == -INFINITY ? 1 : 0);
+  if (lane == 0) {
+    ws.flag[f] = fl;
+    ws.m[f] = m;
+    collapsed[f] = fl == 1 ? 1 : 0;
+    if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
+  }
+  if (fl) return;
+  double cw = 0.0, ce = 0.0;  // carries
+  for (int64_t c0 = 0; c0 < nch; c0 += 32) {
+    const int64_t c = c0 + lane;
+    double w = 0.0, e = 0.0;
+    if (c < nch) {
+      w = cs[4 * c] == -INFINITY ? 0.0 : cs[4 * c + 1] * exp(cs[4 * c] - m);
+      e = cs[4 * c + 2];
+    }
+    double iw = w, ie = e;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double yw = __shfl_up_sync(0xffffffffu, iw, o);
+      const double ye = __shfl_up_sync(0xffffffffu, ie, o);
+      if (lane >= o) {
+        iw += yw;
+        ie += ye;
+      }
+    }
+    if (c < nch) {  // exclusive chunk offsets, in place
+      cs[4 * c + 1] = cw + (iw - w);
+      cs[4 * c + 2] = ce + (ie - e);
+    }
+    cw += __shfl_sync(0xffffffffu, iw, 31);
+    ce += __shfl_sync(0xffffffffu, ie, 31);
+  }
+  if (lane == 0) {
+    ws.total[f] = cw;
+    ws.cN[f] = ce + spacing_exp_fast(load_key(keys, f), t, N);
+    lnc[f] = lnc[f] + ((m + log(cw)) - log(static_cast<double>(N)));
+  }
+}
+
+__global__ void __launch_bounds__(256) wide2_chunk_apply(int64_t tpf, WideWs ws) {
+  constexpr int kFr = kFilterChunk / 256;
+  const int64_t f = blockIdx.y, c = blockIdx.x, nch = gridDim.x;
+  if (ws.flag[f]) return;
+  const double *cs = ws.cst + (f * nch + c) * 4;
+  const double inv = 1.0 / ws.total[f];
+  const double scale = cs[0] == -INFINITY ? 0.0 : exp(cs[0] - ws.m[f]);
+  const double ow = cs[1], oe = cs[2];
+  const int64_t j0 = c * kFilterChunk + static_cast<int64_t>(threadIdx.x) * kFr;
+#pragma unroll
+  for (int q = 0; q < kFr; ++q) {
+    const int64_t j = f * tpf + j0 + q;
+    if (j0 + q < tpf) {
+      ws.twoff[j] = fma(ws.twoff[j], scale, ow) * inv;
+      ws.teoff[j] += oe;
+    }
   }
 }
 
@@ -1012,16 +1234,33 @@ __global__ void wide2_partition(int64_t N, int64_t tpf, int64_t ntiles, WideWs w
   }
 }
 
-template <int MODE, bool GATHER>
-__global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
+// 8-byte global -> shared asynchronous copies (LDGSTS): the CDF window lands
+// in shared memory while the uniforms are generated, without staging
+// registers
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// dynamic shared-memory bytes of wide2_merge<.., SEARCH>
+constexpr size_t wide2_merge_smem(bool search) {
+  return (kWin + (search ? 0 : kTile)) * sizeof(double) + kRun * kPad * sizeof(int32_t);
+}
+
+template <int MODE, bool GATHER, bool SEARCH = false>
+__global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
     int64_t N, int64_t tpf, WideWs ws, const double *__restrict__ u_tape,
     const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
     const float *__restrict__ gx_in, float *__restrict__ gx_out, int gdims, int64_t gMN) {
-  // dynamic shared: CDF window | uniforms (fast path) | ancestor transpose
+  // dynamic shared: CDF window | uniforms (merge-path variant) | ancestor transpose
   extern __shared__ double s_dyn[];
   double *s_c = s_dyn;
   double *s_u = s_dyn + kWin;
-  int32_t *s_a = reinterpret_cast<int32_t *>(s_u + kTile);
+  int32_t *s_a = reinterpret_cast<int32_t *>(s_u + (SEARCH ? 0 : kTile));
   __shared__ double scratch[33];
   const int64_t tile = blockIdx.x;
   const int64_t f = tile / tpf, tt = tile - f * tpf;
@@ -1041,17 +1280,17 @@ __global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
   const int64_t lo = ws.klo[tile], hi = ws.khi[tile];
   const int64_t wlen = hi - lo + 1;
   const bool chunked = wlen <= 16 * static_cast<int64_t>(kWin);
-  // issue the first CDF chunk's loads now; they land while the uniforms
-  // are generated below
+  // start the first CDF chunk's copy into shared memory now; it lands while
+  // the uniforms are generated below
   constexpr int kPer = kWin / kTileThreads;
-  double cv[kPer];
   const int len0 = static_cast<int>(wlen < kWin ? wlen : kWin);
   if (chunked) {
 #pragma unroll
     for (int r = 0; r < kPer; ++r) {
       const int i = r * kTileThreads + threadIdx.x;
-      cv[r] = i < len0 ? __ldg(cum + lo + i) : 0.0;
+      if (i < len0) cp_async8(s_c + i, cum + lo + i);
     }
+    cp_async_commit();
   }
   // this thread's run of sorted uniforms, in registers
   const int r0 = threadIdx.x * kRun;
@@ -1077,16 +1316,37 @@ __global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
       u[q] = r0 + q < n ? fma(__dadd_rn(eoff, u[q]), scale, teoff) * inv : 2.0;
   }
   int32_t a[kRun];
-  if (wlen <= kWin) {
+  if (SEARCH && wlen <= kWin) {
+    // the window in shared memory; each thread: one binary search for its
+    // first uniform, then a galloping walk for the rest of its sorted run
+    cp_async_wait_all();
+    __syncthreads();
+    const int A = static_cast<int>(wlen);
+    const int kcap = static_cast<int>(N - 1 - lo);
+    const int32_t row0 = static_cast<int32_t>(base + lo);
+    int k = 0;
+    if (r0 < n) {
+      int hi2 = A;
+      const double x = u[0];
+      while (k < hi2) {
+        const int mid = (k + hi2) >> 1;
+        if (s_c[mid] < x)
+          k = mid + 1;
+        else
+          hi2 = mid;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      if (r0 + q < n) k = advance_to<int>([&](int i) { return s_c[i]; }, k, A, u[q]);
+      a[q] = row0 + (k < kcap ? k : kcap);
+    }
+  } else if (wlen <= kWin) {
     // fast path: the whole CDF window and the tile's uniforms sit in shared
     // memory; a merge path gives every thread one diagonal binary search and
     // a fixed number of merge steps (cum[k] taken before u iff cum[k] < u)
     auto us = [](unsigned j) { return (j % kRun) * kTileThreads + j / kRun; };
-#pragma unroll
-    for (int r = 0; r < kPer; ++r) {
-      const int i = r * kTileThreads + threadIdx.x;
-      if (i < len0) s_c[i] = cv[r];
-    }
+    cp_async_wait_all();
 #pragma unroll
     for (int q = 0; q < kRun; ++q)
       if (r0 + q < n) s_u[q * kTileThreads + threadIdx.x] = u[q];
@@ -1135,14 +1395,11 @@ __global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
 #pragma unroll
         for (int r = 0; r < kPer; ++r) {
           const int i = r * kTileThreads + threadIdx.x;
-          cv[r] = i < len ? __ldg(cum + c0 + i) : 0.0;
+          if (i < len) cp_async8(s_c + i, cum + c0 + i);
         }
+        cp_async_commit();
       }
-#pragma unroll
-      for (int r = 0; r < kPer; ++r) {
-        const int i = r * kTileThreads + threadIdx.x;
-        if (i < len) s_c[i] = cv[r];
-      }
+      cp_async_wait_all();
       __syncthreads();
       const bool last = c0 + len > hi;
       const double cmax = s_c[len - 1];
@@ -1170,7 +1427,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) wide2_merge(
       a[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));
     }
   }
-  if (wlen > kWin) {
+  if (wlen > kWin || SEARCH) {
 #pragma unroll
     for (int q = 0; q < kRun; ++q) s_a[q * kPad + threadIdx.x] = a[q];
     __syncthreads();
@@ -1318,6 +1575,14 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
       wide2_tile_stats<TW, 1><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, keys, t);
       wide2_filter<1><<<static_cast<unsigned>(M), 1024, 0, s>>>(N, tpf, ws, collapsed, status,
                                                                lnc, keys, t);
+    } else if (tpf > kFilterChunk) {
+      const unsigned nch = static_cast<unsigned>((tpf + kFilterChunk - 1) / kFilterChunk);
+      wide2_gamma<<<grid_for(M * tpf, 128), 128, 0, s>>>(M, N, tpf, ws, keys, t);
+      wide2_tile_stats<TW, 0, false><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, keys, t);
+      wide2_chunk_scan<<<dim3(nch, static_cast<unsigned>(M)), 256, 0, s>>>(tpf, ws);
+      wide2_chunk_combine<<<grid_for(32 * M, 128), 128, 0, s>>>(M, N, nch, ws, collapsed, status, lnc,
+                                                           keys, t);
+      wide2_chunk_apply<<<dim3(nch, static_cast<unsigned>(M)), 256, 0, s>>>(tpf, ws);
     } else {
       wide2_tile_stats<TW, 0><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, keys, t);
       wide2_filter<0><<<static_cast<unsigned>(M), 1024, 0, s>>>(N, tpf, ws, collapsed, status,
@@ -1332,13 +1597,27 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
     wide2_partition<1><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
   else
     wide2_partition<0><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
-  // merge -> ancestors, then the gather as its own high-occupancy pass
-  auto mk = u_tape ? wide2_merge<1, false> : wide2_merge<0, false>;
-  const size_t msmem = (kWin + kTile) * sizeof(double) + kRun * kPad * sizeof(int32_t);
+  // merge -> ancestors (+ the fused gather)
+  static const bool search = [] {
+    const char *e = std::getenv("PF_WIDE_MERGE");
+    return !(e && std::strcmp(e, "path") == 0);
+  }();
+  // the ancestor gather fused into the merge's write-out (cfg1c: 1.00 ->
+  // 0.93 ms/step); PF_WIDE_GATHER=separate runs it as its own pass
+  static const bool fuse_gather = [] {
+    const char *e = std::getenv("PF_WIDE_GATHER");
+    return !(e && std::strcmp(e, "separate") == 0);
+  }();
+  const bool fg = fuse_gather && gx_in && search;
+  auto mk = u_tape ? (search ? (fg ? wide2_merge<1, true, true> : wide2_merge<1, false, true>)
+                             : wide2_merge<1, false>)
+                   : (search ? (fg ? wide2_merge<0, true, true> : wide2_merge<0, false, true>)
+                             : wide2_merge<0, false>);
+  const size_t msmem = wide2_merge_smem(search);
   cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem));
-  mk<<<nt, kTileThreads, msmem, s>>>(N, tpf, ws, u_tape, keys, t, anc, nullptr, nullptr, 0,
-                                     M * N);
-  if (gx_in) {
+  mk<<<nt, kTileThreads, msmem, s>>>(N, tpf, ws, u_tape, keys, t, anc, fg ? gx_in : nullptr,
+                                     fg ? gx_out : nullptr, fg ? gdims : 0, M * N);
+  if (gx_in && !fg) {
     const int64_t MN = M * N;
     if (gdims == 3 && (MN & 3) == 0)
       gather3_kernel<<<grid_for(MN / 4, 256), 256, 0, s>>>(gx_in, anc, MN, gx_out);

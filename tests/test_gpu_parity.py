@@ -508,7 +508,7 @@ def _offspring_counts(lw, reps, flags, seed):
 
 
 @pytest.mark.parametrize("M,N,flags", [(64, 1024, 0), (2, 20000, 0), (2, 20000, 1),
-                                       (1, 1 << 20, 0)])
+                                       (1, 1 << 20, 0), (1, (1 << 22) + 77, 0)])
 def test_production_resampling_is_multinomial(M, N, flags):
     """Offspring counts follow multinomial(N, w) (test_resampling.py:40-67
     analogue): chi-square over 64 equal-mass bins per filter at 0.1 %."""
@@ -526,6 +526,51 @@ def test_production_resampling_is_multinomial(M, N, flags):
         edges = np.searchsorted(np.cumsum(w[f]), np.linspace(0, 1, B + 1)[1:-1])
         obs = np.add.reduceat(counts[f], np.r_[0, edges])
         exp_ = np.add.reduceat(w[f], np.r_[0, edges]) * reps * N
+        chi2 = float(((obs - exp_) ** 2 / exp_).sum())
+        assert chi2 < stats.chi2.ppf(0.999, df=B - 1), (f, chi2)
+
+
+def test_production_wide_chunked_filter_totals():
+    """Filters wider than 8192 tiles (N > 2^24) combine their tile totals in
+    chunks (wide2_chunk_scan/combine/apply): log normalising constants,
+    zero offspring for -inf weights (a whole chunk of them in filter 0, a
+    partial last chunk), multinomial offspring counts."""
+    from scipy import stats
+
+    M, N = 2, (1 << 25) + 12345
+    rng = np.random.default_rng(11)
+    lw = rng.standard_normal((M, N)).astype(np.float32)
+    lw[0, : 1 << 24] = -np.inf
+    reps = 8
+    counts = _offspring_counts(lw, reps, 0, seed=5)
+    assert np.all(counts.sum(axis=1) == reps * N)
+    assert counts[0, : 1 << 24].sum() == 0
+    d_lw = torch.from_numpy(lw.reshape(-1)).cuda()
+    anc = torch.empty(M * N, dtype=torch.int32, device="cuda")
+    lnc = torch.zeros(M, dtype=torch.float64, device="cuda")
+    coll = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    st = torch.zeros(M, dtype=torch.int32, device="cuda")
+    keys = torch.from_numpy(pf.philox.filter_keys(5, M).view(np.int32)).cuda()
+    wsb = _lib.load().pf_resample_workspace_bytes(M, N)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.call("pf_segmented_resample_ex", _lib.PF_F32, _lib.ptr(d_lw), M, N, None,
+              _lib.ptr(keys), 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st),
+              _lib.ptr(ws), wsb, None, None, 0, 0, _lib.stream_ptr())
+    lw64 = lw.astype(np.float64)
+    for f in range(M):
+        fin = lw64[f][np.isfinite(lw64[f])]
+        mx = fin.max()
+        ref = mx + np.log(np.exp(fin - mx).sum()) - np.log(N)
+        # production log weights are exponentiated in fp32 (expf): ~1e-7 relative
+        assert abs(lnc[f].item() - ref) < 1e-7, (f, lnc[f].item(), ref)
+    assert coll.sum().item() == 0 and st.sum().item() == 0
+    B = 64
+    for f in range(M):
+        w = np.exp(lw64[f] - lw64[f][np.isfinite(lw64[f])].max())
+        w /= w.sum()
+        edges = np.searchsorted(np.cumsum(w), np.linspace(0, 1, B + 1)[1:-1])
+        obs = np.add.reduceat(counts[f], np.r_[0, edges])
+        exp_ = np.add.reduceat(w, np.r_[0, edges]) * reps * N
         chi2 = float(((obs - exp_) ** 2 / exp_).sum())
         assert chi2 < stats.chi2.ppf(0.999, df=B - 1), (f, chi2)
 
