@@ -52,6 +52,21 @@ __device__ __forceinline__ double block_max(double v, double *scratch) {
   return r;
 }
 
+// fp32 block max (scratch >= 32 floats); every warp reduces the partials
+__device__ __forceinline__ float block_max_f(float v, float *scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  float x = lane < nw ? scratch[lane] : -INFINITY;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  __syncthreads();
+  return x;
+}
+
 __device__ __forceinline__ int block_or(int v, double *scratch) {
   return __syncthreads_or(v);
 }

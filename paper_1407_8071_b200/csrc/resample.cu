@@ -170,13 +170,43 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
   const int64_t base = f * N;
   const int i0 = tid * IPT;
 
+  // Production draws on fp32 log-weights (kFastExp) stay in fp32 through
+  // the max, expf and the thread's running sum (the input's own rounding,
+  // |lw| * 2^-24 relative, already exceeds these errors); the total, CDF and
+  // uniforms are fp64.  Tape mode and fp64 inputs are fp64 throughout.
+  constexpr bool kFastExp = MODE == 0 && std::is_same<TW, float>::value;
   // 1. load + max (NaN detection: np.max propagates NaN, core.py:132)
   double lw[IPT];
+  float lf[IPT];
   double mx = -INFINITY;
   int nan = 0;
   // VEC: whole runs in range and 16-byte aligned -> vector loads/stores
   // (fully coalesced: consecutive lanes own consecutive runs)
   const bool vec = (IPT % 4 == 0) && (N % IPT == 0) && sizeof(TW) == 4 && ((base & 3) == 0);
+  double m;
+  if constexpr (kFastExp) {
+    if (vec && i0 < N) {
+#pragma unroll
+      for (int q = 0; q < IPT; q += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(logw + base + i0 + q));
+        lf[q] = v.x;
+        lf[q + 1] = v.y;
+        lf[q + 2] = v.z;
+        lf[q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < IPT; ++q) lf[q] = i0 + q < N ? __ldg(logw + base + i0 + q) : -INFINITY;
+    }
+    float mf = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      nan |= isnan(lf[q]);
+      mf = fmaxf(mf, lf[q]);
+    }
+    nan = __syncthreads_or(nan);
+    m = static_cast<double>(block_max_f(mf, reinterpret_cast<float *>(scratch)));
+  } else {
   if (vec && i0 < N) {
 #pragma unroll
     for (int q = 0; q < IPT; q += 4) {
@@ -200,7 +230,8 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
     mx = fmax(mx, lw[q]);
   }
   nan = __syncthreads_or(nan);
-  const double m = block_max(mx, scratch);
+  m = block_max(mx, scratch);
+  }
   if (nan || m == -INFINITY) {
     // NaN -> ValueError on the host; total underflow -> collapse: identity
     // ancestors, lnc unchanged (filters.py:105-109)
@@ -223,30 +254,36 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
     return;
   }
 
-  // 2. e = exp(lw - m) and the total (core.py:134-135).  Production draws
-  // on fp32 log-weights evaluate exp in fp32: the input's own rounding
-  // (|lw| * 2^-24 relative) already exceeds expf's error, and the sums, CDF
-  // and uniforms stay fp64.  Tape mode and fp64 inputs keep fp64 exp.
-  constexpr bool kFastExp = MODE == 0 && std::is_same<TW, float>::value;
-  double part = 0.0;
-#pragma unroll
-  for (int q = 0; q < IPT; ++q) {
-    if (kFastExp)
-      lw[q] = i0 + q < N ? static_cast<double>(expf(static_cast<float>(lw[q] - m))) : 0.0;
-    else
-      lw[q] = i0 + q < N ? exp(__dsub_rn(lw[q], m)) : 0.0;
-    part = __dadd_rn(part, lw[q]);
-  }
-  const double total = block_sum(part, scratch);
-
+  // 2. e = exp(lw - m) and the total (core.py:134-135)
   // 3. w = e / total (IEEE division, core.py:136; production fp32 inputs:
   // reciprocal multiply), CDF = offset + local run
-  double run = 0.0;
-  const double inv_total = kFastExp ? 1.0 / total : 0.0;
+  double total, run = 0.0;
+  if constexpr (kFastExp) {
+    const float mf = static_cast<float>(m);
+    float pf = 0.f;  // running sum of the thread's expf(lw - m)
 #pragma unroll
-  for (int q = 0; q < IPT; ++q) {
-    run = __dadd_rn(run, kFastExp ? lw[q] * inv_total : __ddiv_rn(lw[q], total));
-    lw[q] = run;  // local inclusive prefix
+    for (int q = 0; q < IPT; ++q) {
+      pf += expf(lf[q] - mf);  // padding: expf(-inf) = 0
+      lw[q] = static_cast<double>(pf);
+    }
+    total = block_sum(static_cast<double>(pf), scratch);
+    const double inv_total = 1.0 / total;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) lw[q] *= inv_total;  // local inclusive prefix
+    run = lw[IPT - 1];
+  } else {
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      lw[q] = i0 + q < N ? exp(__dsub_rn(lw[q], m)) : 0.0;
+      part = __dadd_rn(part, lw[q]);
+    }
+    total = block_sum(part, scratch);
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      run = __dadd_rn(run, __ddiv_rn(lw[q], total));
+      lw[q] = run;  // local inclusive prefix
+    }
   }
   double wtot;
   const double off = block_exclusive_scan(run, scratch, &wtot);
@@ -1533,7 +1570,6 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
 #undef PF_PICK
     // thread-major CDF slots: THREADS * IPT doubles (>= N)
     const int ipt = N <= 256 ? 2 : N <= 512 ? 4 : N <= 1024 ? 8 : N <= 2048 ? 8 : 16;
-    // shared: CDF and uniforms (fp64) + ancestors (int32), THREADS * IPT slots each
     const size_t smem = static_cast<size_t>(threads) * ipt * (2 * sizeof(double) + 4);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
