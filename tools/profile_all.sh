@@ -15,7 +15,7 @@ cap lorenz_fast_cfg2 lorenz_fast_kernel cfg2 ""
 cap resample_bank_cfg1b resample_bank_kernel cfg1b ""
 cap wide2_merge_cfg1c wide2_merge cfg1c ""
 cap fhnnet_fast_net fhnnet_fast_kernel net ""
-for c in cfg4 cfg2 cfg1c net; do
+for c in cfg4 cfg2 cfg1b cfg1c net cfg2apf netapf; do
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none -c 80 --csv --log-file $out/launches_$c.csv \
     python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline --profile \
