@@ -261,14 +261,24 @@ struct FhnFast {
 // PP particles are advanced together by the same threads (independent
 // dependency chains -> more ILP per warp, one barrier per Euler step for
 // all PP particles).
+// Row pitch of the shared v plane: no ghost columns (edge threads read
+// themselves, Neumann "ghost = self"), and chosen so that a warp spanning two
+// strips (rows R apart) hits 32 distinct banks: R*W - COLS == 0 (mod 32)
+// (30x50, R=6: W = 51).
+__host__ __device__ constexpr int fhn_pitch(int cols, int r) {
+  for (int w = cols; w < cols + 32; ++w)
+    if ((r * w - cols) % 32 == 0) return w;
+  return cols;
+}
+
 template <int ROWS, int COLS, int R, bool TAPE, int MINB, int PP, bool NF = false>
 __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
     const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
     int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
     const double *__restrict__ tape, uint32_t *__restrict__ status) {
-  constexpr int W = COLS + 2;
-  constexpr int P = (ROWS + 2) * W;
+  constexpr int W = fhn_pitch(COLS, R);
+  constexpr int P = (ROWS + 2) * W;  // + a spare row above and below
   constexpr int NSEG = (ROWS + R - 1) / R;
   constexpr int NODES = ROWS * COLS;
   static_assert(R % 2 == 0, "rows per thread must be even (Philox row pairs)");
@@ -280,9 +290,10 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
   const int col = tid - seg * COLS;
   const bool active = seg < NSEG;
   const int row0 = seg * R;
-  // horizontal ghost target: the mirrored cell for edge columns, else self
-  const int hg = col == 0 ? -1 : (col == COLS - 1 ? 1 : 0);
-  const int base = (row0 + 1) * W + col + 1;  // this thread's first cell
+  // horizontal neighbours; an edge column reads itself (ghost = self)
+  const int lo = col == 0 ? 0 : -1;
+  const int ro = col == COLS - 1 ? 0 : 1;
+  const int base = (row0 + 1) * W + col;  // this thread's first cell
 
   for (int64_t pb = static_cast<int64_t>(blockIdx.x) * PP; pb < MN;
        pb += static_cast<int64_t>(gridDim.x) * PP) {
@@ -308,11 +319,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
           const int node = (row0 + r) * COLS + col;
           v[e][r] = __ldg(xs + node);
           w[e][r] = __ldg(xs + NODES + node);
-          float *cell = vsp + e * 2 * P + base + r * W;
-          cell[0] = v[e][r];
-          cell[hg] = v[e][r];
-          if (r == 0 && row0 == 0) cell[-W] = v[e][r];
-          if (row0 + r == ROWS - 1) cell[W] = v[e][r];
+          vsp[e * 2 * P + base + r * W] = v[e][r];
         }
       }
     }
@@ -328,7 +335,8 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
         for (int e = 0; e < PP; ++e) {
           const float *cur = vsp + e * 2 * P + (k & 1) * P + base;
           float *nxt = vsp + e * 2 * P + ((k & 1) ^ 1) * P + base;
-          float up = cur[-W];  // old value of the row above this strip
+          // old value of the row above this strip (the top row: itself)
+          float up = row0 == 0 ? v[e][0] : cur[-W];
 #pragma unroll
           for (int q = 0; q < R / 2; ++q) {
             float zv0, zw0, zv1, zw1;
@@ -361,19 +369,15 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
               if (row0 + r < ROWS) {
                 const float *cell = cur + r * W;
                 const float u = v[e][r];
-                const float dn = (r < R - 1 && row0 + r + 1 < ROWS) ? v[e][r + 1] : cell[W];
-                const float nb = ((up + dn) + cell[-1]) + cell[1];
+                const float dn = row0 + r == ROWS - 1 ? u : (r < R - 1 ? v[e][r + 1] : cell[W]);
+                const float nb = ((up + dn) + cell[lo]) + cell[ro];
                 const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
                 // u + dt(p3 - w) + dt*coupling*(nb - 4u) + sig_v*zv
                 float un = fmaf(c.dt, p3 - w[e][r], u);
                 un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
                 un = fmaf(sv, h ? zv1 : zv0, un);
                 w[e][r] = fmaf(sw, h ? zw1 : zw0, fmaf(c.wc, w[e][r], fmaf(c.uc, u, c.c0)));
-                float *dst = nxt + r * W;
-                dst[0] = un;
-                dst[hg] = un;
-                if (r == 0 && row0 == 0) dst[-W] = un;
-                if (row0 + r == ROWS - 1) dst[W] = un;
+                nxt[r * W] = un;
                 up = u;
                 v[e][r] = un;
               }
@@ -409,7 +413,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
       for (int i = lane; i < c.n_obs; i += 32) {
         const int n = __ldg(obs_idx + i);
         const int rr = n / COLS;
-        const double rsd = __ldg(y + i) - static_cast<double>(fv[(rr + 1) * W + (n - rr * COLS) + 1]);
+        const double rsd = __ldg(y + i) - static_cast<double>(fv[(rr + 1) * W + (n - rr * COLS)]);
         acc = fma(rsd, rsd, acc);
       }
 #pragma unroll
@@ -508,7 +512,7 @@ static int launch_fhn_fast_t(const FhnFast &fc, const void *x_in, const int32_t 
                              uint32_t *status, cudaStream_t s) {
   constexpr int threads = (((ROWS + R - 1) / R * COLS) + 31) / 32 * 32;
   static_assert(threads <= 256, "lattice too large for the fast kernel");
-  const size_t smem = PP * 2 * static_cast<size_t>((ROWS + 2) * (COLS + 2)) * sizeof(float);
+  const size_t smem = PP * 2 * static_cast<size_t>((ROWS + 2) * fhn_pitch(COLS, R)) * sizeof(float);
   auto kern = fhn_fast_kernel<ROWS, COLS, R, TAPE, MINB, PP, NF>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
