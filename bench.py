@@ -397,7 +397,7 @@ def run_resample(args, cfg):
                        "pf_segmented_resample_ex (wide pipeline: tile stats, filter totals, "
                        "tile CDF, partition, merge, fused gather)"),
             "algorithmic": f"{RESAMPLE_BYTES_PER_PARTICLE:.0f} B/particle x {MN} particles",
-            "traffic": _ncu_traffic(args.config)}
+            "traffic": _ncu_traffic(args.config), "ncu_pipes": _ncu_pipes(args.config)}
     # e2e: host logw in (pinned), host ancestors out, through the C ABI.  A bank
     # of many filters is streamed in filter chunks on three streams (H2D of
     # chunk c+1 and D2H of chunk c-1 overlap the resample of chunk c; PCIe is
@@ -550,6 +550,7 @@ def run_ours(args, cfg):
     roof["kernel_ms"] = kern_ms
     roof["kernel_share_of_step"] = kern_share
     roof["traffic"] = _ncu_traffic(args.config)
+    roof["ncu_pipes"] = _ncu_pipes(args.config)
 
     # e2e through the public API (host observations in, host results out)
     if args.profile:
@@ -746,6 +747,18 @@ def _state_bytes(model):
 def _ncu_traffic(config):
     try:
         with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(config)
+    except OSError:
+        return None
+
+
+def _ncu_pipes(config):
+    """Pipe utilisation of the workload's dominant kernel from the committed
+    ncu capture (profiles/pipes.json): the issue/FMA-pipe evidence behind a
+    low algorithmic-flop fraction (cfg2: the Gaussian draws, not the 20
+    flop/particle-step of the dynamics, fill the pipes)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "pipes.json")) as fh:
             return json.load(fh).get(config)
     except OSError:
         return None
