@@ -368,7 +368,20 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
       for (int q = 0; q < IPT; q += 4)
         *reinterpret_cast<int4 *>(anc + base + i0 + q) =
             make_int4(av[q], av[q + 1], av[q + 2], av[q + 3]);
-      if (GATHER) {
+      if (GATHER && gdims == 3) {
+        // 3-float state (cfg1): all 3*IPT gathered loads in flight first
+        float g[3][IPT];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int q = 0; q < IPT; ++q) g[d][q] = __ldg(gx_in + d * gMN + av[q]);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int q = 0; q < IPT; q += 4)
+            *reinterpret_cast<float4 *>(gx_out + d * gMN + base + i0 + q) =
+                make_float4(g[d][q], g[d][q + 1], g[d][q + 2], g[d][q + 3]);
+      } else if (GATHER) {
         for (int d = 0; d < gdims; ++d) {
           const float *src = gx_in + d * gMN;
           float *dst = gx_out + d * gMN + base + i0;
@@ -1468,6 +1481,31 @@ __global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
 #pragma unroll
     for (int q = 0; q < kRun; ++q) s_a[q * kPad + threadIdx.x] = a[q];
     __syncthreads();
+  }
+  if (GATHER && gdims == 3) {
+    // the 3-float state (cfg1): all 24 gathered loads of the thread's 8
+    // outputs in flight before the first store
+    int32_t ai[kRun];
+#pragma unroll
+    for (int h = 0; h < kRun; ++h) {
+      const int e = threadIdx.x + h * kTileThreads;
+      ai[h] = e < n ? s_a[(e % kRun) * kPad + e / kRun] : 0;
+      if (e < n) anc[base + i0 + e] = ai[h];
+    }
+    float v[3][kRun];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int h = 0; h < kRun; ++h)
+        v[d][h] = threadIdx.x + h * kTileThreads < n ? __ldg(gx_in + d * gMN + ai[h]) : 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int h = 0; h < kRun; ++h) {
+        const int e = threadIdx.x + h * kTileThreads;
+        if (e < n) gx_out[d * gMN + base + i0 + e] = v[d][h];
+      }
+    return;
   }
   // coalesced write-out (thread-strided elements), gather loads batched 4 deep
   for (int e0 = threadIdx.x; e0 < n; e0 += 4 * kTileThreads) {
