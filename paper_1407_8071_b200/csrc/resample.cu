@@ -28,6 +28,15 @@
 namespace pf {
 
 constexpr int kBankMaxN = 8192;
+
+// Production fp32 log weights: exp(x) = 2^(x log2 e) on the MUFU
+// (ex2.approx.ftz; relative error <= ~2^-21 + |x| 2^-24, below the input's own
+// fp32 rounding of |lw| 2^-24); exp(-inf) = 0.
+__device__ __forceinline__ float exp_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  return y;
+}
 constexpr int kBankThreads = 256;
 constexpr int kTile = 2048;          // wide path elements per tile
 constexpr int kTileThreads = 256;
@@ -260,10 +269,10 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
   double total, run = 0.0;
   if constexpr (kFastExp) {
     const float mf = static_cast<float>(m);
-    float pf = 0.f;  // running sum of the thread's expf(lw - m)
+    float pf = 0.f;  // running sum of the thread's exp(lw - m)
 #pragma unroll
     for (int q = 0; q < IPT; ++q) {
-      pf += expf(lf[q] - mf);  // padding: expf(-inf) = 0
+      pf += exp_fast(lf[q] - mf);  // padding: exp(-inf) = 0
       lw[q] = static_cast<double>(pf);
     }
     total = block_sum(static_cast<double>(pf), scratch);
@@ -677,8 +686,9 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restri
   const int r0 = threadIdx.x * kRun;
   double v[kRun];
   double run = 0.0;
-  if constexpr (FAST && std::is_same<TW, float>::value) {
-    // production fp32: w = expf(lw - tile max), an fp32 running sum over the
+  static_assert(!FAST || std::is_same<TW, float>::value, "FAST: fp32 log weights only");
+  if constexpr (FAST) {
+    // production fp32: w = exp(lw - tile max), an fp32 running sum over the
     // thread's run (the same association wide2_tile_stats sums in), scaled by
     // exp(tile max - max) / total in fp64 (see wide2_tile_stats)
     float lf[kRun];
@@ -690,26 +700,10 @@ __global__ void __launch_bounds__(kTileThreads) wide_tile_cum(const TW *__restri
     float pf = 0.f;
 #pragma unroll
     for (int q = 0; q < kRun; ++q) {
-      if (live) pf += expf(lf[q] - mtf);  // padding: expf(-inf) = 0
+      if (live) pf += exp_fast(lf[q] - mtf);  // padding: exp(-inf) = 0
       v[q] = static_cast<double>(pf) * scale;
     }
     run = v[kRun - 1];
-  } else if (FAST) {
-    load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, v);
-    // w = expf(lw - tile max) * exp(tile max - max) / total (see wide2_tile_stats)
-    // a tile of -inf log weights has tmax = -inf: all its weights are 0
-    // (expf(-inf - -inf) would be NaN)
-    const double mt = ws.tmax[tile];
-    const bool live = mt != -INFINITY;
-    const double scale = live ? exp(__dsub_rn(mt, m)) / total : 0.0;
-#pragma unroll
-    for (int q = 0; q < kRun; ++q) {
-      const double w = (live && r0 + q < n)
-                           ? static_cast<double>(expf(static_cast<float>(v[q] - mt))) * scale
-                           : 0.0;
-      run = __dadd_rn(run, w);
-      v[q] = run;
-    }
   } else {
     load_run(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, v);
 #pragma unroll
@@ -971,12 +965,12 @@ __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
       mxf = fmaxf(mxf, lf[q]);
     }
     nanf = __syncthreads_or(nanf);
-    const double mt = block_max(static_cast<double>(mxf), scratch);
+    const double mt = block_max_f(mxf, reinterpret_cast<float *>(scratch));
     float pf = 0.f;
     if (mt != -INFINITY) {
       const float mtf = static_cast<float>(mt);
 #pragma unroll
-      for (int q = 0; q < kRun; ++q) pf += expf(lf[q] - mtf);
+      for (int q = 0; q < kRun; ++q) pf += exp_fast(lf[q] - mtf);
     }
     const double ssum = block_sum(static_cast<double>(pf), scratch);
     if (threadIdx.x == 0) {
@@ -1001,15 +995,10 @@ __global__ void __launch_bounds__(kTileThreads) wide2_tile_stats(
   nan = __syncthreads_or(nan);
   const double m = block_max(mx, scratch);
   double part = 0.0;
-  if (m != -INFINITY) {
-    // production fp32 log-weights: fp32 exp against the TILE max; the CDF
-    // pass (wide_tile_cum<.., true>) recomputes exactly these values, so the
-    // tile totals and the in-tile CDF stay consistent to fp64 rounding
+  if (m != -INFINITY) {  // fp64 exp against the tile max (tape mode, fp64 inputs)
 #pragma unroll
     for (int q = 0; q < kRun; ++q)
-      part = __dadd_rn(part, (MODE == 0 && std::is_same<TW, float>::value)
-                                 ? static_cast<double>(expf(static_cast<float>(lv[q] - m)))
-                                 : exp(__dsub_rn(lv[q], m)));
+      part = __dadd_rn(part, exp(__dsub_rn(lv[q], m)));
   }
   const double ssum = block_sum(part, scratch);
   if (threadIdx.x == 0) {
@@ -1662,10 +1651,14 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
       wide2_filter<0><<<static_cast<unsigned>(M), 1024, 0, s>>>(N, tpf, ws, collapsed, status,
                                                                lnc, keys, t);
     }
-    if (!u_tape && std::is_same<TW, float>::value)
-      wide_tile_cum<TW, true><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
-    else
+    if constexpr (std::is_same<TW, float>::value) {
+      if (!u_tape)
+        wide_tile_cum<TW, true><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+      else
+        wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+    } else {
       wide_tile_cum<TW><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
+    }
   }
   if (u_tape)
     wide2_partition<1><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
