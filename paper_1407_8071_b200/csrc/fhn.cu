@@ -15,6 +15,7 @@
 // store), i.e. 50x less traffic than streaming every Euler step, which
 // turns the kernel from HBM-bound into issue-bound (RNG dominated).
 #include "common.cuh"
+#include <type_traits>
 #include "philox.cuh"
 
 namespace pf {
@@ -325,43 +326,60 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
     }
     __syncthreads();
 
-    // Philox normals come out of box_muller_fast_unscaled: fold sqrt(2 ln 2)
-    const float sv = TAPE ? c.sig_v : c.sig_v * kSqrt2Ln2;
-    const float sw = TAPE ? c.sig_w : c.sig_w * kSqrt2Ln2;
+    // Philox: the per-thread, step-independent part of each row pair's
+    // counter (je, step, node_pair, purpose) is hoisted out of the Euler
+    // loop (philox_pre_t); each pair's two Box-Muller draws give the v
+    // increments of rows 2q, 2q+1 (radius scaled by sig_v) and the w
+    // increments (radius scaled by sig_w): one FFMA per increment.
+    const float s2v = -1.3862943611198906f * c.sig_v * c.sig_v;
+    const float s2w = -1.3862943611198906f * c.sig_w * c.sig_w;
+    PhiloxPreT pre[PP][R / 2];
+    PhiloxUni uni[PP];
+    if (!TAPE && !NF) {
+#pragma unroll
+      for (int e = 0; e < PP; ++e) {
+        uni[e] = philox_uni_t(je[e], kPurposeFhn, key[e]);
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q)
+          pre[e][q] = philox_pre_t(je[e], static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col),
+                                   kPurposeFhn, key[e]);
+      }
+    }
     const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
-    for (int k = 0; k < c.n_sub; ++k) {
+    // one Euler step from plane PAR to plane PAR^1 (parity static: every
+    // shared address is base + immediate)
+    auto euler = [&](int k, auto par_c) {
+      constexpr int PAR = decltype(par_c)::value;
       if (active) {
 #pragma unroll
         for (int e = 0; e < PP; ++e) {
-          const float *cur = vsp + e * 2 * P + (k & 1) * P + base;
-          float *nxt = vsp + e * 2 * P + ((k & 1) ^ 1) * P + base;
+          const float *cur = vsp + e * 2 * P + PAR * P + base;
+          float *nxt = vsp + e * 2 * P + (PAR ^ 1) * P + base;
           // old value of the row above this strip (the top row: itself)
           float up = row0 == 0 ? v[e][0] : cur[-W];
+          const uint32_t c1k0 = (step0 + k) ^ key[e].k0;
 #pragma unroll
           for (int q = 0; q < R / 2; ++q) {
-            float zv0, zw0, zv1, zw1;
+            // v increment of row 2q+h = av * tv[h], w increment = aw * tw[h]
+            float av, aw, tv[2], tw[2];
             if (TAPE) {
               const int64_t b0 =
                   ((fe[e] * c.n_sub + k) * 2 * static_cast<int64_t>(N) + je[e]) * NODES +
                   (row0 + 2 * q) * COLS + col;
               const int64_t wo = static_cast<int64_t>(N) * NODES;
               const bool ok1 = row0 + 2 * q + 1 < ROWS;
-              zv0 = float(tape[b0]);
-              zw0 = float(tape[b0 + wo]);
-              zv1 = ok1 ? float(tape[b0 + COLS]) : 0.f;
-              zw1 = ok1 ? float(tape[b0 + wo + COLS]) : 0.f;
-            } else if (NF) {  // noise-free lookahead: no draws (sig * 0 adds an exact 0)
-              zv0 = zw0 = zv1 = zw1 = 0.f;
+              av = c.sig_v;
+              aw = c.sig_w;
+              tv[0] = float(tape[b0]);
+              tw[0] = float(tape[b0 + wo]);
+              tv[1] = ok1 ? float(tape[b0 + COLS]) : 0.f;
+              tw[1] = ok1 ? float(tape[b0 + wo + COLS]) : 0.f;
+            } else if (NF) {  // noise-free lookahead: no draws (0 * 0 adds an exact 0)
+              av = aw = tv[0] = tv[1] = tw[0] = tw[1] = 0.f;
             } else {
-              const uint32_t node_pair = static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col);
-              const uint4 rr =
-                  philox10(make_uint4(je[e], step0 + k, node_pair, kPurposeFhn), key[e]);
-              const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
-              const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
-              zv0 = g0.x;
-              zw0 = g0.y;
-              zv1 = g1.x;
-              zw1 = g1.y;
+              const uint4 rr = philox10_t(pre[e][q], uni[e], c1k0, key[e]);
+              box_muller_rad_trig(rr.x, rr.y, s2v, av, tv[0], tv[1]);
+              box_muller_rad_trig(rr.z, rr.w, s2w, aw, tw[0], tw[1]);
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -375,8 +393,8 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
                 // u + dt(p3 - w) + dt*coupling*(nb - 4u) + sig_v*zv
                 float un = fmaf(c.dt, p3 - w[e][r], u);
                 un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
-                un = fmaf(sv, h ? zv1 : zv0, un);
-                w[e][r] = fmaf(sw, h ? zw1 : zw0, fmaf(c.wc, w[e][r], fmaf(c.uc, u, c.c0)));
+                un = fmaf(av, tv[h], un);
+                w[e][r] = fmaf(aw, tw[h], fmaf(c.wc, w[e][r], fmaf(c.uc, u, c.c0)));
                 nxt[r * W] = un;
                 up = u;
                 v[e][r] = un;
@@ -386,7 +404,13 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
         }
       }
       __syncthreads();
+    };
+    int k = 0;
+    for (; k + 1 < c.n_sub; k += 2) {
+      euler(k, std::integral_constant<int, 0>{});
+      euler(k + 1, std::integral_constant<int, 1>{});
     }
+    if (k < c.n_sub) euler(k, std::integral_constant<int, 0>{});
 
     // epilogue: divergence flag, store, electrode log-likelihood
 #pragma unroll

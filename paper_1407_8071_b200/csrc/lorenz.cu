@@ -25,6 +25,7 @@ struct LorenzConsts {
   double s, r, b, dt, dts, sq, ns, two_obs_var;
   int n_sub;
   float f_dt, f_ndts, f_r, f_nb, f_cz;  // fp32 production constants (host-folded)
+  float f_s2;                           // -(2 ln 2) * (sqrt(dt) * noise_scale)^2
 };
 
 // One Euler-Maruyama substep in the reference's evaluation order
@@ -155,81 +156,66 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
 }
 
 // fp32 production kernel (Philox): constants host-folded, unpredicated
-// 4-substep chunks (12 normals = 3 Philox blocks).  PP > 1 advances several
-// particles per thread (strided by the block size, loads stay coalesced);
-// measured slower on B200 (the kernel is issue/XU-bound, not latency-bound),
-// so the launcher uses PP = 1.
-template <int PP>
+// 4-substep chunks (12 normals = 3 Philox blocks = 6 Box-Muller pairs).  The
+// noise scale is folded into each pair's radius (cz*z = r'*cos with
+// r' = sqrt(-log2(u) * 2 ln2 * cz^2)), so an increment costs one FFMA.
+// UKEY: every block lies inside one filter (N % 256 == 0), so the filter id,
+// its Philox key and the key schedule are block-uniform and live in uniform
+// registers; the first two Philox rounds then depend only on uniform or
+// loop-invariant words and leave the per-substep path (same draws, same
+// arithmetic as UKEY=false).
+template <bool UKEY>
 __global__ void __launch_bounds__(256) lorenz_fast_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
     const double *__restrict__ y, float *__restrict__ logw, int64_t MN, int32_t N, int obs_dim,
     LorenzConsts c, const uint32_t *__restrict__ keys, uint32_t t,
     uint32_t *__restrict__ status) {
-  const int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x) * PP + threadIdx.x;
-  float a1[PP], a2[PP], a3[PP];
-  Key2 key[PP];
-  uint32_t jj[PP];
-  int64_t ff[PP];
-#pragma unroll
-  for (int e = 0; e < PP; ++e) {
-    int64_t p = base + static_cast<int64_t>(e) * blockDim.x;
-    if (p >= MN) p = MN - 1;  // tail: recompute the last particle, no store
-    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
-    a1[e] = xin[src];
-    a2[e] = xin[MN + src];
-    a3[e] = xin[2 * MN + src];
-    ff[e] = p / N;
-    jj[e] = static_cast<uint32_t>(p - ff[e] * N);
-    key[e] = load_key(keys, ff[e]);
-  }
-  const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb, cz = c.f_cz;
+  int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool live = p < MN;
+  if (!UKEY && !live) p = MN - 1;  // tail: recompute the last particle, no store
+  const int64_t f = UKEY ? (static_cast<int64_t>(blockIdx.x) * 256) / N : p / N;
+  const uint32_t j = static_cast<uint32_t>(p - f * N);
+  const Key2 key = load_key(keys, f);
+  const PhiloxPre pre = philox_pre(j, kPurposeLorenz, key);
+  const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+  float x1 = xin[src], x2 = xin[MN + src], x3 = xin[2 * MN + src];
+  const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb, s2 = c.f_s2;
   const int nfull = c.n_sub >> 2;
   for (int k4 = 0; k4 <= nfull; ++k4) {
     const int left = c.n_sub - 4 * k4;
     if (left <= 0) break;
-    float z[PP][12];
+    float rad[6], tr[12];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-#pragma unroll
-      for (int e = 0; e < PP; ++e) {
-        const uint4 rr = philox10(
-            make_uint4(jj[e], t, static_cast<uint32_t>(k4 * 3 + q), kPurposeLorenz), key[e]);
-        const float2 g0 = box_muller_fast_unscaled(rr.x, rr.y);
-        const float2 g1 = box_muller_fast_unscaled(rr.z, rr.w);
-        z[e][4 * q + 0] = g0.x;
-        z[e][4 * q + 1] = g0.y;
-        z[e][4 * q + 2] = g1.x;
-        z[e][4 * q + 3] = g1.y;
-      }
+      const uint4 rr = philox10_split(pre, t, static_cast<uint32_t>(k4 * 3 + q), key);
+      box_muller_rad_trig(rr.x, rr.y, s2, rad[2 * q], tr[4 * q], tr[4 * q + 1]);
+      box_muller_rad_trig(rr.z, rr.w, s2, rad[2 * q + 1], tr[4 * q + 2], tr[4 * q + 3]);
     }
+    auto sub = [&](int n0) {  // normals n0..n0+2: pair n/2, trig factor n
+      const float n1 = fmaf(rad[n0 >> 1], tr[n0], fmaf(ndts, x1 - x2, x1));
+      const float t2 = fmaf(-x1, x3, fmaf(r, x1, -x2));
+      const float m2 = fmaf(rad[(n0 + 1) >> 1], tr[n0 + 1], fmaf(dt, t2, x2));
+      const float t3 = fmaf(nb, x3, x1 * x2);
+      const float m3 = fmaf(rad[(n0 + 2) >> 1], tr[n0 + 2], fmaf(dt, t3, x3));
+      x1 = n1;
+      x2 = m2;
+      x3 = m3;
+    };
     if (left >= 4) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int e = 0; e < PP; ++e)
-          lorenz_substep_fast(a1[e], a2[e], a3[e], z[e][3 * q], z[e][3 * q + 1], z[e][3 * q + 2],
-                              dt, ndts, r, nb, cz);
+      for (int q = 0; q < 4; ++q) sub(3 * q);
     } else {
 #pragma unroll
       for (int q = 0; q < 3; ++q)
-        if (q < left)
-#pragma unroll
-          for (int e = 0; e < PP; ++e)
-            lorenz_substep_fast(a1[e], a2[e], a3[e], z[e][3 * q], z[e][3 * q + 1],
-                                z[e][3 * q + 2], dt, ndts, r, nb, cz);
+        if (q < left) sub(3 * q);
     }
   }
-#pragma unroll
-  for (int e = 0; e < PP; ++e) {
-    const int64_t p = base + static_cast<int64_t>(e) * blockDim.x;
-    if (p >= MN) continue;
-    if (!(isfinite(a1[e]) && isfinite(a2[e]) && isfinite(a3[e])))
-      atomicOr(status + ff[e], PF_ST_DIVERGED);
-    xout[p] = a1[e];
-    xout[MN + p] = a2[e];
-    xout[2 * MN + p] = a3[e];
-    logw[p] = lorenz_loglik<float>(a1[e], a3[e], y, obs_dim, c.two_obs_var);
-  }
+  if (!live) return;
+  if (!(isfinite(x1) && isfinite(x2) && isfinite(x3))) atomicOr(status + f, PF_ST_DIVERGED);
+  xout[p] = x1;
+  xout[MN + p] = x2;
+  xout[2 * MN + p] = x3;
+  logw[p] = lorenz_loglik<float>(x1, x3, y, obs_dim, c.two_obs_var);
 }
 
 // Noise-free interval (the auxiliary filter's point prediction,
@@ -355,6 +341,7 @@ static LorenzConsts make_consts(const pf_lorenz_params *p) {
   c.f_r = static_cast<float>(c.r);
   c.f_nb = static_cast<float>(-c.b);
   c.f_cz = static_cast<float>(c.sq * c.ns) * kSqrt2Ln2;
+  c.f_s2 = static_cast<float>(-2.0 * std::log(2.0) * (c.sq * c.ns) * (c.sq * c.ns));
   return c;
 }
 
@@ -434,9 +421,12 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
     if (z_tape)
       lorenz_pw_kernel<float, 1><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
                                                       c, keys, t, z_tape, status);
+    else if (N % 256 == 0)
+      lorenz_fast_kernel<true><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim, c,
+                                                    keys, t, status);
     else
-      lorenz_fast_kernel<1><<<grid_for(MN, 256), 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32,
-                                                              p->obs_dim, c, keys, t, status);
+      lorenz_fast_kernel<false><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim, c,
+                                                     keys, t, status);
   }
   return check_launch("pf_lorenz_propagate_weight");
 }

@@ -30,6 +30,106 @@ __device__ __forceinline__ uint4 philox10(uint4 c, Key2 k) {
   return c;
 }
 
+// Philox4x32-10 split for a counter (c0, c1, c2, c3) whose words c0 and c3
+// are fixed for a thread (particle index, purpose tag) while c2 varies (draw
+// index) and c1 is block-uniform (observation time): the parts of rounds 1-2
+// that depend only on (c0, c3, key) are computed once per thread
+// (philox_pre), the rest (philox10_split) is bit-identical to philox10.
+// 32x32 -> 64 product as one IMAD.WIDE.U32 (ptxas otherwise may split the
+// lo/hi halves into IMAD + IMAD.HI, two issue slots).
+__device__ __forceinline__ void mulhilo(uint32_t m, uint32_t a, uint32_t &lo, uint32_t &hi) {
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(m));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
+}
+
+struct PhiloxPre {
+  uint32_t w1, y2, h2;  // round-1 W; round-2 lo/hi of M1 * Z1
+};
+
+__device__ __forceinline__ PhiloxPre philox_pre(uint32_t c0, uint32_t c3, Key2 k) {
+  const uint32_t z1 = __umulhi(0xD2511F53u, c0) ^ c3 ^ k.k1;
+  return PhiloxPre{0xD2511F53u * c0, 0xCD9E8D57u * z1, __umulhi(0xCD9E8D57u, z1)};
+}
+
+__device__ __forceinline__ uint4 philox10_split(const PhiloxPre &pre, uint32_t c1, uint32_t c2,
+                                                Key2 k) {
+  // round 1 (key k): X1 = hi(M1 c2) ^ c1 ^ k0, Y1 = lo(M1 c2), Z1/W1 in pre
+  const uint32_t x1 = __umulhi(0xCD9E8D57u, c2) ^ c1 ^ k.k0;
+  const uint32_t y1 = 0xCD9E8D57u * c2;
+  // round 2 (key k + C)
+  uint32_t k0 = k.k0 + 0x9E3779B9u, k1 = k.k1 + 0xBB67AE85u;
+  uint4 c = make_uint4(pre.h2 ^ y1 ^ k0, pre.y2, __umulhi(0xD2511F53u, x1) ^ pre.w1 ^ k1,
+                       0xD2511F53u * x1);
+#pragma unroll
+  for (int i = 2; i < 10; ++i) {
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+    uint32_t lo0, hi0, lo1, hi1;
+    mulhilo(0xD2511F53u, c.x, lo0, hi0);
+    mulhilo(0xCD9E8D57u, c.z, lo1, hi1);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+
+// Philox4x32-10 for a counter (c0, c1, c2, c3) = (block-uniform particle
+// index, per-step uniform time word, thread-fixed draw index, purpose): the
+// FH-N lattice layout, where only c1 changes from one Euler step to the next.
+// philox_pre_t hoists everything of rounds 1-3 that does not depend on c1
+// (3 words per thread and draw index); philox10_t is bit-identical to
+// philox10(make_uint4(c0, c1, c2, c3), k).
+struct PhiloxPreT {
+  uint32_t h1;        // hi(M1 c2)                      (round 1, X1 = h1 ^ c1 ^ k0)
+  uint32_t lo3, hi3;  // lo/hi(M0 X2), X2 independent of c1 (round 3)
+};
+struct PhiloxUni {    // block-uniform, c1-independent words (uniform registers)
+  uint32_t w1k1;      // W1 ^ (k1 + C1)         (round 2, Z2 = hi(M0 X1) ^ W1 ^ k1')
+  uint32_t y2k0;      // Y2 ^ (k0 + 2 C0)       (round 3, X3 = hi(M1 Z2) ^ Y2 ^ k0'')
+};
+
+__device__ __forceinline__ PhiloxUni philox_uni_t(uint32_t c0, uint32_t c3, Key2 k) {
+  const uint32_t w1 = 0xD2511F53u * c0;
+  const uint32_t z1 = __umulhi(0xD2511F53u, c0) ^ c3 ^ k.k1;
+  const uint32_t y2 = 0xCD9E8D57u * z1;
+  return PhiloxUni{w1 ^ (k.k1 + 0xBB67AE85u), y2 ^ (k.k0 + 2u * 0x9E3779B9u)};
+}
+
+__device__ __forceinline__ PhiloxPreT philox_pre_t(uint32_t c0, uint32_t c2, uint32_t c3,
+                                                   Key2 k) {
+  const uint32_t z1 = __umulhi(0xD2511F53u, c0) ^ c3 ^ k.k1;
+  const uint32_t y1 = 0xCD9E8D57u * c2;
+  const uint32_t x2 = __umulhi(0xCD9E8D57u, z1) ^ y1 ^ (k.k0 + 0x9E3779B9u);
+  PhiloxPreT pre;
+  pre.h1 = __umulhi(0xCD9E8D57u, c2);
+  mulhilo(0xD2511F53u, x2, pre.lo3, pre.hi3);
+  return pre;
+}
+
+// c1k0 = c1 ^ k0 (per step, uniform)
+__device__ __forceinline__ uint4 philox10_t(const PhiloxPreT &pre, const PhiloxUni &u,
+                                            uint32_t c1k0, Key2 k) {
+  uint32_t lo, hi;
+  // round 1 -> X1; round 2: Z2, W2
+  const uint32_t x1 = pre.h1 ^ c1k0;
+  mulhilo(0xD2511F53u, x1, lo, hi);
+  const uint32_t z2 = hi ^ u.w1k1, w2 = lo;
+  // round 3 (key k + 2C)
+  mulhilo(0xCD9E8D57u, z2, lo, hi);
+  uint4 c = make_uint4(hi ^ u.y2k0, lo, pre.hi3 ^ w2 ^ (k.k1 + 2u * 0xBB67AE85u), pre.lo3);
+  uint32_t k0 = k.k0 + 2u * 0x9E3779B9u, k1 = k.k1 + 2u * 0xBB67AE85u;
+#pragma unroll
+  for (int i = 3; i < 10; ++i) {
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+    uint32_t lo0, hi0, lo1, hi1;
+    mulhilo(0xD2511F53u, c.x, lo0, hi0);
+    mulhilo(0xCD9E8D57u, c.z, lo1, hi1);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+
 __device__ __forceinline__ Key2 load_key(const uint32_t *keys, int64_t f) {
   const uint2 k = __ldg(reinterpret_cast<const uint2 *>(keys) + f);
   return Key2{k.x, k.y};
@@ -93,6 +193,19 @@ __device__ __forceinline__ float2 box_muller_fast_unscaled(uint32_t a, uint32_t 
   const float x = __uint_as_float((b & 0x007fffffu) | 0x40000000u);
   const float ang = fmaf(x, 3.14159265358979f, -9.42477796076938f);
   return make_float2(r * cos_approx(ang), r * sin_approx(ang));
+}
+
+// Box-Muller with the caller's noise scale folded into the radius: returns
+// r' = sqrt(log2(u) * s2) with s2 = -(2 ln 2) s^2 and the trig factors, so
+// that s*z0 = r'*c0 and s*z1 = r'*s1 (one FFMA per increment at the caller).
+__device__ __forceinline__ void box_muller_rad_trig(uint32_t a, uint32_t b, float s2,
+                                                    float &rad, float &c0, float &s1) {
+  const float u = fmaf(static_cast<float>(a), 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+  rad = sqrt_approx(lg2_approx(u) * s2);
+  const float x = __uint_as_float((b & 0x007fffffu) | 0x40000000u);
+  const float ang = fmaf(x, 3.14159265358979f, -9.42477796076938f);
+  c0 = cos_approx(ang);
+  s1 = sin_approx(ang);
 }
 
 // ---- fp64 transforms (53-bit uniforms) ------------------------------------
