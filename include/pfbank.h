@@ -127,7 +127,9 @@ const char *pf_last_error(void);
 int pf_version(void);
 int pf_device_sm_count(int *out);
 
-/* Philox4x32-10 known-answer helper: out[4] for ctr[4], key[2] (device). */
+/* Philox4x32-10 known-answer helper: out[4] for ctr[4], key[2] (device).
+   Also evaluates the kernels' hoisted form (philox10_t) and returns the
+   complemented words if the two ever differ. */
 int pf_philox_kat(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t n, void *stream);
 
 /* ---- L1 operator drop-ins (accel.py) --------------------------------- */

@@ -28,7 +28,17 @@ int check_launch(const char *what) {
 
 __global__ void philox_kat_kernel(const uint4 *ctr, const uint2 *key, uint4 *out, int64_t n) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) out[i] = philox10(ctr[i], Key2{key[i].x, key[i].y});
+  if (i >= n) return;
+  const uint4 c = ctr[i];
+  const Key2 k{key[i].x, key[i].y};
+  uint4 r = philox10(c, k);
+  // the hoisted form used by the lattice/Lorenz kernels must agree bit for
+  // bit; a mismatch poisons the answer (the KAT test then fails)
+  const uint4 h = philox10_t(philox_pre_t(c.x, c.z, c.w, k), philox_uni_t(c.x, c.w, k),
+                             c.y ^ k.k0, k);
+  if (h.x != r.x || h.y != r.y || h.z != r.z || h.w != r.w)
+    r = make_uint4(~r.x, ~r.y, ~r.z, ~r.w);
+  out[i] = r;
 }
 
 template <typename T>

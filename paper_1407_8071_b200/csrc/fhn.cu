@@ -15,6 +15,8 @@
 // store), i.e. 50x less traffic than streaming every Euler step, which
 // turns the kernel from HBM-bound into issue-bound (RNG dominated).
 #include "common.cuh"
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include "philox.cuh"
 
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(256) fhn_interval_kernel(
 //    dependent Philox/MUFU latencies.
 struct FhnFast {
   int rows, cols, n_sub, n_obs, nseg, nodes;
-  float a3, a2, a1, a0;       // cubic
+  float a3, a2, a1, a0;       // u + dt*cubic(u) - 4*dt*coupling*u, folded into one cubic
   float dt, dtc, dtc4;        // dt, dt*coupling, 4*dt*coupling
   float wc, uc, c0;           // w' = wc*w + uc*u + c0  (1+dt*b1, dt*b0, dt*b2)
   float sig_v, sig_w;
@@ -389,10 +391,11 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
                 const float u = v[e][r];
                 const float dn = row0 + r == ROWS - 1 ? u : (r < R - 1 ? v[e][r + 1] : cell[W]);
                 const float nb = ((up + dn) + cell[lo]) + cell[ro];
-                const float p3 = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
-                // u + dt(p3 - w) + dt*coupling*(nb - 4u) + sig_v*zv
-                float un = fmaf(c.dt, p3 - w[e][r], u);
-                un = fmaf(c.dtc, nb, fmaf(-c.dtc4, u, un));
+                // u + dt(p3(u) - w) + dt*coupling*(nb - 4u) + sig_v*zv, with
+                // u + dt p3(u) - 4 dt coupling u one host-folded cubic
+                float un = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
+                un = fmaf(-c.dt, w[e][r], un);
+                un = fmaf(c.dtc, nb, un);
                 un = fmaf(av, tv[h], un);
                 w[e][r] = fmaf(aw, tw[h], fmaf(c.wc, w[e][r], fmaf(c.uc, u, c.c0)));
                 nxt[r * W] = un;
@@ -572,10 +575,10 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   fc.n_obs = c.n_obs;
   fc.nseg = c.nseg;
   fc.nodes = c.nodes;
-  fc.a3 = float(c.a3);
-  fc.a2 = float(c.a2);
-  fc.a1 = float(c.a1);
-  fc.a0 = float(c.a0);
+  fc.a3 = float(c.dt * c.a3);
+  fc.a2 = float(c.dt * c.a2);
+  fc.a1 = float(1.0 + c.dt * c.a1 - 4.0 * c.dt * c.coupling);
+  fc.a0 = float(c.dt * c.a0);
   fc.dt = float(c.dt);
   fc.dtc = float(c.dt * c.coupling);
   fc.dtc4 = float(4.0 * c.dt * c.coupling);
@@ -588,12 +591,15 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   if (tape)
     return launch_fhn_fast_t<30, 50, true, 3, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                  keys, t, tape, status, s);
-  // one particle per CTA, 3 CTAs/SM: measured 46.1 ms vs 46.5 ms for two
-  // particles per CTA and 46.9-48.4 ms for 4-5 CTAs/SM (cfg4)
+  // one particle per CTA, 2 CTAs/SM (102 registers: the Philox key schedule
+  // and the hoisted rounds stay in registers): cfg4 41.8 ms/interval vs 43.1
+  // at 3 CTAs/SM (78 registers, round keys rematerialised every step), 42.2
+  // at 4 CTAs/SM and 42.8 for two particles per CTA at 2 CTAs/SM.  The
+  // noise-free lookahead variant has no draws and keeps 3 CTAs/SM.
   if (c.sig_v == 0.0 && c.sig_w == 0.0)  // the auxiliary filter's point prediction
     return launch_fhn_fast_t<30, 50, false, 3, 1, true>(fc, x_in, anc, x_out, y, obs_idx, logw,
                                                         MN, N, keys, t, tape, status, s);
-  return launch_fhn_fast_t<30, 50, false, 3, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+  return launch_fhn_fast_t<30, 50, false, 2, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                 keys, t, tape, status, s);
 }
 

@@ -160,10 +160,8 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
 // noise scale is folded into each pair's radius (cz*z = r'*cos with
 // r' = sqrt(-log2(u) * 2 ln2 * cz^2)), so an increment costs one FFMA.
 // UKEY: every block lies inside one filter (N % 256 == 0), so the filter id,
-// its Philox key and the key schedule are block-uniform and live in uniform
-// registers; the first two Philox rounds then depend only on uniform or
-// loop-invariant words and leave the per-substep path (same draws, same
-// arithmetic as UKEY=false).
+// its Philox key and the key schedule are block-uniform (uniform registers);
+// same draws and arithmetic as UKEY=false.
 template <bool UKEY>
 __global__ void __launch_bounds__(256) lorenz_fast_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
@@ -176,7 +174,10 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
   const int64_t f = UKEY ? (static_cast<int64_t>(blockIdx.x) * 256) / N : p / N;
   const uint32_t j = static_cast<uint32_t>(p - f * N);
   const Key2 key = load_key(keys, f);
-  const PhiloxPre pre = philox_pre(j, kPurposeLorenz, key);
+  // counter (t, draw index, particle, purpose): only the uniform draw index
+  // changes inside the loop, rounds 1-3 are mostly hoisted (philox10_t)
+  const PhiloxPreT pre = philox_pre_t(t, j, kPurposeLorenz, key);
+  const PhiloxUni uni = philox_uni_t(t, kPurposeLorenz, key);
   const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
   float x1 = xin[src], x2 = xin[MN + src], x3 = xin[2 * MN + src];
   const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb, s2 = c.f_s2;
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
     float rad[6], tr[12];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const uint4 rr = philox10_split(pre, t, static_cast<uint32_t>(k4 * 3 + q), key);
+      const uint4 rr = philox10_t(pre, uni, static_cast<uint32_t>(k4 * 3 + q) ^ key.k0, key);
       box_muller_rad_trig(rr.x, rr.y, s2, rad[2 * q], tr[4 * q], tr[4 * q + 1]);
       box_muller_rad_trig(rr.z, rr.w, s2, rad[2 * q + 1], tr[4 * q + 2], tr[4 * q + 3]);
     }

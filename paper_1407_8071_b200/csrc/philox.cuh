@@ -30,11 +30,6 @@ __device__ __forceinline__ uint4 philox10(uint4 c, Key2 k) {
   return c;
 }
 
-// Philox4x32-10 split for a counter (c0, c1, c2, c3) whose words c0 and c3
-// are fixed for a thread (particle index, purpose tag) while c2 varies (draw
-// index) and c1 is block-uniform (observation time): the parts of rounds 1-2
-// that depend only on (c0, c3, key) are computed once per thread
-// (philox_pre), the rest (philox10_split) is bit-identical to philox10.
 // 32x32 -> 64 product as one IMAD.WIDE.U32 (ptxas otherwise may split the
 // lo/hi halves into IMAD + IMAD.HI, two issue slots).
 __device__ __forceinline__ void mulhilo(uint32_t m, uint32_t a, uint32_t &lo, uint32_t &hi) {
@@ -43,39 +38,10 @@ __device__ __forceinline__ void mulhilo(uint32_t m, uint32_t a, uint32_t &lo, ui
   asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
 }
 
-struct PhiloxPre {
-  uint32_t w1, y2, h2;  // round-1 W; round-2 lo/hi of M1 * Z1
-};
-
-__device__ __forceinline__ PhiloxPre philox_pre(uint32_t c0, uint32_t c3, Key2 k) {
-  const uint32_t z1 = __umulhi(0xD2511F53u, c0) ^ c3 ^ k.k1;
-  return PhiloxPre{0xD2511F53u * c0, 0xCD9E8D57u * z1, __umulhi(0xCD9E8D57u, z1)};
-}
-
-__device__ __forceinline__ uint4 philox10_split(const PhiloxPre &pre, uint32_t c1, uint32_t c2,
-                                                Key2 k) {
-  // round 1 (key k): X1 = hi(M1 c2) ^ c1 ^ k0, Y1 = lo(M1 c2), Z1/W1 in pre
-  const uint32_t x1 = __umulhi(0xCD9E8D57u, c2) ^ c1 ^ k.k0;
-  const uint32_t y1 = 0xCD9E8D57u * c2;
-  // round 2 (key k + C)
-  uint32_t k0 = k.k0 + 0x9E3779B9u, k1 = k.k1 + 0xBB67AE85u;
-  uint4 c = make_uint4(pre.h2 ^ y1 ^ k0, pre.y2, __umulhi(0xD2511F53u, x1) ^ pre.w1 ^ k1,
-                       0xD2511F53u * x1);
-#pragma unroll
-  for (int i = 2; i < 10; ++i) {
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-    uint32_t lo0, hi0, lo1, hi1;
-    mulhilo(0xD2511F53u, c.x, lo0, hi0);
-    mulhilo(0xCD9E8D57u, c.z, lo1, hi1);
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-  }
-  return c;
-}
-
-// Philox4x32-10 for a counter (c0, c1, c2, c3) = (block-uniform particle
-// index, per-step uniform time word, thread-fixed draw index, purpose): the
-// FH-N lattice layout, where only c1 changes from one Euler step to the next.
+// Philox4x32-10 for a counter (c0, c1, c2, c3) with c0 block-uniform and
+// fixed (FH-N: particle index; Lorenz: observation time), c1 the uniform word
+// that changes inside the loop (FH-N: Euler step; Lorenz: draw index), c2
+// fixed per thread (FH-N: node pair; Lorenz: particle) and c3 the purpose.
 // philox_pre_t hoists everything of rounds 1-3 that does not depend on c1
 // (3 words per thread and draw index); philox10_t is bit-identical to
 // philox10(make_uint4(c0, c1, c2, c3), k).
