@@ -527,14 +527,14 @@ def run_ours(args, cfg):
         achieved = ps_per_launch * per_ps / (kern_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
-                "kernel": "fhnnet_step_kernel<float,0,4>",
+                "kernel": "fhnnet_fast_kernel (fp32, Philox)",
                 "algorithmic": f"{per_ps:.0f} B/particle-step (24 B/node: U,V fp32 + history "
                                f"bits, read + write) x {ps_per_launch} particle-steps per launch"}
     elif cfg["kind"] == "fhn":
         achieved = ps_per_launch * FHN_BYTES_PER_PS / (kern_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
-                "kernel": "fhn_interval_kernel<float,0>",
+                "kernel": "fhn_fast_kernel<30,50,6> (fp32, Philox)",
                 "algorithmic": f"{FHN_BYTES_PER_PS:.0f} B/particle-step x {ps_per_launch} "
                                f"particle-steps per launch"}
         phys = ps_per_launch / n_sub * (2 * 2 * model.nodes * 4 + 4 + 4)
@@ -545,7 +545,7 @@ def run_ours(args, cfg):
         roof = {"bound": "fp32", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
                 "peak_source": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (SURVEY §8d)",
-                "kernel": "lorenz_pw_kernel<float,0>",
+                "kernel": "lorenz_fast_kernel (fp32, Philox)",
                 "algorithmic": f"{LORENZ_FLOP_PER_PS:.0f} flop/particle-step x {ps_per_launch}"}
     roof["kernel_ms"] = kern_ms
     roof["kernel_share_of_step"] = kern_share

@@ -422,7 +422,7 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
     if (z_tape)
       lorenz_pw_kernel<float, 1><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
                                                       c, keys, t, z_tape, status);
-    else if (N % 256 == 0)
+    else if (N % 256 == 0)  // occupancy 4-8 blocks/SM measured equal (issue-bound)
       lorenz_fast_kernel<true><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim, c,
                                                     keys, t, status);
     else
