@@ -163,7 +163,7 @@ __device__ __forceinline__ void est_block_write(double (&acc)[kEstMaxDim], int d
 }
 
 template <typename TW, int MODE, int THREADS, int IPT, bool GATHER>
-__global__ void __launch_bounds__(THREADS) resample_bank_kernel(
+__global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank_kernel(
     const TW *__restrict__ logw, int32_t N, const double *__restrict__ u_tape,
     const uint32_t *__restrict__ keys, uint32_t t, int32_t *__restrict__ anc,
     double *__restrict__ lnc, uint8_t *__restrict__ collapsed, uint32_t *__restrict__ status,
@@ -356,14 +356,21 @@ __global__ void __launch_bounds__(THREADS) resample_bank_kernel(
     int a = lo, b = d0 - lo;
     double ca = a < N ? s_cum[slot(a)] : INFINITY;
     double ub = b < N ? s_u[slot(b)] : INFINITY;
-    for (int d = d0; d < d1; ++d) {
-      if (b >= N || ca < ub) {
-        ++a;
-        ca = a < N ? s_cum[slot(a)] : INFINITY;
-      } else {
-        s_anc[slot(b)] = static_cast<int32_t>(base + (a < N - 1 ? a : N - 1));
-        ++b;
-        ub = b < N ? s_u[slot(b)] : INFINITY;
+    // branch-free steps (no warp divergence): one predicated store and one
+    // shared load of the next element of whichever sequence advanced
+    const int nsteps = d1 - d0;
+#pragma unroll
+    for (int st = 0; st < 2 * IPT; ++st) {
+      if (st < nsteps) {
+        const bool ta = b >= N || ca < ub;
+        if (!ta) s_anc[slot(b)] = static_cast<int32_t>(base + (a < N - 1 ? a : N - 1));
+        a += ta;
+        b += !ta;
+        const int i = ta ? a : b;
+        const double *src = (ta ? s_cum : s_u) + slot(i);
+        const double nv = i < N ? *src : INFINITY;
+        ca = ta ? nv : ca;
+        ub = ta ? ub : nv;
       }
     }
   }
