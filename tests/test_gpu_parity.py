@@ -639,3 +639,36 @@ def test_lorenz_helpers_match_reference(golden):
     tr = pf.lorenz_transition(np.array([1.0, 2.0, 3.0]), np.random.default_rng(3))
     assert np.array_equal(tr, g["lz_tr"])
     assert pf.lorenz_log_likelihood(0.7, np.array([1.0, 2.0, 3.0])) == float(g["lz_ll"])
+
+
+@pytest.mark.gpu
+def test_lorenz_uniform_key_kernel_matches_generic():
+    """lorenz_fast_kernel<UKEY=true> (N % 256 == 0: block-uniform key and
+    filter id) draws and computes exactly like the generic variant: particle j
+    of filter f has the same Philox counter and key in a bank of N=256 (uniform
+    path) and N=257 (generic path), so the propagated states must agree bit
+    for bit."""
+    import paper_1407_8071_b200 as pf
+
+    model = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3")
+    params = model.params()
+    M = 3
+    keys = torch.from_numpy(np.array([[11, 22], [33, 44], [55, 66]], np.uint32).view(np.int32)).cuda()
+    y = torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda")
+    rng = np.random.default_rng(5)
+    base = rng.standard_normal((3, M, 257)).astype(np.float32) * 5.0
+    outs = {}
+    for N in (256, 257):
+        xin = torch.from_numpy(np.ascontiguousarray(base[:, :, :N].reshape(3, M * N))).cuda()
+        xout = torch.empty_like(xin)
+        logw = torch.empty(M * N, dtype=torch.float32, device="cuda")
+        status = torch.zeros(M, dtype=torch.int32, device="cuda")
+        _lib.call("pf_lorenz_propagate_weight", params, _lib.PF_F32, _lib.ptr(xin), None,
+                  _lib.ptr(xout), _lib.ptr(y), _lib.ptr(logw), M, N, _lib.ptr(keys), 3, None,
+                  _lib.ptr(status), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        outs[N] = (xout.cpu().numpy().reshape(3, M, N)[:, :, :256],
+                   logw.cpu().numpy().reshape(M, N)[:, :256])
+    assert np.all(np.isfinite(outs[256][0]))
+    assert np.array_equal(outs[256][0], outs[257][0])
+    assert np.array_equal(outs[256][1], outs[257][1])
