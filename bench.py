@@ -495,18 +495,19 @@ def run_ours(args, cfg):
         exch.finish()
     else:
         bank.run_native(0, args.warmup)
-    bank.prepare_timing(args.steps if world == 1 else 1)  # timing events outside the region
+    bank.prepare_timing(args.steps)  # timing events outside the region
     _barrier(world)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kern_list = []
     with ClockSampler(local) as clocks:
         start.record()
-        if exch:
+        if exch:  # one interval per call (its estimate all-reduce follows), no host waits
             for i in range(args.steps):
                 k = args.warmup + i
-                kern_list += bank.run_native(k, 1, time_propagate=True)
+                bank.run_native(k, 1, time_propagate=True, slot=i)
                 exch.step_done(k)
             exch.finish()
+            kern_list = bank.pool_propagate_ms(args.steps)
         else:
             kern_list = bank.run_native(args.warmup, args.steps, time_propagate=True)
         end.record()

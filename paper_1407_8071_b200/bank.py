@@ -304,12 +304,15 @@ class FilterBank:
         return d
 
     def run_native(self, k0: int, n_steps: int, time_propagate: bool = False,
-                   time_steps: bool = False):
+                   time_steps: bool = False, slot: int | None = None):
         """Observations k0..k0+n_steps-1 in one native call (pf_bank_run).
 
         time_propagate=True returns the per-interval durations (ms) of the
         propagate kernel, measured with CUDA events on the launch stream;
-        time_steps=True stores whole-interval durations in self.last_step_ms."""
+        time_steps=True stores whole-interval durations in self.last_step_ms.
+        slot=i (after prepare_timing(n)): record into intervals i.. of the
+        prepared pool of n intervals without any host wait; read them later
+        with pool_propagate_ms(n)."""
         import ctypes
 
         if self.obs is None:
@@ -319,9 +322,17 @@ class FilterBank:
         if self._desc is None:
             self._desc = self._bank_desc()
         timed = (time_propagate or time_steps) and n_steps > 0
+        if slot is not None:  # slice of a larger prepared pool, nothing to wait for
+            evs, handles = self._slot_pool
+            if 4 * (slot + n_steps) > len(evs):
+                raise ValueError("run_native: slot beyond the prepared timing pool")
+            timed = False
         pool = self.__dict__.get("_event_pools", {}).get(4 * n_steps) if timed else None
         ms = sm = None
-        if pool is not None:  # prepared events: recorded by the driver, no host wait
+        if slot is not None:
+            self._desc.events = ctypes.c_void_p(ctypes.addressof(handles) +
+                                                4 * slot * ctypes.sizeof(ctypes.c_void_p))
+        elif pool is not None:  # prepared events: recorded by the driver, no host wait
             evs, handles = pool
             self._desc.events = ctypes.cast(handles, ctypes.c_void_p)
         elif timed:  # the driver creates the events and waits for the last one
@@ -356,8 +367,16 @@ class FilterBank:
 
     def prepare_timing(self, n_steps: int):
         """Create the timing events of an n_steps run_native call ahead of time
-        (keeps their creation out of a timed region)."""
-        self._event_pool(4 * n_steps)
+        (keeps their creation out of a timed region); they also serve
+        run_native(..., slot=i) calls of one interval each."""
+        self._slot_pool = self._event_pool(4 * n_steps)
+
+    def pool_propagate_ms(self, n_steps: int):
+        """Propagate durations (ms) of intervals 0..n_steps-1 recorded through
+        run_native(..., slot=i); waits for the last one."""
+        evs, _ = self._slot_pool
+        evs[4 * n_steps - 1].synchronize()
+        return [evs[4 * i + 1].elapsed_time(evs[4 * i + 2]) for i in range(n_steps)]
 
     def _event_pool(self, n):
         """n timing events and their raw handles (ctypes array), created once

@@ -672,3 +672,33 @@ def test_lorenz_uniform_key_kernel_matches_generic():
     assert np.all(np.isfinite(outs[256][0]))
     assert np.array_equal(outs[256][0], outs[257][0])
     assert np.array_equal(outs[256][1], outs[257][1])
+
+
+def test_native_slot_timing_matches_one_call():
+    """run_native one interval at a time into slots of a prepared event pool
+    (the multi-GPU bench path: no host wait per interval) gives the same
+    filter results as one multi-interval call, and a positive propagate
+    duration per interval."""
+    truth0, _, obs = orc.lorenz_truth(seed=4, n_obs=5)
+    gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(truth0), prior_var=1.0)
+    keys = pf.philox.filter_keys(9, 4)
+    res = []
+    for sliced in (False, True):
+        bank = pf.FilterBank(gm, 4, 512, keys, len(obs), dtype="float32")
+        bank.load_observations(obs)
+        bank.init()
+        if sliced:
+            bank.prepare_timing(len(obs))
+            for k in range(len(obs)):
+                assert bank.run_native(k, 1, time_propagate=True, slot=k) is None
+            ms = bank.pool_propagate_ms(len(obs))
+            assert len(ms) == len(obs) and all(m > 0 for m in ms)
+            with pytest.raises(ValueError):
+                bank.run_native(0, 1, time_propagate=True, slot=len(obs))
+        else:
+            bank.run_native(0, len(obs))
+        torch.cuda.synchronize()
+        res.append((bank.est.cpu().numpy(), bank.lnc_tr.cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
