@@ -398,6 +398,8 @@ def run_resample(args, cfg):
                        "tile CDF, partition, merge, fused gather)"),
             "algorithmic": f"{RESAMPLE_BYTES_PER_PARTICLE:.0f} B/particle x {MN} particles",
             "traffic": _ncu_traffic(args.config), "ncu_pipes": _ncu_pipes(args.config)}
+    if N <= 8192:  # one resample launch per step: the step time is the kernel time
+        roof["issue"] = _issue_roofline(roof["ncu_pipes"], per * 1e3)
     # e2e: host logw in (pinned), host ancestors out, through the C ABI.  A bank
     # of many filters is streamed in filter chunks on three streams (H2D of
     # chunk c+1 and D2H of chunk c-1 overlap the resample of chunk c; PCIe is
@@ -552,6 +554,7 @@ def run_ours(args, cfg):
     roof["kernel_share_of_step"] = kern_share
     roof["traffic"] = _ncu_traffic(args.config)
     roof["ncu_pipes"] = _ncu_pipes(args.config)
+    roof["issue"] = _issue_roofline(roof["ncu_pipes"], kern_ms)
 
     # e2e through the public API (host observations in, host results out)
     if args.profile:
@@ -751,6 +754,19 @@ def _ncu_traffic(config):
             return json.load(fh).get(config)
     except OSError:
         return None
+
+
+def _issue_roofline(pipes, kern_ms, sm_mhz=1965.0):
+    """Second roofline for the issue-bound kernels: warp instructions per launch
+    (committed ncu count of the same launch) / the live kernel time, against
+    148 SMs x 4 schedulers x 1 instruction/clock at the max SM clock."""
+    if not pipes or "warp_inst_per_launch" not in pipes or not kern_ms:
+        return None
+    achieved = pipes["warp_inst_per_launch"] / (kern_ms / 1e3)
+    peak = 148 * 4 * sm_mhz * 1e6
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
+            "frac": achieved / peak,
+            "source": "smsp__inst_executed.sum (profiles/pipes.json) / live kernel time"}
 
 
 def _ncu_pipes(config):
