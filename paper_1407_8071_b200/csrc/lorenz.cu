@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
   // changes inside the loop, rounds 1-3 are mostly hoisted (philox10_t)
   const PhiloxPreT pre = philox_pre_t(t, j, kPurposeLorenz, key);
   const PhiloxUni uni = philox_uni_t(t, kPurposeLorenz, key);
+  const PhiloxKeys rk = philox_round_keys(key);
   const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
   float x1 = xin[src], x2 = xin[MN + src], x3 = xin[2 * MN + src];
   const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb, s2 = c.f_s2;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
     float rad[6], tr[12];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const uint4 rr = philox10_t(pre, uni, static_cast<uint32_t>(k4 * 3 + q) ^ key.k0, key);
+      const uint4 rr = philox10_t(pre, uni, static_cast<uint32_t>(k4 * 3 + q) ^ key.k0, rk);
       box_muller_rad_trig(rr.x, rr.y, s2, rad[2 * q], tr[4 * q], tr[4 * q + 1]);
       box_muller_rad_trig(rr.z, rr.w, s2, rad[2 * q + 1], tr[4 * q + 2], tr[4 * q + 3]);
     }

@@ -96,6 +96,40 @@ __device__ __forceinline__ uint4 philox10_t(const PhiloxPreT &pre, const PhiloxU
   return c;
 }
 
+// The Philox key schedule k + i*C (i = 0..9) computed once per thread (for a
+// block-uniform key the compiler can keep it in uniform registers).
+struct PhiloxKeys {
+  uint32_t k0[10], k1[10];
+};
+__device__ __forceinline__ PhiloxKeys philox_round_keys(Key2 k) {
+  PhiloxKeys r;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    r.k0[i] = k.k0 + static_cast<uint32_t>(i) * 0x9E3779B9u;
+    r.k1[i] = k.k1 + static_cast<uint32_t>(i) * 0xBB67AE85u;
+  }
+  return r;
+}
+
+// philox10_t with a precomputed key schedule (bit-identical)
+__device__ __forceinline__ uint4 philox10_t(const PhiloxPreT &pre, const PhiloxUni &u,
+                                            uint32_t c1k0, const PhiloxKeys &rk) {
+  uint32_t lo, hi;
+  const uint32_t x1 = pre.h1 ^ c1k0;
+  mulhilo(0xD2511F53u, x1, lo, hi);
+  const uint32_t z2 = hi ^ u.w1k1, w2 = lo;
+  mulhilo(0xCD9E8D57u, z2, lo, hi);
+  uint4 c = make_uint4(hi ^ u.y2k0, lo, pre.hi3 ^ w2 ^ rk.k1[2], pre.lo3);
+#pragma unroll
+  for (int i = 3; i < 10; ++i) {
+    uint32_t lo0, hi0, lo1, hi1;
+    mulhilo(0xD2511F53u, c.x, lo0, hi0);
+    mulhilo(0xCD9E8D57u, c.z, lo1, hi1);
+    c = make_uint4(hi1 ^ c.y ^ rk.k0[i], lo1, hi0 ^ c.w ^ rk.k1[i], lo0);
+  }
+  return c;
+}
+
 __device__ __forceinline__ Key2 load_key(const uint32_t *keys, int64_t f) {
   const uint2 k = __ldg(reinterpret_cast<const uint2 *>(keys) + f);
   return Key2{k.x, k.y};
