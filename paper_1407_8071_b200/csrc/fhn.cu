@@ -15,8 +15,6 @@
 // store), i.e. 50x less traffic than streaming every Euler step, which
 // turns the kernel from HBM-bound into issue-bound (RNG dominated).
 #include "common.cuh"
-#include <cstdlib>
-#include <cstring>
 #include <type_traits>
 #include "philox.cuh"
 
@@ -337,10 +335,12 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
     const float s2w = -1.3862943611198906f * c.sig_w * c.sig_w;
     PhiloxPreT pre[PP][R / 2];
     PhiloxUni uni[PP];
+    PhiloxKeys rk[PP];
     if (!TAPE && !NF) {
 #pragma unroll
       for (int e = 0; e < PP; ++e) {
         uni[e] = philox_uni_t(je[e], kPurposeFhn, key[e]);
+        rk[e] = philox_round_keys(key[e]);
 #pragma unroll
         for (int q = 0; q < R / 2; ++q)
           pre[e][q] = philox_pre_t(je[e], static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col),
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
             } else if (NF) {  // noise-free lookahead: no draws (0 * 0 adds an exact 0)
               av = aw = tv[0] = tv[1] = tw[0] = tw[1] = 0.f;
             } else {
-              const uint4 rr = philox10_t(pre[e][q], uni[e], c1k0, key[e]);
+              const uint4 rr = philox10_t(pre[e][q], uni[e], c1k0, rk[e]);
               box_muller_rad_trig(rr.x, rr.y, s2v, av, tv[0], tv[1]);
               box_muller_rad_trig(rr.z, rr.w, s2w, aw, tw[0], tw[1]);
             }
