@@ -127,6 +127,11 @@ const char *pf_last_error(void);
 int pf_version(void);
 int pf_device_sm_count(int *out);
 
+/* FP32 peak probe (measurement helper for bench.py's Lorenz roofline): one
+   launch of SMs x 8 blocks x 256 threads, each running 8 independent FFMA chains
+   for iters x 16 steps = 256 * iters flop per thread.  Time it with events. */
+int pf_probe_fp32_fma(float *sink, int64_t iters, void *stream);
+
 /* Philox4x32-10 known-answer helper: out[4] for ctr[4], key[2] (device).
    Also evaluates the kernels' hoisted form (philox10_t) and returns the
    complemented words if the two ever differ. */

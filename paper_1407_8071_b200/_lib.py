@@ -94,6 +94,7 @@ SIGNATURES = {
     "pf_version": (ctypes.c_int, []),
     "pf_device_sm_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     "pf_philox_kat": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp]),
+    "pf_probe_fp32_fma": (ctypes.c_int, [c_vp, c_i64, c_vp]),
     "pf_op_lorenz_euler_block": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i64, c_f64, c_f64, c_f64,
                                                 c_f64, c_vp, c_vp]),
     "pf_op_fhn_euler_block": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_f64,

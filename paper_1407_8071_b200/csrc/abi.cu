@@ -41,6 +41,26 @@ __global__ void philox_kat_kernel(const uint4 *ctr, const uint2 *key, uint4 *out
   out[i] = r;
 }
 
+// FP32 peak probe: 8 independent FFMA chains per thread, 8 x 256-thread
+// blocks per SM (64 warps), iters x 8 x 2 flop per thread; the result is
+// stored only if impossible so the chains stay live.
+__global__ void __launch_bounds__(256) fma_chain_kernel(float *sink, int64_t iters) {
+  float a[8];
+  const float m = 1.0000001f, c = 1e-7f * static_cast<float>(threadIdx.x & 7);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = static_cast<float>(threadIdx.x + i);
+  for (int64_t k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fmaf(a[i], m, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == -1.0f) sink[threadIdx.x] = s;
+}
+
 template <typename T>
 __global__ void fill_rows_kernel(T *x, int64_t total, int64_t row_len, const double *row) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -85,6 +105,14 @@ int pf_device_sm_count(int *out) {
   if (cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return PF_ECUDA;
   return PF_OK;
+}
+
+int pf_probe_fp32_fma(float *sink, int64_t iters, void *stream) {
+  PF_REQUIRE(sink && iters >= 1, "pf_probe_fp32_fma: bad arguments");
+  int sms = kSmCount;
+  pf_device_sm_count(&sms);
+  fma_chain_kernel<<<sms * 8, 256, 0, as_stream(stream)>>>(sink, iters);
+  return check_launch("pf_probe_fp32_fma");
 }
 
 int pf_philox_kat(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t n,
