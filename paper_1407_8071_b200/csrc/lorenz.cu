@@ -182,16 +182,22 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
   const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
   float x1 = xin[src], x2 = xin[MN + src], x3 = xin[2 * MN + src];
   const float dt = c.f_dt, ndts = c.f_ndts, r = c.f_r, nb = c.f_nb, s2 = c.f_s2;
-  const int nfull = c.n_sub >> 2;
-  for (int k4 = 0; k4 <= nfull; ++k4) {
-    const int left = c.n_sub - 4 * k4;
-    if (left <= 0) break;
+  // Software-pipelined chunks of 4 substeps: the Philox blocks of chunk k+1
+  // are generated in the same basic block as chunk k's Box-Muller transforms
+  // (MUFU-heavy) and Euler steps (FFMA), so the integer, XU and FMA work
+  // interleave instead of arriving in bursts.
+  const int nch = (c.n_sub + 3) >> 2;
+  auto draws = [&](int k4, uint4 *rr) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      rr[q] = philox10_t(pre, uni, static_cast<uint32_t>(k4 * 3 + q) ^ key.k0, rk);
+  };
+  auto chunk = [&](const uint4 *rr, int left) {
     float rad[6], tr[12];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const uint4 rr = philox10_t(pre, uni, static_cast<uint32_t>(k4 * 3 + q) ^ key.k0, rk);
-      box_muller_rad_trig(rr.x, rr.y, s2, rad[2 * q], tr[4 * q], tr[4 * q + 1]);
-      box_muller_rad_trig(rr.z, rr.w, s2, rad[2 * q + 1], tr[4 * q + 2], tr[4 * q + 3]);
+      box_muller_rad_trig(rr[q].x, rr[q].y, s2, rad[2 * q], tr[4 * q], tr[4 * q + 1]);
+      box_muller_rad_trig(rr[q].z, rr[q].w, s2, rad[2 * q + 1], tr[4 * q + 2], tr[4 * q + 3]);
     }
     auto sub = [&](int n0) {  // normals n0..n0+2: pair n/2, trig factor n
       const float n1 = fmaf(rad[n0 >> 1], tr[n0], fmaf(ndts, x1 - x2, x1));
@@ -211,6 +217,17 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
       for (int q = 0; q < 3; ++q)
         if (q < left) sub(3 * q);
     }
+  };
+  if (nch > 0) {
+    uint4 cur[3], nxt[3];
+    draws(0, cur);
+    for (int k4 = 0; k4 + 1 < nch; ++k4) {  // full chunks: only the last can be partial
+      draws(k4 + 1, nxt);
+      chunk(cur, 4);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) cur[q] = nxt[q];
+    }
+    chunk(cur, c.n_sub - 4 * (nch - 1));
   }
   if (!live) return;
   if (!(isfinite(x1) && isfinite(x2) && isfinite(x3))) atomicOr(status + f, PF_ST_DIVERGED);
