@@ -91,6 +91,46 @@ __device__ __forceinline__ double block_exclusive_scan(double v, double *scratch
   return warp > 0 ? __dadd_rn(woff, excl) : excl;
 }
 
+// Exclusive block scan of a pair of fp64 values per thread (two independent
+// scans in one pass: one barrier pair instead of two).  scratch >= 33.
+__device__ __forceinline__ double2 block_exclusive_scan2(double2 v, double2 *scratch,
+                                                         double2 *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  double x = v.x, y = v.y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double a = __shfl_up_sync(0xffffffffu, x, o);
+    const double b = __shfl_up_sync(0xffffffffu, y, o);
+    if (lane >= o) {
+      x = __dadd_rn(x, a);
+      y = __dadd_rn(y, b);
+    }
+  }
+  if (lane == 31) scratch[warp] = make_double2(x, y);
+  __syncthreads();
+  double2 wv = lane < nw ? scratch[lane] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double a = __shfl_up_sync(0xffffffffu, wv.x, o);
+    const double b = __shfl_up_sync(0xffffffffu, wv.y, o);
+    if (lane >= o) {
+      wv.x = __dadd_rn(wv.x, a);
+      wv.y = __dadd_rn(wv.y, b);
+    }
+  }
+  const int src = warp > 0 ? warp - 1 : 0;
+  const double wox = __shfl_sync(0xffffffffu, wv.x, src);
+  const double woy = __shfl_sync(0xffffffffu, wv.y, src);
+  total->x = __shfl_sync(0xffffffffu, wv.x, nw - 1);
+  total->y = __shfl_sync(0xffffffffu, wv.y, nw - 1);
+  const double px = __shfl_up_sync(0xffffffffu, x, 1);
+  const double py = __shfl_up_sync(0xffffffffu, y, 1);
+  const double ex = lane > 0 ? px : 0.0, ey = lane > 0 ? py : 0.0;
+  __syncthreads();
+  return warp > 0 ? make_double2(__dadd_rn(wox, ex), __dadd_rn(woy, ey)) : make_double2(ex, ey);
+}
+
 // ---- bank path: one CTA per filter --------------------------------------
 // Thread t owns the IPT consecutive particles [t*IPT, t*IPT+IPT): weights,
 // CDF and sorted uniforms live in registers, per-thread sums are combined
@@ -171,6 +211,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
     EstFuse ef) {
   extern __shared__ double s_cum[];  // THREADS * IPT slots, thread-major
   __shared__ double scratch[33];
+  __shared__ double2 scratch2[33];
   __shared__ double s_red[(THREADS / 32) * kEstMaxDim];
   const TW *ex = static_cast<const TW *>(ef.x);
   const double invN = 1.0 / static_cast<double>(N);
@@ -267,7 +308,12 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
   // 3. w = e / total (IEEE division, core.py:136; production fp32 inputs:
   // reciprocal multiply), CDF = offset + local run
   double total, run = 0.0;
+  double u[IPT];
   if constexpr (kFastExp) {
+    // production fp32: the thread's unnormalised weight runs and its
+    // unnormalised exponential spacings (resampling.py:21-26) are scanned
+    // together (one block scan of pairs); CDF = (offset + run) / total,
+    // uniforms = (offset + run) / c[N]
     const float mf = static_cast<float>(m);
     float pf = 0.f;  // running sum of the thread's exp(lw - m)
 #pragma unroll
@@ -275,37 +321,6 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
       pf += exp_fast(lf[q] - mf);  // padding: exp(-inf) = 0
       lw[q] = static_cast<double>(pf);
     }
-    total = block_sum(static_cast<double>(pf), scratch);
-    const double inv_total = 1.0 / total;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) lw[q] *= inv_total;  // local inclusive prefix
-    run = lw[IPT - 1];
-  } else {
-    double part = 0.0;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-      lw[q] = i0 + q < N ? exp(__dsub_rn(lw[q], m)) : 0.0;
-      part = __dadd_rn(part, lw[q]);
-    }
-    total = block_sum(part, scratch);
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-      run = __dadd_rn(run, __ddiv_rn(lw[q], total));
-      lw[q] = run;  // local inclusive prefix
-    }
-  }
-  double wtot;
-  const double off = block_exclusive_scan(run, scratch, &wtot);
-#pragma unroll
-  for (int q = 0; q < IPT; ++q)
-    if (i0 + q < N) s_cum[q * THREADS + tid] = __dadd_rn(off, lw[q]);
-
-  // 4. this thread's sorted uniforms (resampling.py:21-26)
-  double u[IPT];
-  if (MODE == 1) {
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __ldg(u_tape + base + i0 + q) : 2.0;
-  } else {
     const Key2 key = load_key(keys, f);
     double erun = 0.0;
 #pragma unroll
@@ -321,12 +336,64 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
         u[q + h] = erun;
       }
     }
-    double etot;
-    const double eoff = block_exclusive_scan(erun, scratch, &etot);
-    const double cN = __dadd_rn(etot, spacing_exp_fast(key, t, N));  // c[N]
+    double2 tot2;
+    const double2 off2 =
+        block_exclusive_scan2(make_double2(static_cast<double>(pf), erun), scratch2, &tot2);
+    total = tot2.x;
+    const double inv_total = 1.0 / total;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+      if (i0 + q < N) s_cum[q * THREADS + tid] = __dadd_rn(off2.x, lw[q]) * inv_total;
+    const double cN = __dadd_rn(tot2.y, spacing_exp_fast(key, t, N));  // c[N]
     const double inv = 1.0 / cN;  // production draws: reciprocal multiply
 #pragma unroll
-    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __dadd_rn(eoff, u[q]) * inv : 2.0;
+    for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __dadd_rn(off2.y, u[q]) * inv : 2.0;
+  } else {
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      lw[q] = i0 + q < N ? exp(__dsub_rn(lw[q], m)) : 0.0;
+      part = __dadd_rn(part, lw[q]);
+    }
+    total = block_sum(part, scratch);
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      run = __dadd_rn(run, __ddiv_rn(lw[q], total));
+      lw[q] = run;  // local inclusive prefix
+    }
+    double wtot;
+    const double off = block_exclusive_scan(run, scratch, &wtot);
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+      if (i0 + q < N) s_cum[q * THREADS + tid] = __dadd_rn(off, lw[q]);
+
+    // 4. this thread's sorted uniforms (resampling.py:21-26)
+    if (MODE == 1) {
+#pragma unroll
+      for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __ldg(u_tape + base + i0 + q) : 2.0;
+    } else {
+      const Key2 key = load_key(keys, f);
+      double erun = 0.0;
+#pragma unroll
+      for (int q = 0; q < IPT; q += 4) {
+        const uint4 r = philox10(make_uint4(static_cast<uint32_t>((i0 + q) >> 2), t, 0u,
+                                            kPurposeResample),
+                                 key);
+        const uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int h = 0; h < 4 && q + h < IPT; ++h) {
+          const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
+          erun = __dadd_rn(erun, e);
+          u[q + h] = erun;
+        }
+      }
+      double etot;
+      const double eoff = block_exclusive_scan(erun, scratch, &etot);
+      const double cN = __dadd_rn(etot, spacing_exp_fast(key, t, N));  // c[N]
+      const double inv = 1.0 / cN;  // production draws: reciprocal multiply
+#pragma unroll
+      for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __dadd_rn(eoff, u[q]) * inv : 2.0;
+    }
   }
   __syncthreads();  // s_cum complete
 
