@@ -424,21 +424,35 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
     double ca = a < N ? s_cum[slot(a)] : INFINITY;
     double ub = b < N ? s_u[slot(b)] : INFINITY;
     // branch-free steps (no warp divergence): one predicated store and one
-    // shared load of the next element of whichever sequence advanced
-    const int nsteps = d1 - d0;
+    // shared load of the next element of whichever sequence advanced, both
+    // sequences addressed from one 32-bit shared base (s_u = s_cum +
+    // THREADS*IPT; explicit ld/st.shared keep ptxas from re-deriving the
+    // shared window address every step)
+    const uint32_t sc = static_cast<uint32_t>(__cvta_generic_to_shared(s_cum));
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s_anc));
+    auto step = [&]() {
+      const bool ta = b >= N || ca < ub;
+      const uint32_t av = static_cast<uint32_t>(base + (a < N - 1 ? a : N - 1));
+      asm volatile(
+          "{\n .reg .pred p;\n setp.eq.u32 p, %2, 0;\n @p st.shared.u32 [%0], %1;\n}\n" ::"r"(
+              sa + 4u * slot(b)),
+          "r"(av), "r"(static_cast<uint32_t>(ta))
+          : "memory");
+      a += ta;
+      b += !ta;
+      const int i = ta ? a : b;
+      const uint32_t idx = slot(i) + (ta ? 0u : static_cast<uint32_t>(THREADS * IPT));
+      double nv;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(nv) : "r"(sc + 8u * idx));
+      nv = i < N ? nv : INFINITY;
+      ca = ta ? nv : ca;
+      ub = ta ? ub : nv;
+    };
+    if (d1 - d0 == 2 * IPT) {  // every diagonal but the ones past 2N
 #pragma unroll
-    for (int st = 0; st < 2 * IPT; ++st) {
-      if (st < nsteps) {
-        const bool ta = b >= N || ca < ub;
-        if (!ta) s_anc[slot(b)] = static_cast<int32_t>(base + (a < N - 1 ? a : N - 1));
-        a += ta;
-        b += !ta;
-        const int i = ta ? a : b;
-        const double *src = (ta ? s_cum : s_u) + slot(i);
-        const double nv = i < N ? *src : INFINITY;
-        ca = ta ? nv : ca;
-        ub = ta ? ub : nv;
-      }
+      for (int st = 0; st < 2 * IPT; ++st) step();
+    } else {
+      for (int st = d0; st < d1; ++st) step();
     }
   }
   __syncthreads();
