@@ -412,10 +412,15 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
   {
     auto slot = [](unsigned i) { return (i & (IPT - 1)) * THREADS + i / IPT; };
     const int d0 = min(tid * 2 * IPT, 2 * N), d1 = min(d0 + 2 * IPT, 2 * N);
+    const uint32_t sc = static_cast<uint32_t>(__cvta_generic_to_shared(s_cum));
+    const uint32_t su = sc + 8u * static_cast<uint32_t>(THREADS * IPT);
     int lo = max(0, d0 - N), hi = min(d0, N);
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (s_cum[slot(mid)] < s_u[slot(d0 - 1 - mid)])
+      double cm, um;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cm) : "r"(sc + 8u * slot(mid)));
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(um) : "r"(su + 8u * slot(d0 - 1 - mid)));
+      if (cm < um)
         lo = mid + 1;
       else
         hi = mid;
@@ -428,7 +433,6 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
     // sequences addressed from one 32-bit shared base (s_u = s_cum +
     // THREADS*IPT; explicit ld/st.shared keep ptxas from re-deriving the
     // shared window address every step)
-    const uint32_t sc = static_cast<uint32_t>(__cvta_generic_to_shared(s_cum));
     const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s_anc));
     auto step = [&]() {
       const bool ta = b >= N || ca < ub;
