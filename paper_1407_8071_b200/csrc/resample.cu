@@ -1455,13 +1455,21 @@ __global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
     const int A = static_cast<int>(wlen);
     const int kcap = static_cast<int>(N - 1 - lo);
     const int32_t row0 = static_cast<int32_t>(base + lo);
+    // explicit 32-bit shared loads: ptxas otherwise re-derives the shared
+    // window address inside the search loops
+    const uint32_t scb = static_cast<uint32_t>(__cvta_generic_to_shared(s_c));
+    auto cs = [&](int i) {
+      double v;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(scb + 8u * static_cast<uint32_t>(i)));
+      return v;
+    };
     int k = 0;
     if (r0 < n) {
       int hi2 = A;
       const double x = u[0];
       while (k < hi2) {
         const int mid = (k + hi2) >> 1;
-        if (s_c[mid] < x)
+        if (cs(mid) < x)
           k = mid + 1;
         else
           hi2 = mid;
@@ -1469,7 +1477,7 @@ __global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
     }
 #pragma unroll
     for (int q = 0; q < kRun; ++q) {
-      if (r0 + q < n) k = advance_to<int>([&](int i) { return s_c[i]; }, k, A, u[q]);
+      if (r0 + q < n) k = advance_to<int>(cs, k, A, u[q]);
       a[q] = row0 + (k < kcap ? k : kcap);
     }
   } else if (wlen <= kWin) {
