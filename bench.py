@@ -514,35 +514,34 @@ def run_ours(args, cfg):
                          est_row_offset=lo)
     bank.load_observations(obs)
     bank.init()
-    exch = pdist.EstimateExchange(est_full) if world > 1 else None
+    comm = None
+    if world > 1:
+        # the native driver all-reduces each observation's disjoint-support
+        # estimate block over NCCL on a side stream (pf_comm, dist.NativeComm)
+        comm = pdist.native_comm()
+        if comm is None:
+            raise SystemExit("multi-GPU bench needs the native NCCL exchange (pf_comm)")
+        bank.set_exchange(comm, M * est_dim)
 
-    # warm-up, then K timed intervals through the native driver (pf_bank_run);
-    # CUDA events around each propagate launch (same stream) give the dominant
+    # warm-up, then K timed intervals in one native call (pf_bank_run); CUDA
+    # events around each propagate launch (same stream) give the dominant
     # kernel's duration inside the timed region
-    if exch:
-        for k in range(args.warmup):
-            bank.run_native(k, 1)
-            exch.step_done(k)
-        exch.finish()
-    else:
-        bank.run_native(0, args.warmup)
+    bank.run_native(0, args.warmup)
+    if comm is not None:
+        comm.join()
     bank.prepare_timing(args.steps)  # timing events outside the region
     _barrier(world)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kern_list = []
     with ClockSampler(local) as clocks:
         start.record()
-        if exch:  # one interval per call (its estimate all-reduce follows), no host waits
-            for i in range(args.steps):
-                k = args.warmup + i
-                bank.run_native(k, 1, time_propagate=True, slot=i)
-                exch.step_done(k)
-            exch.finish()
-            kern_list = bank.pool_propagate_ms(args.steps)
-        else:
-            kern_list = bank.run_native(args.warmup, args.steps, time_propagate=True)
+        # events recorded into the prepared pool: no host wait inside the region
+        bank.run_native(args.warmup, args.steps, slot=0)
+        if comm is not None:  # the last observation's exchange is part of the step
+            comm.join()
         end.record()
         torch.cuda.synchronize()
+    kern_list = bank.pool_propagate_ms(args.steps)
     _barrier(world)
     local_s = start.elapsed_time(end) / 1e3
     elapsed = _max_over_ranks(local_s, world)
@@ -563,15 +562,32 @@ def run_ours(args, cfg):
                 "algorithmic": f"{per_ps:.0f} B/particle-step (24 B/node: U,V fp32 + history "
                                f"bits, read + write) x {ps_per_launch} particle-steps per launch"}
     elif cfg["kind"] == "fhn":
-        achieved = ps_per_launch * FHN_BYTES_PER_PS / (kern_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "peak_source": peak_src,
-                "kernel": "fhn_fast_kernel<30,50,6> (fp32, Philox)",
-                "algorithmic": f"{FHN_BYTES_PER_PS:.0f} B/particle-step x {ps_per_launch} "
-                               f"particle-steps per launch"}
+        # The kernel keeps each particle on chip for all n_sub Euler steps
+        # (DESIGN §3), so HBM is not its bound: the headline is the issue
+        # roofline (SURVEY §7 hard part 3).  Beside it: the physical HBM
+        # fraction (bytes the launch must move / kernel time) and, labelled,
+        # the SURVEY §8d per-step streaming model.
+        pipes = _ncu_pipes(args.config)
+        roof = _issue_roofline(pipes, kern_ms) or {"bound": "issue", "achieved": None,
+                                                    "frac": None, "unit": "warp-inst/s"}
+        roof["kernel"] = "fhn_fast_kernel<30,50,6> (fp32, Philox)"
+        roof["algorithmic"] = (f"{pipes['warp_inst_per_launch']:.4g} warp instructions per "
+                               f"launch (ncu smsp__inst_executed.sum, same launch) / live "
+                               f"kernel time" if pipes else "no committed ncu count")
         phys = ps_per_launch / n_sub * (2 * 2 * model.nodes * 4 + 4 + 4)
-        roof["physical_bytes_per_launch"] = phys
-        roof["physical_gbs"] = phys / (kern_ms / 1e3) / 1e9
+        roof["hbm_physical"] = {
+            "bytes_per_launch": phys, "achieved": phys / (kern_ms / 1e3) / 1e9,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_source": peak_src,
+            "frac": phys / (kern_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+            "note": "gathered state read + state write (16 B/node) + logw + ancestor per "
+                    "particle per launch"}
+        model_gbs = ps_per_launch * FHN_BYTES_PER_PS / (kern_ms / 1e3) / 1e9
+        roof["streaming_model"] = {
+            "achieved": model_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": model_gbs / peaks["hbm_gbs"],
+            "note": f"SURVEY §8d model {FHN_BYTES_PER_PS:.0f} B/particle-step (16 B/node per "
+                    f"Euler step) x {ps_per_launch} particle-steps; NOT HBM traffic (the "
+                    f"kernel does not stream every step)"}
     else:
         achieved = ps_per_launch * LORENZ_FLOP_PER_PS / (kern_ms / 1e3) / 1e12
         fpk, fsrc = fp32_peak()
@@ -584,7 +600,8 @@ def run_ours(args, cfg):
     roof["kernel_share_of_step"] = kern_share
     roof["traffic"] = _ncu_traffic(args.config)
     roof["ncu_pipes"] = _ncu_pipes(args.config)
-    roof["issue"] = _issue_roofline(roof["ncu_pipes"], kern_ms)
+    if roof["bound"] != "issue":
+        roof["issue"] = _issue_roofline(roof["ncu_pipes"], kern_ms)
 
     # e2e through the public API (host observations in, host results out)
     if args.profile:
@@ -594,7 +611,7 @@ def run_ours(args, cfg):
     _barrier(world)
     e2e_obs = obs[: args.steps]
     # release the timed bank so the caching allocator can serve the e2e call
-    del bank, est_full, exch
+    del bank, est_full
     # one untimed call over the warm-up observations (first-use costs: lazy
     # module loading of the e2e path, allocator growth), then the timed call
     warm = pf.run_ensemble(model, obs[: max(args.warmup, 1)], "bootstrap", M, N, 7,
@@ -795,7 +812,8 @@ def _issue_roofline(pipes, kern_ms, sm_mhz=1965.0):
     achieved = pipes["warp_inst_per_launch"] / (kern_ms / 1e3)
     peak = 148 * 4 * sm_mhz * 1e6
     return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
-            "frac": achieved / peak,
+            "frac": achieved / peak, "peak_source": "148 SMs x 4 schedulers x 1 warp-inst/clk "
+                                                   f"x {sm_mhz:.0f} MHz",
             "source": "smsp__inst_executed.sum (profiles/pipes.json) / live kernel time"}
 
 
@@ -811,6 +829,37 @@ def _ncu_pipes(config):
         return None
 
 
+def _free_port():
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(n):
+    """`bench.py --gpus N` outside torchrun: re-exec this command under
+    torch.distributed.run with N ranks (one per GPU, NCCL), after checking
+    that N GPUs are visible - a box with fewer GPUs fails loudly instead of
+    silently measuring one rank.  NCCL_DEBUG=INFO (init subsystem) puts the
+    communicator lines, with their rank counts, on stderr."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} requested but {have} CUDA device(s) visible",
+                          "n_gpus": n}))
+        sys.stderr.write(f"bench.py: --gpus {n} needs {n} GPUs, found {have}\n")
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
@@ -823,6 +872,14 @@ def main():
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no e2e / CPU baseline): for ncu captures")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return launch_ranks(args.gpus)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        return 2
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference_arm(args, cfg)

@@ -200,6 +200,18 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
                                uint32_t t, const double *z_tape, uint32_t *status,
                                void *stream);
 
+/* Kernel selection for the *_ex entry points (per call; no process-wide
+ * state).  0 = the production choice.  PF_KERNEL_GENERIC forces the generic
+ * (runtime-geometry, accurate-libm) kernel instead of the specialised fast
+ * one, with the same Philox counters and draw layout - the comparison tests
+ * pin the fast kernels against it. */
+#define PF_KERNEL_GENERIC 1u
+int pf_lorenz_propagate_weight_ex(const pf_lorenz_params *p, pf_dtype dtype, const void *x_in,
+                                  const int32_t *anc, void *x_out, const double *y,
+                                  void *logw_out, int64_t M, int64_t N, const uint32_t *keys,
+                                  uint32_t t, const double *z_tape, uint32_t *status,
+                                  uint32_t flags, void *stream);
+
 /* One FH-N observation interval: n_sub lattice Euler steps with the particle
  * resident in shared memory/registers, ancestor gather fused into the load,
  * electrode log-likelihood fused into the epilogue.
@@ -208,6 +220,10 @@ int pf_fhn_interval(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
                     const int32_t *anc, void *x_out, const double *y, const int32_t *obs_idx,
                     void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
                     const double *z_tape, uint32_t *status, void *stream);
+int pf_fhn_interval_ex(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
+                       const int32_t *anc, void *x_out, const double *y, const int32_t *obs_idx,
+                       void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                       const double *z_tape, uint32_t *status, uint32_t flags, void *stream);
 
 /* normalize_log_weights + multinomial_resample_indices for M segments
  * (core.py:116-138, resampling.py:21-43, accel.py:175-203):
@@ -230,6 +246,12 @@ int pf_segmented_resample(pf_dtype logw_dtype, const void *logw, int64_t M, int6
  *    strictly sequential cumsum) so ancestors are bit-identical to the
  *    reference's for identical uniforms (oracle mode; slower). */
 #define PF_RS_REFERENCE_ORDER 1u
+/* Wide (N > 8192) production pipeline alternatives, same ancestors:
+ * PF_RS_WIDE_MERGE_PATH merges by merge path instead of the per-thread
+ * search; PF_RS_WIDE_GATHER_SEPARATE runs the ancestor gather as its own
+ * pass instead of fusing it into the merge's write-out. */
+#define PF_RS_WIDE_MERGE_PATH 2u
+#define PF_RS_WIDE_GATHER_SEPARATE 4u
 int pf_segmented_resample_ex(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
                              const double *u_tape, const uint32_t *keys, uint32_t t,
                              int32_t *anc_out, double *lnc, uint8_t *collapsed, uint32_t *status,
@@ -266,6 +288,12 @@ int pf_fhnnet_step(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
                    void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
                    const double *stim_tape, const double *z_tape, uint32_t *status,
                    void *stream);
+int pf_fhnnet_step_ex(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
+                      const uint32_t *q_in, const int32_t *anc, void *x_out, uint32_t *q_out,
+                      const double *forcing_mask, const double *y, const int32_t *obs_idx,
+                      void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                      const double *stim_tape, const double *z_tape, uint32_t *status,
+                      uint32_t flags, void *stream);
 /* Reference state rows (n, (2 + hold) * nodes) fp64 [U, V, Q(t) .. Q(t-hold+1)]
  * <-> device planes + history bits (fhn.py:122-138 unpack/pack).  Q entries
  * are indicators; any nonzero value packs as 1.  unpack gathers rows anc[p]
@@ -325,6 +353,32 @@ int pf_island_pool(const double *est, int64_t est_stride, int64_t M, int64_t dim
                    const double *log_weights, double *out, void *stream);
 /* out[0] = max + log(sum exp(lnc - max)) - log(M)  (filters.py:301-303). */
 int pf_island_trace(const double *lnc, int64_t M, double *out, void *stream);
+
+/* ---- multi-GPU estimate exchange (NCCL) --------------------
+ * Replaces the reference's fork pool + pickled per-filter estimates
+ * (ensemble.py:96-108).  One communicator per process group; rank 0 makes
+ * the id, the caller broadcasts it (torch.distributed), every rank calls
+ * pf_comm_init concurrently.  NCCL is bound at run time (the libnccl.so.2
+ * torch loaded); pf_comm_available() == 0 when it cannot be found.
+ * All-reduces run on the communicator's side stream after an event of the
+ * given stream; pf_comm_join makes `stream` wait for every exchange issued
+ * so far (no host wait). */
+#define PF_COMM_ID_BYTES 128
+typedef struct pf_comm pf_comm;
+int pf_comm_available(void);
+int pf_comm_nccl_version(void);
+int pf_comm_unique_id(uint8_t *id_out /* PF_COMM_ID_BYTES */);
+int pf_comm_init(const uint8_t *id, int32_t nranks, int32_t rank, pf_comm **out);
+int pf_comm_destroy(pf_comm *c);
+/* in-place sum over ranks of count doubles, ordered after `stream`'s work;
+ * `stream` waits for the result */
+int pf_comm_allreduce_f64(pf_comm *c, double *buf, int64_t count, void *stream);
+/* the per-observation exchanges of steps k0..k0+n_steps-1 of an estimate
+ * trace est[k*step_stride .. +count) without running a bank (a rank that
+ * owns no filters still joins every collective) */
+int pf_comm_exchange_steps(pf_comm *c, double *est, int64_t step_stride, int64_t count,
+                           int32_t k0, int32_t n_steps, void *stream);
+int pf_comm_join(pf_comm *c, void *stream);
 
 /* ---- native bank driver ------------------------------------------------ */
 /* Production-mode (Philox) bootstrap bank: runs observations k0..k0+n-1 back
@@ -387,6 +441,12 @@ typedef struct pf_bank_desc {
   uint32_t *q_tmp;     /* FH-N network lookahead history */
   double *lnc_before;  /* (M) */
   uint8_t *coll1;      /* (M) first-stage collapse flags */
+  uint32_t kernel_flags; /* PF_KERNEL_* for the propagate launches (0 = production) */
+  /* multi-GPU: after observation k's estimate, all-reduce the exch_count
+   * doubles at est + k*est_step_stride (the disjoint-support (M_total, width)
+   * block) over comm; NULL / 0 = single process */
+  pf_comm *comm;
+  int64_t exch_count;
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);

@@ -25,6 +25,9 @@ PF_ECUDA = -5
 PF_ST_DIVERGED = 1
 PF_ST_NAN_WEIGHT = 2
 PF_RS_REFERENCE_ORDER = 1
+PF_RS_WIDE_MERGE_PATH = 2
+PF_RS_WIDE_GATHER_SEPARATE = 4
+PF_KERNEL_GENERIC = 1
 PF_F32 = 0
 PF_F64 = 1
 
@@ -79,7 +82,8 @@ class BankDesc(ctypes.Structure):
                 ("step_ms", ctypes.POINTER(ctypes.c_float)), ("events", c_vp),
                 ("variant", c_i32), ("params0", c_vp), ("lam", c_vp), ("anc1", c_vp),
                 ("anc_comp", c_vp), ("x_tmp", c_vp), ("q_tmp", c_vp), ("lnc_before", c_vp),
-                ("coll1", c_vp)]
+                ("coll1", c_vp), ("kernel_flags", c_u32), ("comm", c_vp),
+                ("exch_count", c_i64)]
 
 
 PF_MODEL_LORENZ = 0
@@ -112,9 +116,15 @@ SIGNATURES = {
     "pf_lorenz_propagate_weight": (ctypes.c_int, [ctypes.POINTER(LorenzParams), ctypes.c_int,
                                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
                                                   c_vp, c_u32, c_vp, c_vp, c_vp]),
+    "pf_lorenz_propagate_weight_ex": (ctypes.c_int, [ctypes.POINTER(LorenzParams), ctypes.c_int,
+                                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
+                                                     c_vp, c_u32, c_vp, c_vp, c_u32, c_vp]),
     "pf_fhn_interval": (ctypes.c_int, [ctypes.POINTER(FhnParams), ctypes.c_int, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_u32, c_vp, c_vp,
                                        c_vp]),
+    "pf_fhn_interval_ex": (ctypes.c_int, [ctypes.POINTER(FhnParams), ctypes.c_int, c_vp, c_vp,
+                                          c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_u32, c_vp,
+                                          c_vp, c_u32, c_vp]),
     "pf_resample_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "pf_segmented_resample": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_u32,
                                              c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
@@ -128,6 +138,9 @@ SIGNATURES = {
     "pf_fhnnet_step": (ctypes.c_int, [ctypes.POINTER(FhnNetParams), ctypes.c_int, c_vp, c_vp,
                                       c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
                                       c_vp, c_u32, c_vp, c_vp, c_vp, c_vp]),
+    "pf_fhnnet_step_ex": (ctypes.c_int, [ctypes.POINTER(FhnNetParams), ctypes.c_int, c_vp, c_vp,
+                                         c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
+                                         c_vp, c_u32, c_vp, c_vp, c_vp, c_u32, c_vp]),
     "pf_fhnnet_pack": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "pf_fhnnet_unpack": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32,
                                         c_vp, c_vp]),
@@ -158,7 +171,17 @@ SIGNATURES = {
     "pf_apf_second_stage_weights": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pf_apf_finish": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pf_ensemble_average": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "pf_comm_available": (ctypes.c_int, []),
+    "pf_comm_nccl_version": (ctypes.c_int, []),
+    "pf_comm_unique_id": (ctypes.c_int, [c_vp]),
+    "pf_comm_init": (ctypes.c_int, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "pf_comm_destroy": (ctypes.c_int, [c_vp]),
+    "pf_comm_allreduce_f64": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "pf_comm_exchange_steps": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i64, c_i32, c_i32, c_vp]),
+    "pf_comm_join": (ctypes.c_int, [c_vp, c_vp]),
 }
+
+PF_COMM_ID_BYTES = 128
 
 _lock = threading.Lock()
 _lib = None

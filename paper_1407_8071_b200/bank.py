@@ -61,7 +61,8 @@ class FilterBank:
     def __init__(self, model, n_filters: int, n_particles: int, keys, n_steps: int, *,
                  dtype=None, tape: DrawTape | None = None, filter_offset: int = 0,
                  estimate: str = "full", est_buffer=None, est_row_offset: int = 0,
-                 reference_order: bool = True, variant: str = "bootstrap"):
+                 reference_order: bool = True, variant: str = "bootstrap",
+                 kernel_flags: int = 0):
         import torch
 
         _lib.require_cuda()
@@ -74,6 +75,9 @@ class FilterBank:
         if variant not in ("bootstrap", "auxiliary"):
             raise ValueError(f"unknown filter variant {variant!r}")
         self.variant = variant
+        # _lib.PF_KERNEL_GENERIC: the propagate launches use the generic
+        # kernels (comparison tests); 0 = production kernels
+        self.kernel_flags = int(kernel_flags)
         self.model = model
         self.M, self.N = int(n_filters), int(n_particles)
         self.MN = self.M * self.N
@@ -219,11 +223,11 @@ class FilterBank:
         s = _lib.stream_ptr()
         if self.model.kind == "fhnnet":
             stim, z = noise if noise is not None else (None, None)
-            _lib.call("pf_fhnnet_step", params, self.code, _lib.ptr(xin), _lib.ptr(qin),
+            _lib.call("pf_fhnnet_step_ex", params, self.code, _lib.ptr(xin), _lib.ptr(qin),
                       _lib.ptr(anc), _lib.ptr(xout), _lib.ptr(qout), _lib.ptr(self.fmask),
                       y_ptr, _lib.ptr(self.obs_idx), _lib.ptr(logw), self.M, self.N,
                       _lib.ptr(self.keys), t, _lib.ptr(stim), _lib.ptr(z),
-                      _lib.ptr(self.status), s)
+                      _lib.ptr(self.status), self.kernel_flags, s)
         elif self.model.kind in ("hmm", "lgm"):
             fn = "pf_hmm_propagate_weight" if self.model.kind == "hmm" else \
                 "pf_lgm_propagate_weight"
@@ -231,14 +235,15 @@ class FilterBank:
                       _lib.ptr(logw), self.M, self.N, _lib.ptr(self.keys), t, _lib.ptr(noise),
                       _lib.ptr(self.status), s)
         elif self.model.kind == "lorenz":
-            _lib.call("pf_lorenz_propagate_weight", params, self.code, _lib.ptr(xin),
+            _lib.call("pf_lorenz_propagate_weight_ex", params, self.code, _lib.ptr(xin),
                       _lib.ptr(anc), _lib.ptr(xout), y_ptr, _lib.ptr(logw), self.M, self.N,
-                      _lib.ptr(self.keys), t, _lib.ptr(noise), _lib.ptr(self.status), s)
+                      _lib.ptr(self.keys), t, _lib.ptr(noise), _lib.ptr(self.status),
+                      self.kernel_flags, s)
         else:
-            _lib.call("pf_fhn_interval", params, self.code, _lib.ptr(xin), _lib.ptr(anc),
+            _lib.call("pf_fhn_interval_ex", params, self.code, _lib.ptr(xin), _lib.ptr(anc),
                       _lib.ptr(xout), y_ptr, _lib.ptr(self.obs_idx), _lib.ptr(logw),
                       self.M, self.N, _lib.ptr(self.keys), t, _lib.ptr(noise),
-                      _lib.ptr(self.status), s)
+                      _lib.ptr(self.status), self.kernel_flags, s)
 
     def _resample(self, logw, uni, t, anc_out):
         _lib.call("pf_segmented_resample_ex", self.code, _lib.ptr(logw), self.M, self.N,
@@ -293,6 +298,13 @@ class FilterBank:
         d.est_dim = self.est_dim
         d.lnc_trace = self.lnc_tr.data_ptr()
         d.collapsed_trace = self.coll_tr.data_ptr()
+        d.kernel_flags = self.kernel_flags
+        comm = getattr(self, "comm", None)
+        if comm is not None:
+            if self.est.shape[1] * self.est_width != self.exch_count or self.est_row < 0:
+                raise ValueError("set_exchange: count must cover the whole (M_total, width) block")
+            d.comm = comm.handle
+            d.exch_count = self.exch_count
         if self.variant == "auxiliary":
             d.variant = 1
             d.params0 = ctypes.cast(ctypes.pointer(self.params0), ctypes.c_void_p)
@@ -302,6 +314,15 @@ class FilterBank:
             d.q_tmp = self.q_tmp.data_ptr() if self.q_tmp is not None else None
             d.lnc_before, d.coll1 = self.lnc_before.data_ptr(), self.coll1.data_ptr()
         return d
+
+    def set_exchange(self, comm, count: int):
+        """Multi-GPU: after each observation the native driver all-reduces the
+        `count` doubles of that observation's estimate block (est[k], the
+        caller's disjoint-support (M_total, width) buffer) over `comm`
+        (dist.NativeComm); None disables it."""
+        self.comm = comm
+        self.exch_count = int(count) if comm is not None else 0
+        self._desc = None
 
     def run_native(self, k0: int, n_steps: int, time_propagate: bool = False,
                    time_steps: bool = False, slot: int | None = None):

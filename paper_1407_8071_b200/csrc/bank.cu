@@ -10,18 +10,6 @@
 
 #include <vector>
 
-extern "C" int pf_lorenz_propagate_weight(const pf_lorenz_params *, pf_dtype, const void *,
-                                          const int32_t *, void *, const double *, void *,
-                                          int64_t, int64_t, const uint32_t *, uint32_t,
-                                          const double *, uint32_t *, void *);
-extern "C" int pf_fhnnet_step(const pf_fhnnet_params *, pf_dtype, const void *, const uint32_t *,
-                              const int32_t *, void *, uint32_t *, const double *, const double *,
-                              const int32_t *, void *, int64_t, int64_t, const uint32_t *,
-                              uint32_t, const double *, const double *, uint32_t *, void *);
-extern "C" int pf_fhn_interval(const pf_fhn_params *, pf_dtype, const void *, const int32_t *,
-                               void *, const double *, const int32_t *, void *, int64_t, int64_t,
-                               const uint32_t *, uint32_t, const double *, uint32_t *, void *);
-
 using namespace pf;
 
 // One propagate+weight launch of the descriptor's model with the given
@@ -32,9 +20,9 @@ static int bank_propagate(const pf_bank_desc *d, const void *params, const void 
                           const double *y, void *logw, uint32_t t, void *stream) {
   switch (d->model) {
     case PF_MODEL_LORENZ:
-      return pf_lorenz_propagate_weight(static_cast<const pf_lorenz_params *>(params), d->dtype,
-                                        xin, anc, xout, y, logw, d->M, d->N, d->keys, t, nullptr,
-                                        d->status, stream);
+      return pf_lorenz_propagate_weight_ex(static_cast<const pf_lorenz_params *>(params),
+                                           d->dtype, xin, anc, xout, y, logw, d->M, d->N, d->keys,
+                                           t, nullptr, d->status, d->kernel_flags, stream);
     case PF_MODEL_HMM:
       return pf_hmm_propagate_weight(static_cast<const pf_hmm_params *>(params), d->dtype, xin,
                                      anc, xout, y, logw, d->M, d->N, d->keys, t, nullptr,
@@ -44,13 +32,14 @@ static int bank_propagate(const pf_bank_desc *d, const void *params, const void 
                                      anc, xout, y, logw, d->M, d->N, d->keys, t, nullptr,
                                      d->status, stream);
     case PF_MODEL_FHNNET:
-      return pf_fhnnet_step(static_cast<const pf_fhnnet_params *>(params), d->dtype, xin, qin,
-                            anc, xout, qout, d->forcing_mask, y, d->obs_idx, logw, d->M, d->N,
-                            d->keys, t, nullptr, nullptr, d->status, stream);
+      return pf_fhnnet_step_ex(static_cast<const pf_fhnnet_params *>(params), d->dtype, xin,
+                               qin, anc, xout, qout, d->forcing_mask, y, d->obs_idx, logw, d->M,
+                               d->N, d->keys, t, nullptr, nullptr, d->status, d->kernel_flags,
+                               stream);
     default:
-      return pf_fhn_interval(static_cast<const pf_fhn_params *>(params), d->dtype, xin, anc,
-                             xout, y, d->obs_idx, logw, d->M, d->N, d->keys, t, nullptr,
-                             d->status, stream);
+      return pf_fhn_interval_ex(static_cast<const pf_fhn_params *>(params), d->dtype, xin, anc,
+                                xout, y, d->obs_idx, logw, d->M, d->N, d->keys, t, nullptr,
+                                d->status, d->kernel_flags, stream);
   }
 }
 
@@ -171,6 +160,13 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
       const int32_t nodes = d->fhnnet->J * d->fhnnet->J;
       rc = pf_bits_estimate(d->q[cur ^ 1], nodes, d->est_bits, d->anc, d->M, d->N,
                             est + d->est_dim, est_f, stream);
+      if (rc) return rc;
+    }
+    // multi-GPU: this observation's disjoint-support estimate block, summed
+    // over ranks on the communicator's side stream (overlaps the next interval)
+    if (d->comm && d->exch_count > 0) {
+      rc = comm_allreduce_after(d->comm, d->est + static_cast<int64_t>(k) * d->est_step_stride,
+                                d->exch_count, s);
       if (rc) return rc;
     }
     if (d->lnc_trace &&

@@ -69,6 +69,10 @@ int segmented_resample_fused(pf_dtype dtype, const void *logw, int64_t M, int64_
                              const void *x, int dim, double *est, int64_t est_stride,
                              cudaStream_t s, bool *fused);
 
+// multi-GPU exchange (comm.cu): all-reduce(sum) of count doubles at buf on
+// the communicator's side stream, ordered after the work enqueued on s
+int comm_allreduce_after(pf_comm *c, double *buf, int64_t count, cudaStream_t s);
+
 inline unsigned grid_for(int64_t n, int block) {
   return static_cast<unsigned>((n + block - 1) / block);
 }

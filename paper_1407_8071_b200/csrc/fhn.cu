@@ -105,12 +105,15 @@ __global__ void __launch_bounds__(256) fhn_interval_kernel(
                                                  kPurposeFhn),
                                       key);
             if (sizeof(T) == 4) {
-              const float2 g0 = box_muller_f32(rr.x, rr.y);
-              const float2 g1 = box_muller_f32(rr.z, rr.w);
-              zv[2 * q] = T(g0.x);
-              zw[2 * q] = T(g0.y);
-              zv[2 * q + 1] = T(g1.x);
-              zw[2 * q + 1] = T(g1.y);
+              // the fast kernel's draw layout, evaluated with accurate
+              // libm functions: words (x, y) -> v increments of rows 2q,
+              // 2q+1 (cos, sin), words (z, w) -> their w increments
+              const float2 gv = box_muller_ref_f32(rr.x, rr.y);
+              const float2 gw = box_muller_ref_f32(rr.z, rr.w);
+              zv[2 * q] = T(gv.x);
+              zv[2 * q + 1] = T(gv.y);
+              zw[2 * q] = T(gw.x);
+              zw[2 * q + 1] = T(gw.y);
             } else {
               const double2 g0 = box_muller_f64(rr.x, rr.y, rr.z, rr.w);
               const uint4 r2 = philox10(make_uint4(static_cast<uint32_t>(j), step0 + k,
@@ -613,6 +616,14 @@ int pf_fhn_interval(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
                     const int32_t *anc, void *x_out, const double *y, const int32_t *obs_idx,
                     void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
                     const double *z_tape, uint32_t *status, void *stream) {
+  return pf_fhn_interval_ex(p, dtype, x_in, anc, x_out, y, obs_idx, logw_out, M, N, keys, t,
+                            z_tape, status, 0u, stream);
+}
+
+int pf_fhn_interval_ex(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
+                       const int32_t *anc, void *x_out, const double *y, const int32_t *obs_idx,
+                       void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                       const double *z_tape, uint32_t *status, uint32_t flags, void *stream) {
   PF_REQUIRE(p && x_in && x_out && y && obs_idx && logw_out && status, "pf_fhn_interval: null");
   PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_fhn_interval: bad M/N");
   PF_REQUIRE(p->rows >= 1 && p->cols >= 1 && p->n_sub >= 0, "pf_fhn_interval: bad lattice");
@@ -626,7 +637,7 @@ int pf_fhn_interval(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
   const int64_t MN = M * N;
   const int32_t n32 = static_cast<int32_t>(N);
   const cudaStream_t s = as_stream(stream);
-  if (dtype == PF_F32 && fhn_fast_supported(p))
+  if (dtype == PF_F32 && fhn_fast_supported(p) && !(flags & PF_KERNEL_GENERIC))
     return launch_fhn_fast(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32, keys, t, z_tape,
                            status, s);
   if (dtype == PF_F64)

@@ -671,12 +671,12 @@ static int net_fast_warps(const NetConsts &c) {
 
 // The bulk-copy kernel serves fp32 Philox steps on lattices with J % 4 == 0
 // and J <= 32 (one 4-node group per compute thread).
-// PF_FHNNET_KERNEL=generic forces the generic kernel (comparison tests).
-static bool net_fast_ok(const NetConsts &c, pf_dtype dtype, bool tape) {
+// flags & PF_KERNEL_GENERIC (pf_fhnnet_step_ex) forces the generic kernel
+// (comparison tests).
+static bool net_fast_ok(const NetConsts &c, pf_dtype dtype, bool tape, uint32_t flags) {
   if (dtype != PF_F32 || tape || c.J % 4 != 0 || net_fast_warps(c) == 0)
     return false;
-  const char *env = std::getenv("PF_FHNNET_KERNEL");
-  return !(env && std::strcmp(env, "generic") == 0);
+  return !(flags & PF_KERNEL_GENERIC);
 }
 
 // Zone log-likelihood of stored rows (fhn.py:199-207), one warp per row:
@@ -786,6 +786,16 @@ int pf_fhnnet_step(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
                    void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
                    const double *stim_tape, const double *z_tape, uint32_t *status,
                    void *stream) {
+  return pf_fhnnet_step_ex(p, dtype, x_in, q_in, anc, x_out, q_out, forcing_mask, y, obs_idx,
+                           logw_out, M, N, keys, t, stim_tape, z_tape, status, 0u, stream);
+}
+
+int pf_fhnnet_step_ex(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
+                      const uint32_t *q_in, const int32_t *anc, void *x_out, uint32_t *q_out,
+                      const double *forcing_mask, const double *y, const int32_t *obs_idx,
+                      void *logw_out, int64_t M, int64_t N, const uint32_t *keys, uint32_t t,
+                      const double *stim_tape, const double *z_tape, uint32_t *status,
+                      uint32_t flags, void *stream) {
   PF_REQUIRE(p && x_in && q_in && x_out && q_out && forcing_mask && status,
              "pf_fhnnet_step: null argument");
   PF_REQUIRE(p->J >= 1 && p->stim_hold >= 1 && p->stim_hold <= 32,
@@ -803,7 +813,7 @@ int pf_fhnnet_step(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_in,
   const int64_t MN = M * N;
   const int32_t n32 = static_cast<int32_t>(N);
   const bool tape = p->stochastic && stim_tape;
-  if (net_fast_ok(c, dtype, tape)) {
+  if (net_fast_ok(c, dtype, tape, flags)) {
 #define PF_NET_FAST(CW)                                                                       \
   return c.stochastic                                                                        \
              ? launch_net_fast<CW, 3>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y,      \

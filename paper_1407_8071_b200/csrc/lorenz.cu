@@ -337,13 +337,6 @@ __global__ void lorenz_block_op_kernel(const double *__restrict__ st,
   out[3 * i + 2] = x3;
 }
 
-// PF_LORENZ_KERNEL=thread keeps one thread per particle for small banks too
-// (comparison tests)
-static bool force_thread_kernel() {
-  const char *e = std::getenv("PF_LORENZ_KERNEL");
-  return e && std::strcmp(e, "thread") == 0;
-}
-
 static LorenzConsts make_consts(const pf_lorenz_params *p) {
   LorenzConsts c;
   c.s = p->s;
@@ -394,6 +387,17 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
                                void *logw_out, int64_t M, int64_t N, const uint32_t *keys,
                                uint32_t t, const double *z_tape, uint32_t *status,
                                void *stream) {
+  return pf_lorenz_propagate_weight_ex(p, dtype, x_in, anc, x_out, y, logw_out, M, N, keys, t,
+                                       z_tape, status, 0u, stream);
+}
+
+// flags & PF_KERNEL_GENERIC keeps one thread per particle for small fp64
+// banks too (comparison tests of the warp-per-particle kernel).
+int pf_lorenz_propagate_weight_ex(const pf_lorenz_params *p, pf_dtype dtype, const void *x_in,
+                                  const int32_t *anc, void *x_out, const double *y,
+                                  void *logw_out, int64_t M, int64_t N, const uint32_t *keys,
+                                  uint32_t t, const double *z_tape, uint32_t *status,
+                                  uint32_t flags, void *stream) {
   PF_REQUIRE(p && x_in && x_out && y && logw_out && status, "pf_lorenz_propagate_weight: null");
   PF_REQUIRE(M >= 1 && N >= 1 && M * N <= INT32_MAX, "pf_lorenz_propagate_weight: bad M/N");
   PF_REQUIRE(p->n_sub >= 0, "substeps must be >= 0");
@@ -427,7 +431,7 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
     if (z_tape)
       lorenz_pw_kernel<double, 1><<<grid, 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32, p->obs_dim,
                                                        c, keys, t, z_tape, status);
-    else if (MN <= kSmallBank && !force_thread_kernel())
+    else if (MN <= kSmallBank && !(flags & PF_KERNEL_GENERIC))
       lorenz_small_kernel<<<grid_for(MN, 8), 256, 0, s>>>(xi, anc, xo, y, lw, MN, n32,
                                                           p->obs_dim, c, keys, t, status);
     else

@@ -135,16 +135,19 @@ __device__ __forceinline__ Key2 load_key(const uint32_t *keys, int64_t f) {
   return Key2{k.x, k.y};
 }
 
-// ---- fp32 Box-Muller: two N(0,1) from two 32-bit words ---------------------
-// radius from a 32-bit uniform in (0,1] (max |z| = sqrt(2*32*ln2) = 6.66),
-// angle from the top 24 bits.  Fast-path MUFU instructions (lg2, sqrt,
-// sin/cos); accuracy ~1e-6 relative, far below the Monte Carlo noise.
-__device__ __forceinline__ float2 box_muller_f32(uint32_t a, uint32_t b) {
+// ---- fp32 Box-Muller, accurate libm form (generic kernels) ------------------
+// The same map from two 32-bit words to two N(0,1) as box_muller_rad_trig
+// below - radius from u = (a + 1/2) 2^-32 in (0,1) (max |z| = 6.66), angle
+// pi*x - 3*pi from the low 23 bits of b (x in [2,4)) - but with accurate
+// logf/sqrtf/sincosf instead of the MUFU approximations, so a generic kernel
+// reproduces the fast kernels' draws to ~1e-6 and can check them.
+__device__ __forceinline__ float2 box_muller_ref_f32(uint32_t a, uint32_t b) {
   const float u = fmaf(static_cast<float>(a), 2.3283064365386963e-10f, 1.1641532182693481e-10f);
-  const float r = sqrtf(-1.3862943611198906f * __log2f(u));  // -2 ln u = -2 ln2 log2 u
-  const float ang = static_cast<float>(b >> 8) * 5.9604644775390625e-08f;  // [0,1)
+  const float r = sqrtf(-2.0f * logf(u));
+  const float x = __uint_as_float((b & 0x007fffffu) | 0x40000000u);
+  const float ang = fmaf(x, 3.14159265358979f, -9.42477796076938f);
   float s, c;
-  __sincosf(6.283185307179586f * ang, &s, &c);
+  sincosf(ang, &s, &c);
   return make_float2(r * c, r * s);
 }
 

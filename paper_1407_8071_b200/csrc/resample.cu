@@ -1765,16 +1765,11 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
   else
     wide2_partition<0><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape, keys, t);
   // merge -> ancestors (+ the fused gather)
-  static const bool search = [] {
-    const char *e = std::getenv("PF_WIDE_MERGE");
-    return !(e && std::strcmp(e, "path") == 0);
-  }();
+  // per-thread search (default) or merge path (flags & PF_RS_WIDE_MERGE_PATH)
+  const bool search = !(flags & PF_RS_WIDE_MERGE_PATH);
   // the ancestor gather fused into the merge's write-out (cfg1c: 1.00 ->
-  // 0.93 ms/step); PF_WIDE_GATHER=separate runs it as its own pass
-  static const bool fuse_gather = [] {
-    const char *e = std::getenv("PF_WIDE_GATHER");
-    return !(e && std::strcmp(e, "separate") == 0);
-  }();
+  // 0.93 ms/step); flags & PF_RS_WIDE_GATHER_SEPARATE runs it as its own pass
+  const bool fuse_gather = !(flags & PF_RS_WIDE_GATHER_SEPARATE);
   const bool fg = fuse_gather && gx_in && search;
   auto mk = u_tape ? (search ? (fg ? wide2_merge<1, true, true> : wide2_merge<1, false, true>)
                              : wide2_merge<1, false>)
@@ -1896,7 +1891,9 @@ int pf_segmented_resample_ex(pf_dtype logw_dtype, const void *logw, int64_t M, i
   PF_REQUIRE(u_tape || keys, "pf_segmented_resample_ex: need keys (Philox) or u_tape");
   PF_REQUIRE(!x_in || (x_out && dims >= 1 && x_in != x_out),
              "pf_segmented_resample_ex: gather needs x_out != x_in and dims >= 1");
-  PF_REQUIRE((flags & ~PF_RS_REFERENCE_ORDER) == 0, "pf_segmented_resample_ex: unknown flags");
+  PF_REQUIRE((flags & ~(PF_RS_REFERENCE_ORDER | PF_RS_WIDE_MERGE_PATH |
+                        PF_RS_WIDE_GATHER_SEPARATE)) == 0,
+             "pf_segmented_resample_ex: unknown flags");
   const cudaStream_t s = as_stream(stream);
   if (logw_dtype == PF_F64)
     return launch_resample<double>(logw, M, N, u_tape, keys, t, anc_out, lnc, collapsed, status,

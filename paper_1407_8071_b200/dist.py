@@ -82,6 +82,93 @@ class EstimateExchange:
             torch.cuda.current_stream(self.buffer.device).wait_stream(self.side)
 
 
+class NativeComm:
+    """The NCCL communicator of libpfbank's native exchange (pf_comm_*),
+    built over the default process group: rank 0 creates the NCCL id, the
+    group broadcasts it, every rank joins.  The native bank driver issues
+    each observation's estimate all-reduce itself (pf_bank_desc.comm), so a
+    sharded record is one host call per rank with no Python per observation.
+    """
+
+    def __init__(self):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        rank, size = world()
+        self.rank, self.size = rank, size
+        buf = (ctypes.c_uint8 * _lib.PF_COMM_ID_BYTES)()
+        if rank == 0:
+            _lib.call("pf_comm_unique_id", ctypes.cast(buf, ctypes.c_void_p))
+        if size > 1:
+            dev = torch.device("cuda", torch.cuda.current_device()) \
+                if dist.get_backend() == "nccl" else torch.device("cpu")
+            t = torch.tensor(list(bytes(buf)), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, src=0)
+            buf = (ctypes.c_uint8 * _lib.PF_COMM_ID_BYTES)(*t.cpu().tolist())
+        self.handle = ctypes.c_void_p()
+        _lib.call("pf_comm_init", ctypes.cast(buf, ctypes.c_void_p), size, rank,
+                  ctypes.byref(self.handle))
+        self.nccl_version = _lib.load().pf_comm_nccl_version()
+
+    def join(self, stream=None):
+        """The stream (default: current) waits for every exchange issued so far."""
+        from . import _lib
+
+        _lib.call("pf_comm_join", self.handle, _lib.stream_ptr(stream))
+
+    def allreduce_f64(self, t):
+        """In-place sum over ranks of a contiguous float64 CUDA tensor,
+        ordered on the current stream."""
+        from . import _lib
+
+        assert t.dtype.itemsize == 8 and t.is_contiguous() and t.is_cuda
+        _lib.call("pf_comm_allreduce_f64", self.handle, _lib.ptr(t), t.numel(),
+                  _lib.stream_ptr())
+        return t
+
+    def exchange_steps(self, est, k0, n_steps):
+        """The per-observation exchanges of est[k0:k0+n] (T, M, width) without a
+        bank (a rank that owns no filters joins every collective)."""
+        from . import _lib
+
+        _lib.call("pf_comm_exchange_steps", self.handle, _lib.ptr(est), est.stride(0),
+                  est[0].numel(), k0, n_steps, _lib.stream_ptr())
+
+    def close(self):
+        from . import _lib
+
+        if self.handle:
+            _lib.call("pf_comm_destroy", self.handle)
+            self.handle = None
+
+
+_NATIVE = {}
+
+
+def native_comm():
+    """The process's NativeComm for the default group (created on first use,
+    collectively: every rank must call it), or None when the group is not
+    NCCL or libpfbank cannot bind NCCL (then the torch EstimateExchange
+    path is used)."""
+    import torch.distributed as dist
+
+    from . import _lib
+
+    if not initialized() or dist.get_backend() != "nccl":
+        return None
+    if not _lib.load().pf_comm_available():
+        return None
+    key = (world(), id(dist.group.WORLD))
+    if key not in _NATIVE:
+        _NATIVE.clear()
+        _NATIVE[key] = NativeComm()
+    return _NATIVE[key]
+
+
 def allreduce_disjoint(t):
     """Blocking disjoint-support all-reduce (small end-of-run traces)."""
     import torch.distributed as dist

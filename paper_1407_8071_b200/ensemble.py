@@ -160,22 +160,39 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     dev = torch.device("cuda", torch.cuda.current_device())
     est_dim = estimate_width(model, estimate)
     est_full = torch.zeros((T, n_filters, est_dim), dtype=torch.float64, device=dev)
-    bank = FilterBank(model, hi - lo, n_particles, keys[lo:hi], T, dtype=dtype, tape=tape,
-                      filter_offset=lo, estimate=estimate, est_buffer=est_full,
-                      est_row_offset=lo, variant=variant)
-    bank.load_observations(obs)
-    bank.init()
-    exch = dist.EstimateExchange(est_full) if use_exch else None
+    # a rank whose block is empty (n_filters < world) runs no bank but still
+    # joins every collective, so no rank waits on another forever
+    bank = None
+    if hi > lo:
+        bank = FilterBank(model, hi - lo, n_particles, keys[lo:hi], T, dtype=dtype, tape=tape,
+                          filter_offset=lo, estimate=estimate, est_buffer=est_full,
+                          est_row_offset=lo, variant=variant)
+        bank.load_observations(obs)
+        bank.init()
+    # NCCL process group: the native driver issues the per-observation
+    # exchange itself (pf_comm); otherwise the torch side-stream exchange
+    comm = dist.native_comm() if use_exch else None
+    native = bank is None or bank._native_ok()
     secs = None
-    if exch is None and bank._native_ok():
-        # the whole record in one native call, per-step device times from it
-        bank.run_native(0, T, time_steps=True)
-        secs = bank.last_step_ms.astype(np.float64) / 1e3
+    if native and (not use_exch or comm is not None):
+        if bank is not None:
+            if comm is not None:
+                bank.set_exchange(comm, n_filters * est_dim)
+            # the whole record in one native call, per-step device times from it
+            bank.run_native(0, T, time_steps=True)
+            secs = bank.last_step_ms.astype(np.float64) / 1e3
+        else:
+            comm.exchange_steps(est_full, 0, T)
+            secs = np.zeros(T)
+        if comm is not None:
+            comm.join()
     else:
+        exch = dist.EstimateExchange(est_full) if use_exch else None
         events = [torch.cuda.Event(enable_timing=True) for _ in range(T + 1)]
         events[0].record()
         for k in range(T):
-            bank.step(k)
+            if bank is not None:
+                bank.step(k)
             events[k + 1].record()
             if exch is not None:
                 exch.step_done(k)
@@ -188,10 +205,18 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     lnc_full = torch.zeros((T, n_filters), dtype=torch.float64, device=dev)
     coll_full = torch.zeros((T, n_filters), dtype=torch.int32, device=dev)
     st_full = torch.zeros(n_filters, dtype=torch.int32, device=dev)
-    lnc_full[:, lo:hi] = bank.lnc_tr
-    coll_full[:, lo:hi] = bank.coll_tr.to(torch.int32)
-    st_full[lo:hi] = bank.status
-    if use_exch:
+    if bank is not None:
+        lnc_full[:, lo:hi] = bank.lnc_tr
+        coll_full[:, lo:hi] = bank.coll_tr.to(torch.int32)
+        st_full[lo:hi] = bank.status
+    if comm is not None:  # one packed exchange (small integers are exact in fp64)
+        packed = torch.cat([lnc_full.reshape(-1), coll_full.reshape(-1).double(),
+                            st_full.double()])
+        comm.allreduce_f64(packed)
+        lnc_full.copy_(packed[: T * n_filters].view(T, n_filters))
+        coll_full.copy_(packed[T * n_filters: 2 * T * n_filters].view(T, n_filters).to(torch.int32))
+        st_full.copy_(packed[2 * T * n_filters:].to(torch.int32))
+    elif use_exch:
         for t_ in (lnc_full, coll_full, st_full):
             dist.allreduce_disjoint(t_)
     torch.cuda.synchronize()

@@ -22,8 +22,8 @@ def _free_port():
 def test_shard_range_partitions_filters():
     for m in (1, 2, 7, 64, 4096):
         for w in (1, 2, 3, 8):
-            if m < w:
-                continue
+            # m < w: the high ranks own an empty block (they run no bank but
+            # join every collective, ensemble.run_ensemble)
             spans = [pdist.shard_range(m, r, w) for r in range(w)]
             assert spans[0][0] == 0 and spans[-1][1] == m
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
@@ -71,11 +71,12 @@ def _worker(rank, world, port, T, M, dim, q):
         dist.destroy_process_group()
 
 
-def test_disjoint_allreduce_two_ranks_bit_identical():
+@pytest.mark.parametrize("M", [7, 1])  # M=1 < world: rank 1 owns no filter
+def test_disjoint_allreduce_two_ranks_bit_identical(M):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, 5, 7, 4, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 5, M, 4, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in procs)
@@ -130,3 +131,46 @@ def test_island_exchange_two_ranks():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_bench_gpus_flag_fails_loudly_without_enough_gpus():
+    """`bench.py --gpus 2` on a box with fewer GPUs exits non-zero with an
+    error line instead of silently measuring one rank."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                       cwd=repo, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2, (r.returncode, r.stderr[-2000:])
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert "error" in line and line["n_gpus"] == 2
+
+
+def test_bench_launcher_spawns_one_rank_per_gpu(monkeypatch):
+    """With N GPUs visible and no WORLD_SIZE, bench.py re-execs itself under
+    torch.distributed.run with N ranks on 127.0.0.1 and NCCL init logging."""
+    import importlib
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, repo)
+    bench = importlib.import_module("bench")
+    seen = {}
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 8)
+    monkeypatch.setattr(subprocess, "call", lambda cmd, env: seen.update(cmd=cmd, env=env) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "8", "--steps", "5"])
+    assert bench.main() == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=8" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "8", "--steps", "5"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"
+    # under torchrun the world size must match --gpus
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    assert bench.main() == 2

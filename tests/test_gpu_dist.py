@@ -31,6 +31,15 @@ a = pf.run_ensemble(m, obs, "bootstrap", 6, 256, 3, shard=True)
 b = pf.run_ensemble(m, obs, "bootstrap", 6, 256, 3, shard=False)
 assert a.same_result(b), "exchange path changed the result"
 assert a.mean_estimates.tobytes() == b.mean_estimates.tobytes()
+# the sharded record ran through the native driver's NCCL exchange (pf_comm)
+from paper_1407_8071_b200 import dist as pdist
+assert pdist._NATIVE, "native NCCL exchange not used"
+fm, _, fobs = pf.simulate.fhn_truth(4, 3, pf.FhnLatticeModel())
+fa = pf.run_ensemble(fm, fobs, "bootstrap", 3, 64, 3, dtype="float32", estimate="projection",
+                     shard=True)
+fb = pf.run_ensemble(fm, fobs, "bootstrap", 3, 64, 3, dtype="float32", estimate="projection",
+                     shard=False)
+assert fa.same_result(fb), "FH-N exchange path changed the result"
 # double bootstrap: the sharded island path (disjoint all-reduces, island
 # materialisation, point-to-point exchange) equals the single-GPU path
 from paper_1407_8071_b200 import islands

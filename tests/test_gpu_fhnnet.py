@@ -278,19 +278,17 @@ def test_fast_kernel_matches_generic(golden, monkeypatch, J, noise_free):
     idx = torch.from_numpy(gm.obs_indices.astype(np.int32)).cuda()
     mask = gm.device_mask()
     outs = []
-    for kernel in ("fast", "generic"):
-        if kernel == "generic":
-            monkeypatch.setenv("PF_FHNNET_KERNEL", "generic")
+    for flags in (0, pf._lib.PF_KERNEL_GENERIC):
         x, q = gm.to_device(x0, dtype=torch.float32)
         xo, qo = torch.empty_like(x), torch.empty_like(q)
         lw = torch.empty(M * N, dtype=torch.float32, device="cuda")
         st = torch.zeros(M, dtype=torch.int32, device="cuda")
         for t in (81, 5000):  # forcing on / off
-            pf._lib.call("pf_fhnnet_step", gm.params(noise_free=noise_free), pf._lib.PF_F32,
-                         pf._lib.ptr(x),
+            pf._lib.call("pf_fhnnet_step_ex", gm.params(noise_free=noise_free),
+                         pf._lib.PF_F32, pf._lib.ptr(x),
                          pf._lib.ptr(q), pf._lib.ptr(anc), pf._lib.ptr(xo), pf._lib.ptr(qo),
                          pf._lib.ptr(mask), pf._lib.ptr(dy), pf._lib.ptr(idx), pf._lib.ptr(lw),
-                         M, N, pf._lib.ptr(keys), t, None, None, pf._lib.ptr(st),
+                         M, N, pf._lib.ptr(keys), t, None, None, pf._lib.ptr(st), flags,
                          pf._lib.stream_ptr())
             torch.cuda.synchronize()
             outs.append((gm.from_device(xo, qo), lw.cpu().numpy().copy(), st.cpu().numpy()))

@@ -575,26 +575,32 @@ def test_production_wide_chunked_filter_totals():
         assert chi2 < stats.chi2.ppf(0.999, df=B - 1), (f, chi2)
 
 
-def test_small_bank_warp_kernel_bit_identical(monkeypatch):
+def test_small_bank_warp_kernel_bit_identical():
     """fp64 production banks below 2^15 particles run one warp per particle
     (RNG in parallel, lane 0 runs the substep chain); the result is
-    bit-identical to the thread-per-particle kernel."""
+    bit-identical to the thread-per-particle kernel (PF_KERNEL_GENERIC)."""
     truth0, _, obs = orc.lorenz_truth(seed=8, n_obs=6)
     gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
                           prior_mean=tuple(truth0), prior_var=1.0)
-    outs = []
-    for kernel in ("warp", "thread"):
-        if kernel == "thread":
-            monkeypatch.setenv("PF_LORENZ_KERNEL", "thread")
-        outs.append(pf.run_ensemble(gm, obs, "bootstrap", 4, 1000, 5))
-    assert outs[0].same_result(outs[1])
-    # odd substep count: the last pair's second substep is dropped
     gm3 = pf.Lorenz63Model(substeps=3, prior_mean=tuple(truth0))
-    monkeypatch.delenv("PF_LORENZ_KERNEL")
-    a = pf.run_filter(gm3, obs[:, :1], "bootstrap", 100, 2)
-    monkeypatch.setenv("PF_LORENZ_KERNEL", "thread")
-    b = pf.run_filter(gm3, obs[:, :1], "bootstrap", 100, 2)
-    assert a.same_result(b)
+
+    def run(model, y, M, N, flags):
+        bank = pf.FilterBank(model, M, N, pf.philox.filter_keys(5, M), len(y),
+                             kernel_flags=flags)
+        bank.load_observations(y)
+        bank.init()
+        bank.run()
+        torch.cuda.synchronize()
+        bank.check_status()
+        return (bank.est.cpu().numpy(), bank.lnc_tr.cpu().numpy(), bank.anc.cpu().numpy(),
+                bank.x[bank.cur].cpu().numpy())
+
+    for model, y, M, N in ((gm, obs, 4, 1000), (gm3, obs[:, :1], 1, 100)):
+        # odd substep count (gm3): the last pair's second substep is dropped
+        a = run(model, y, M, N, 0)
+        b = run(model, y, M, N, _lib.PF_KERNEL_GENERIC)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
