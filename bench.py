@@ -530,13 +530,19 @@ def run_ours(args, cfg):
     if comm is not None:
         comm.join()
     bank.prepare_timing(args.steps)  # timing events outside the region
+    # launch-bound banks: the K intervals as one prebuilt CUDA graph
+    graph = bank.capture(args.warmup, args.steps, slot=0) if bank.use_graph and comm is None \
+        else None
     _barrier(world)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kern_list = []
     with ClockSampler(local) as clocks:
         start.record()
         # events recorded into the prepared pool: no host wait inside the region
-        bank.run_native(args.warmup, args.steps, slot=0)
+        if graph is not None:
+            graph.launch()
+        else:
+            bank.run_native(args.warmup, args.steps, slot=0)
         if comm is not None:  # the last observation's exchange is part of the step
             comm.join()
         end.record()
@@ -611,7 +617,8 @@ def run_ours(args, cfg):
     _barrier(world)
     e2e_obs = obs[: args.steps]
     # release the timed bank so the caching allocator can serve the e2e call
-    del bank, est_full
+    used_graph = graph is not None
+    del graph, bank, est_full
     # one untimed call over the warm-up observations (first-use costs: lazy
     # module loading of the e2e path, allocator growth), then the timed call
     warm = pf.run_ensemble(model, obs[: max(args.warmup, 1)], "bootstrap", M, N, 7,
@@ -650,6 +657,7 @@ def run_ours(args, cfg):
                            if cfg["kind"] in ("fhn", "fhnnet")
                            else "state < L2; compute-bound kernel"},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+                "cuda_graph": used_graph,
                 # per step: propagate + resample (+ the estimate pass unless the
                 # planar-state estimate is fused into the bank resampler)
                 "gpu_launches": (2 if cfg["kind"] == "lorenz" and N <= 8192 else 3) *

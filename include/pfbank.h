@@ -447,9 +447,23 @@ typedef struct pf_bank_desc {
    * block) over comm; NULL / 0 = single process */
   pf_comm *comm;
   int64_t exch_count;
+  /* nonzero: pf_bank_run captures its n_steps >= 2 intervals into one CUDA
+   * graph and launches it (launch-bound small banks; ignored with comm) */
+  int32_t use_graph;
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);
+
+/* The same intervals as pf_bank_run(d, k0, n_steps, cur, have_ancestors)
+ * captured once (on `stream`) into an instantiated CUDA graph; each
+ * pf_bank_graph_launch enqueues all of them.  The descriptor's buffers are
+ * baked in; d->events (if any) are recorded by the graph; comm and
+ * host-read timing (prop_ms/step_ms) are not allowed. */
+typedef struct pf_bank_graph pf_bank_graph;
+int pf_bank_graph_create(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
+                         int32_t have_ancestors, void *stream, pf_bank_graph **out);
+int pf_bank_graph_launch(pf_bank_graph *g, void *stream);
+int pf_bank_graph_destroy(pf_bank_graph *g);
 
 /* ---- auxiliary particle filter glue (filters.py:115-154) --------------- */
 /* First stage: filters whose lambda are all -inf get lambda := 0 (uniform

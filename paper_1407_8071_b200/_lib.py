@@ -83,7 +83,7 @@ class BankDesc(ctypes.Structure):
                 ("variant", c_i32), ("params0", c_vp), ("lam", c_vp), ("anc1", c_vp),
                 ("anc_comp", c_vp), ("x_tmp", c_vp), ("q_tmp", c_vp), ("lnc_before", c_vp),
                 ("coll1", c_vp), ("kernel_flags", c_u32), ("comm", c_vp),
-                ("exch_count", c_i64)]
+                ("exch_count", c_i64), ("use_graph", c_i32)]
 
 
 PF_MODEL_LORENZ = 0
@@ -171,6 +171,10 @@ SIGNATURES = {
     "pf_apf_second_stage_weights": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pf_apf_finish": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "pf_ensemble_average": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]),
+    "pf_bank_graph_create": (ctypes.c_int, [ctypes.POINTER(BankDesc), c_i32, c_i32, c_i32, c_i32,
+                                            c_vp, ctypes.POINTER(c_vp)]),
+    "pf_bank_graph_launch": (ctypes.c_int, [c_vp, c_vp]),
+    "pf_bank_graph_destroy": (ctypes.c_int, [c_vp]),
     "pf_comm_available": (ctypes.c_int, []),
     "pf_comm_nccl_version": (ctypes.c_int, []),
     "pf_comm_unique_id": (ctypes.c_int, [c_vp]),

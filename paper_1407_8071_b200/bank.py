@@ -62,7 +62,7 @@ class FilterBank:
                  dtype=None, tape: DrawTape | None = None, filter_offset: int = 0,
                  estimate: str = "full", est_buffer=None, est_row_offset: int = 0,
                  reference_order: bool = True, variant: str = "bootstrap",
-                 kernel_flags: int = 0):
+                 kernel_flags: int = 0, graph: bool | None = None):
         import torch
 
         _lib.require_cuda()
@@ -81,6 +81,10 @@ class FilterBank:
         self.model = model
         self.M, self.N = int(n_filters), int(n_particles)
         self.MN = self.M * self.N
+        # launch-bound banks run their native records as one CUDA graph
+        # (pf_bank_desc.use_graph); graph=None picks it for banks of up to
+        # 2^20 particles, whose intervals are tens of microseconds
+        self.use_graph = bool(graph) if graph is not None else self.MN <= (1 << 20)
         self.T = int(n_steps)
         self.dtype = _torch_dtype(dtype)
         self.code = _lib.dtype_code(self.dtype)
@@ -299,6 +303,7 @@ class FilterBank:
         d.lnc_trace = self.lnc_tr.data_ptr()
         d.collapsed_trace = self.coll_tr.data_ptr()
         d.kernel_flags = self.kernel_flags
+        d.use_graph = 1 if self.use_graph else 0
         comm = getattr(self, "comm", None)
         if comm is not None:
             if self.est.shape[1] * self.est_width != self.exch_count or self.est_row < 0:
@@ -385,6 +390,31 @@ class FilterBank:
                                           for i in range(n_steps)], dtype=np.float32)
         return [evs[4 * i + 1].elapsed_time(evs[4 * i + 2]) for i in range(n_steps)] \
             if time_propagate else None
+
+    def capture(self, k0: int, n_steps: int, slot: int | None = None) -> "BankGraph":
+        """Capture observations k0..k0+n_steps-1 (the next ones this bank
+        would run) into one instantiated CUDA graph (pf_bank_graph_create);
+        BankGraph.launch() then enqueues them all.  slot=i records the
+        prepare_timing pool's events i.. like run_native(..., slot=i)."""
+        import ctypes
+
+        if not self._native_ok():
+            raise RuntimeError("capture: production banks only")
+        if self._desc is None:
+            self._desc = self._bank_desc()
+        if slot is not None:
+            evs, handles = self._slot_pool
+            if 4 * (slot + n_steps) > len(evs):
+                raise ValueError("capture: slot beyond the prepared timing pool")
+            self._desc.events = ctypes.c_void_p(ctypes.addressof(handles) +
+                                                4 * slot * ctypes.sizeof(ctypes.c_void_p))
+        h = ctypes.c_void_p()
+        try:
+            _lib.call("pf_bank_graph_create", self._desc, k0, n_steps, self.cur,
+                      1 if self.steps_done > 0 else 0, _lib.stream_ptr(), ctypes.byref(h))
+        finally:
+            self._desc.events = None
+        return BankGraph(self, h, n_steps)
 
     def prepare_timing(self, n_steps: int):
         """Create the timing events of an n_steps run_native call ahead of time
@@ -516,3 +546,31 @@ class FilterBank:
     def collapse_steps(self) -> list[list[int]]:
         c = self.coll_tr.cpu().numpy()
         return [[int(k) + 1 for k in np.nonzero(c[:, f])[0]] for f in range(self.M)]
+
+
+class BankGraph:
+    """An instantiated CUDA graph of a bank's next n_steps intervals
+    (FilterBank.capture); launch() once advances the bank like run_native."""
+
+    def __init__(self, bank, handle, n_steps):
+        self.bank, self.handle, self.n_steps, self.launched = bank, handle, n_steps, False
+
+    def launch(self):
+        if self.launched:
+            raise RuntimeError("BankGraph: already launched (capture a new one)")
+        _lib.call("pf_bank_graph_launch", self.handle, _lib.stream_ptr())
+        self.launched = True
+        self.bank.cur ^= self.n_steps & 1
+        self.bank.steps_done += self.n_steps
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                import torch
+
+                torch.cuda.synchronize()
+                _lib.load().pf_bank_graph_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self.handle = None

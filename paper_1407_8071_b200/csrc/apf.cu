@@ -24,9 +24,18 @@ __global__ void apf_prepare_kernel(T *__restrict__ lam, int32_t N, uint8_t *__re
   __shared__ double scratch[33];
   const int64_t f = blockIdx.x, base = f * N;
   double mx = -INFINITY;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) mx = fmax(mx, static_cast<double>(lam[base + i]));
+  int nan = 0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double x = static_cast<double>(lam[base + i]);
+    nan |= isnan(x);
+    mx = fmax(mx, x);  // fmax drops NaN: tracked separately
+  }
   const double m = block_max(mx, scratch);
-  const bool collapse = m == -INFINITY;  // NaN is left to the resampler (ValueError)
+  // np.max is NaN as soon as one lambda is (core.py:127-133): then lambda is
+  // left untouched so the first-stage resampler flags it (ValueError), even
+  // when every other value is -inf
+  const bool any_nan = __syncthreads_or(nan) != 0;
+  const bool collapse = !any_nan && m == -INFINITY;
   if (collapse)
     for (int i = threadIdx.x; i < N; i += blockDim.x) lam[base + i] = T(0);
   if (threadIdx.x == 0) coll1[f] = collapse ? 1 : 0;

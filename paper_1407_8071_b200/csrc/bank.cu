@@ -8,6 +8,7 @@
 // run at the device's launch rate.
 #include "common.cuh"
 
+#include <mutex>
 #include <vector>
 
 using namespace pf;
@@ -53,10 +54,9 @@ static const void *bank_params(const pf_bank_desc *d) {
   }
 }
 
-extern "C" {
+namespace {
 
-int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
-                int32_t have_ancestors, void *stream) {
+int bank_validate(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur) {
   PF_REQUIRE(d && n_steps >= 0 && k0 >= 0 && (cur == 0 || cur == 1), "pf_bank_run: bad arguments");
   PF_REQUIRE(d->model == PF_MODEL_LORENZ
                  ? d->lorenz != nullptr
@@ -70,31 +70,20 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
   PF_REQUIRE(d->x[0] && d->x[1] && d->logw && d->anc && d->lnc && d->collapsed && d->status &&
                  d->keys && d->obs && d->est,
              "pf_bank_run: null buffer");
-  const cudaStream_t s = as_stream(stream);
-  const int64_t MN = d->M * d->N;
-  // optional per-interval timing (events on the launch stream): start of the
-  // interval, around the (main) propagate kernel - the dominant one - and the
-  // end of the interval: 4 events per interval
-  struct Events {
-    std::vector<cudaEvent_t> e;
-    ~Events() {
-      for (cudaEvent_t x : e) cudaEventDestroy(x);
-    }
-  } evs;
-  cudaEvent_t *ev = nullptr;
-  if (d->events && n_steps > 0) {
-    // caller-owned, pre-created timing events: record only, no host wait
-    ev = reinterpret_cast<cudaEvent_t *>(d->events);
-  } else if ((d->prop_ms || d->step_ms) && n_steps > 0) {
-    evs.e.resize(4 * static_cast<size_t>(n_steps));
-    for (auto &x : evs.e) cudaEventCreate(&x);
-    ev = evs.e.data();
-  }
-  const bool apf = d->variant == 1;
-  PF_REQUIRE(!apf || (d->params0 && d->lam && d->anc1 && d->anc_comp && d->x_tmp &&
-                      d->lnc_before && d->coll1 &&
-                      (d->model != PF_MODEL_FHNNET || d->q_tmp)),
+  PF_REQUIRE(d->variant != 1 || (d->params0 && d->lam && d->anc1 && d->anc_comp && d->x_tmp &&
+                                 d->lnc_before && d->coll1 &&
+                                 (d->model != PF_MODEL_FHNNET || d->q_tmp)),
              "pf_bank_run: auxiliary variant needs params0 and the APF scratch buffers");
+  return PF_OK;
+}
+
+// Enqueue observations k0..k0+n_steps-1 on stream s (directly, or into a
+// graph being captured on s).  ev: NULL or 4 timing events per interval.
+int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
+                        int32_t have_ancestors, cudaStream_t s, cudaEvent_t *ev) {
+  void *stream = s;
+  const int64_t MN = d->M * d->N;
+  const bool apf = d->variant == 1;
   // planar states (x[d*MN + p]): the estimate is fused into the resampler
   const bool planar = d->model == PF_MODEL_LORENZ || d->model == PF_MODEL_HMM ||
                       d->model == PF_MODEL_LGM;
@@ -181,6 +170,132 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     cur ^= 1;
   }
   (void)MN;
+  return PF_OK;
+}
+
+}  // namespace
+
+// An instantiated CUDA graph of n_steps intervals (launch-bound banks: one
+// graph launch replaces ~4 launches per observation and their host costs).
+struct pf_bank_graph {
+  cudaGraphExec_t exec = nullptr;
+  int32_t n_steps = 0;
+};
+
+namespace {
+
+// Capture runs on a private stream (the caller's may be the legacy default
+// stream, which cannot capture); capturing executes nothing, and the graph
+// is launched on the caller's stream, so stream order is the caller's.
+cudaStream_t capture_stream() {
+  thread_local cudaStream_t cs[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 16) return nullptr;
+  if (!cs[dev]) cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking);
+  return cs[dev];
+}
+
+int graph_capture(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
+                  int32_t have_ancestors, cudaStream_t, cudaEvent_t *ev, pf_bank_graph **out) {
+  *out = nullptr;
+  cudaGetLastError();
+  const cudaStream_t s = capture_stream();
+  if (!s || cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed) != cudaSuccess)
+    return check_launch("pf_bank_graph: begin capture");
+  const int rc = bank_enqueue(d, k0, n_steps, cur, have_ancestors, s, ev);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s, &g);
+  if (rc != PF_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ce != cudaSuccess || !g) return check_launch("pf_bank_graph: end capture");
+  auto *bg = new pf_bank_graph();
+  bg->n_steps = n_steps;
+  const cudaError_t ie = cudaGraphInstantiate(&bg->exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ie != cudaSuccess) {
+    delete bg;
+    return check_launch("pf_bank_graph: instantiate");
+  }
+  *out = bg;
+  return PF_OK;
+}
+
+// Executable graphs of pf_bank_run calls: destroyed once their completion
+// event has fired (checked at the next call), never while still running.
+struct Retired {
+  cudaGraphExec_t exec;
+  cudaEvent_t done;
+};
+std::mutex g_retired_mu;
+std::vector<Retired> g_retired;
+
+void retire(cudaGraphExec_t exec, cudaStream_t s) {
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEventRecord(e, s);
+  std::lock_guard<std::mutex> lk(g_retired_mu);
+  g_retired.push_back({exec, e});
+}
+
+void reap() {
+  std::lock_guard<std::mutex> lk(g_retired_mu);
+  for (size_t i = 0; i < g_retired.size();) {
+    if (cudaEventQuery(g_retired[i].done) == cudaSuccess) {
+      cudaGraphExecDestroy(g_retired[i].exec);
+      cudaEventDestroy(g_retired[i].done);
+      g_retired[i] = g_retired.back();
+      g_retired.pop_back();
+    } else {
+      ++i;
+    }
+  }
+  cudaGetLastError();  // a pending (not ready) query is not an error
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
+                int32_t have_ancestors, void *stream) {
+  const int vr = bank_validate(d, k0, n_steps, cur);
+  if (vr != PF_OK) return vr;
+  const cudaStream_t s = as_stream(stream);
+  reap();
+  // optional per-interval timing (events on the launch stream): start of the
+  // interval, around the (main) propagate kernel - the dominant one - and the
+  // end of the interval: 4 events per interval
+  struct Events {
+    std::vector<cudaEvent_t> e;
+    ~Events() {
+      for (cudaEvent_t x : e) cudaEventDestroy(x);
+    }
+  } evs;
+  cudaEvent_t *ev = nullptr;
+  if (d->events && n_steps > 0) {
+    // caller-owned, pre-created timing events: record only, no host wait
+    ev = reinterpret_cast<cudaEvent_t *>(d->events);
+  } else if ((d->prop_ms || d->step_ms) && n_steps > 0) {
+    evs.e.resize(4 * static_cast<size_t>(n_steps));
+    for (auto &x : evs.e) cudaEventCreate(&x);
+    ev = evs.e.data();
+  }
+  int rc;
+  if (d->use_graph && n_steps >= 2 && !d->comm) {
+    pf_bank_graph *g = nullptr;
+    rc = graph_capture(d, k0, n_steps, cur, have_ancestors, s, ev, &g);
+    if (rc != PF_OK) return rc;
+    const cudaError_t le = cudaGraphLaunch(g->exec, s);
+    retire(g->exec, s);
+    delete g;
+    if (le != cudaSuccess) return check_launch("pf_bank_run: graph launch");
+  } else {
+    rc = bank_enqueue(d, k0, n_steps, cur, have_ancestors, s, ev);
+    if (rc != PF_OK) return rc;
+  }
   if (ev && !d->events) {
     cudaEventSynchronize(ev[4 * n_steps - 1]);
     for (int32_t i = 0; i < n_steps; ++i) {
@@ -189,6 +304,31 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     }
   }
   return check_launch("pf_bank_run");
+}
+
+int pf_bank_graph_create(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
+                         int32_t have_ancestors, void *stream, pf_bank_graph **out) {
+  PF_REQUIRE(out, "pf_bank_graph_create: null out");
+  const int vr = bank_validate(d, k0, n_steps, cur);
+  if (vr != PF_OK) return vr;
+  PF_REQUIRE(n_steps >= 1 && !d->comm && !d->prop_ms && !d->step_ms,
+             "pf_bank_graph_create: needs n_steps >= 1, no comm and no host-read timing");
+  return graph_capture(d, k0, n_steps, cur, have_ancestors, as_stream(stream),
+                       reinterpret_cast<cudaEvent_t *>(d->events), out);
+}
+
+int pf_bank_graph_launch(pf_bank_graph *g, void *stream) {
+  PF_REQUIRE(g && g->exec, "pf_bank_graph_launch: null graph");
+  if (cudaGraphLaunch(g->exec, as_stream(stream)) != cudaSuccess)
+    return check_launch("pf_bank_graph_launch");
+  return PF_OK;
+}
+
+int pf_bank_graph_destroy(pf_bank_graph *g) {
+  if (!g) return PF_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  delete g;
+  return PF_OK;
 }
 
 }  // extern "C"

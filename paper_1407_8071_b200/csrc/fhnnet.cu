@@ -624,7 +624,6 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
     if (lane == 0) {
-      mbar_arrive(&empty[k]);  // this warp is done with stage k
       if (logw) {
         s_part[k][warp] = part;
         __threadfence_block();
@@ -637,6 +636,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW 
           s_cnt[k] = 0;
         }
       }
+      // this warp is done with stage k - including its s_part / s_cnt slot,
+      // so no warp can reach item i+S (same stage) before item i's combine
+      // has read and reset them
+      mbar_arrive(&empty[k]);
     }
   }
 }

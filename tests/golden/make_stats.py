@@ -18,6 +18,9 @@ Writes tests/golden/stats.npz:
   - ``lz_est_mean`` / ``lz_est_m2`` (T, 3): mean over seeds of the ensemble
     estimate and of its square (bias^2 / variance decomposition against the
     proxy, metrics.bias_variance).
+  - ``lz_var_s`` (S,): per seed, mean over (t, d) of (estimate - lz_est_mean)^2
+    (its mean x S/(S-1) is the variance term of the MSE decomposition; its
+    spread gives that term's standard error).
 * cfg3 model (FH-N 30 x 50 lattice), truth seed 12, T = 10 observations,
   M = 4 x N = 64:
   - ``fhn_mse`` (S,): per master seed, mean over (t, node) of
@@ -83,6 +86,7 @@ def main():
     ap.add_argument("--workers", type=int, default=os.cpu_count())
     ap.add_argument("--lz-seeds", type=int, default=1024)
     ap.add_argument("--fhn-seeds", type=int, default=128)
+    ap.add_argument("--reuse-fhn", action="store_true")
     args = ap.parse_args()
     ctx = get_context("fork")
     out = {}
@@ -93,24 +97,26 @@ def main():
     out["lz_proxy"] = proxy
     print(f"proxy done {time.time() - t0:.0f}s", flush=True)
     S = args.lz_seeds
-    mse = np.empty(S)
-    s1 = np.zeros_like(proxy)
-    s2 = np.zeros_like(proxy)
+    ests = np.empty((S,) + proxy.shape)
     with ProcessPoolExecutor(args.workers, mp_context=ctx) as pool:
         for seed, est in pool.map(_lz_task, range(S), chunksize=4):
-            mse[seed] = ((est - proxy) ** 2).mean()
-            s1 += est
-            s2 += est * est
+            ests[seed] = est
+    mse = ((ests - proxy) ** 2).mean(axis=(1, 2))
     out["lz_mse"] = mse
-    out["lz_est_mean"] = s1 / S
-    out["lz_est_m2"] = s2 / S
+    out["lz_est_mean"] = ests.mean(axis=0)
+    out["lz_est_m2"] = (ests * ests).mean(axis=0)
+    out["lz_var_s"] = ((ests - ests.mean(axis=0)) ** 2).mean(axis=(1, 2))
     print(f"lorenz {S} seeds done {time.time() - t0:.0f}s: mse {mse.mean():.5f} "
           f"cv {mse.std(ddof=1) / mse.mean():.3f}", flush=True)
     F = args.fhn_seeds
     fmse = np.empty(F)
-    with ProcessPoolExecutor(args.workers, mp_context=ctx) as pool:
-        for seed, m in pool.map(_fhn_task, range(F)):
-            fmse[seed] = m
+    if args.reuse_fhn:  # keep the FH-N statistics of an existing fixture
+        fmse = np.load(os.path.join(HERE, "stats.npz"))["fhn_mse"]
+        F = fmse.shape[0]
+    else:
+        with ProcessPoolExecutor(args.workers, mp_context=ctx) as pool:
+            for seed, m in pool.map(_fhn_task, range(F)):
+                fmse[seed] = m
     out["fhn_mse"] = fmse
     print(f"fhn {F} seeds done {time.time() - t0:.0f}s: mse {fmse.mean():.6f} "
           f"cv {fmse.std(ddof=1) / fmse.mean():.3f}", flush=True)

@@ -176,3 +176,45 @@ def test_native_apf_driver_matches_stepwise(kind):
         assert np.linalg.norm(a[0] - b[0]) <= 1e-13 * np.linalg.norm(b[0])
         assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
         assert np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_first_stage_nan_is_not_a_collapse(dtype):
+    """core.py:127-133: np.max of first-stage log weights containing NaN is
+    NaN, so the reference raises ValueError - also when every other value is
+    -inf.  pf_apf_first_stage_prepare must leave such a filter's lambda
+    untouched (no uniform fallback) so the first-stage resampler flags it."""
+    from paper_1407_8071_b200 import _lib
+
+    M, N = 4, 64
+    lam = np.zeros((M, N))
+    lam[0] = -np.inf                      # a genuine collapse -> lambda := 0, flagged
+    lam[1] = np.nan                       # all NaN
+    lam[2] = -np.inf
+    lam[2, 7] = np.nan                    # NaN among -inf
+    lam[3] = np.random.default_rng(0).normal(size=N)
+    d = torch.from_numpy(lam.reshape(-1)).to(dtype).cuda()
+    coll1 = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    code = _lib.PF_F64 if dtype == torch.float64 else _lib.PF_F32
+    _lib.call("pf_apf_first_stage_prepare", code, _lib.ptr(d), M, N, _lib.ptr(coll1),
+              _lib.stream_ptr())
+    out = d.cpu().numpy().reshape(M, N).astype(np.float64)
+    assert coll1.cpu().numpy().tolist() == [1, 0, 0, 0]
+    assert np.all(out[0] == 0.0)
+    assert np.all(np.isnan(out[1])) and np.isnan(out[2, 7]) and np.isneginf(out[2, 0])
+    assert np.array_equal(out[3], lam[3].astype(np.float32 if dtype == torch.float32
+                                                else np.float64))
+    # the resampler then reports the NaN (-> ValueError on the host)
+    anc = torch.empty(M * N, dtype=torch.int32, device="cuda")
+    lnc = torch.zeros(M, dtype=torch.float64, device="cuda")
+    coll = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    st = torch.zeros(M, dtype=torch.int32, device="cuda")
+    keys = torch.from_numpy(pf.philox.filter_keys(1, M).view(np.int32)).cuda()
+    _lib.call("pf_segmented_resample_ex", code, _lib.ptr(d), M, N, None, _lib.ptr(keys), 1,
+              _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st), None, 0, None, None,
+              0, 0, _lib.stream_ptr())
+    status = st.cpu().numpy()
+    assert (status[1] & _lib.PF_ST_NAN_WEIGHT) and (status[2] & _lib.PF_ST_NAN_WEIGHT)
+    assert not (status[0] & _lib.PF_ST_NAN_WEIGHT) and not (status[3] & _lib.PF_ST_NAN_WEIGHT)
+    with pytest.raises(ValueError):
+        _lib.raise_status(status)

@@ -1,0 +1,80 @@
+"""CUDA-graph execution of the native interval pipeline (launch-bound small
+banks, SURVEY §7 hard part 5) is bit-identical to stream launches: the
+graph replays exactly the kernels pf_bank_run would enqueue (propagate,
+resample with fused estimate, trace copies; the auxiliary filter's full
+apf_step sequence).  Reference loop being replaced: filters.py:184-191."""
+
+import numpy as np
+import pytest
+
+from oracle import parpf_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1407_8071_b200 as pf  # noqa: E402
+
+
+def _models():
+    truth0, _, obs = orc.lorenz_truth(seed=8, n_obs=12)
+    lz = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
+                          prior_mean=tuple(truth0), prior_var=1.0)
+    fm, _, fobs = pf.simulate.fhn_truth(5, 4, pf.FhnLatticeModel())
+    return [(lz, obs, "float64", "bootstrap"), (lz, obs, "float32", "auxiliary"),
+            (fm, fobs, "float32", "bootstrap")]
+
+
+def _state(bank):
+    torch.cuda.synchronize()
+    bank.check_status()
+    return [t.cpu().numpy() for t in (bank.est, bank.lnc_tr, bank.coll_tr, bank.anc,
+                                      bank.x[bank.cur])]
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_graph_run_native_bit_identical(case):
+    model, obs, dtype, variant = _models()[case]
+    M, N, T = 4, 256, len(obs)
+    outs = []
+    for graph in (False, True):
+        bank = pf.FilterBank(model, M, N, pf.philox.filter_keys(3, M), T, dtype=dtype,
+                             variant=variant, graph=graph,
+                             estimate="projection" if model.kind == "fhn" else "full")
+        bank.load_observations(obs)
+        bank.init()
+        bank.run_native(0, 1)          # first interval (no ancestors yet), stream launch
+        bank.run_native(1, T - 1)      # the rest: one graph when graph=True
+        outs.append(_state(bank))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_capture_then_launch_equals_run_native():
+    model, obs, dtype, _ = _models()[0]
+    M, N, T = 4, 1000, len(obs)
+    outs = []
+    for use_capture in (False, True):
+        bank = pf.FilterBank(model, M, N, pf.philox.filter_keys(9, M), T, dtype=dtype)
+        bank.load_observations(obs)
+        bank.init()
+        bank.run_native(0, 3)
+        bank.prepare_timing(T - 3)
+        if use_capture:
+            g = bank.capture(3, T - 3, slot=0)
+            g.launch()
+            with pytest.raises(RuntimeError):
+                g.launch()
+        else:
+            bank.run_native(3, T - 3, slot=0)
+        ms = bank.pool_propagate_ms(T - 3)
+        assert all(m > 0 for m in ms)
+        outs.append(_state(bank))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    # run_ensemble on a small bank goes through the graph path and matches
+    # the explicit stream-launched bank
+    out = pf.run_ensemble(model, obs, "bootstrap", M, N, 9)
+    assert np.array_equal(np.stack([o.estimates for o in out.filter_outputs], axis=1), outs[0][0])

@@ -32,3 +32,21 @@ def test_sorted_uniform_rows_match_reference_draws():
     for f in range(3):
         assert np.array_equal(a[f], orc.sorted_uniforms(50, rng))
     assert np.all(np.diff(a, axis=1) >= 0) and np.all((a > 0) & (a < 1))
+
+
+def test_streaming_ensemble_equals_run_ensemble():
+    """oracle.tapes.StreamingEnsemble (the full-size oracle-mode runs) draws
+    and computes exactly what run_ensemble does."""
+    from oracle import tapes
+
+    truth0, _, obs = orc.lorenz_truth(seed=3, n_obs=4)
+    m = orc.LorenzConfigModel(prior_mean=tuple(truth0))
+    traces, _ = orc.run_ensemble(m, obs, 3, 50, 7, keep_steps=True)
+    se = tapes.StreamingEnsemble(m, obs, 3, 50, 7)
+    assert np.array_equal(se.prior, np.stack([t.prior_noise for t in traces]))
+    for k in range(4):
+        r = se.step(k)
+        assert np.array_equal(r["noise"], np.stack([t.steps[k].noise for t in traces]))
+        assert np.array_equal(r["ancestors"], np.stack([t.steps[k].ancestors for t in traces]))
+        assert np.array_equal(r["estimates"], np.stack([t.estimates[k] for t in traces]))
+        assert np.array_equal(r["lnc"], np.array([t.log_norm_const[k] for t in traces]))
