@@ -83,6 +83,12 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
                         int32_t have_ancestors, cudaStream_t s, cudaEvent_t *ev) {
   void *stream = s;
   const int64_t MN = d->M * d->N;
+  // inside a graph capture a plain event record only orders captured work;
+  // timing events must become external event-record nodes of the graph
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const unsigned rec_flags =
+      cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
   const bool apf = d->variant == 1;
   // planar states (x[d*MN + p]): the estimate is fused into the resampler
   const bool planar = d->model == PF_MODEL_LORENZ || d->model == PF_MODEL_HMM ||
@@ -95,7 +101,7 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
     const int32_t *anc = (have_ancestors || i > 0) ? d->anc : nullptr;
     const double *y = d->obs + static_cast<int64_t>(k) * d->dim_y;
     int rc;
-    if (ev) cudaEventRecord(ev[4 * i], s);
+    if (ev) cudaEventRecordWithFlags(ev[4 * i], s, rec_flags);
     uint32_t *qin = d->q[cur], *qout = d->q[cur ^ 1];
     const int32_t *src_anc = anc;
     if (apf) {
@@ -117,19 +123,27 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
       if (rc) return rc;
       src_anc = d->anc_comp;
     }
-    if (ev) cudaEventRecord(ev[4 * i + 1], s);
+    if (ev) cudaEventRecordWithFlags(ev[4 * i + 1], s, rec_flags);
     rc = bank_propagate(d, bank_params(d), xin, qin, src_anc, xout, qout, y, d->logw, t, stream);
     if (!rc && apf)  // second stage weights log w - lambda[anc1] (filters.py:143)
       rc = pf_apf_second_stage_weights(d->dtype, d->logw, d->lam, d->anc1, MN, stream);
-    if (ev) cudaEventRecord(ev[4 * i + 2], s);
+    if (ev) cudaEventRecordWithFlags(ev[4 * i + 2], s, rec_flags);
     if (rc) return rc;
     double *est = d->est + static_cast<int64_t>(k) * d->est_step_stride + d->est_offset;
     const int64_t est_f0 = d->est_stride_f ? d->est_stride_f : d->est_dim;
     bool fused = false;
+    // planar states: estimate and both trace rows written by the resampler
+    // itself (one launch per interval besides the propagate)
+    double *lnc_row = d->lnc_trace ? d->lnc_trace + static_cast<int64_t>(k) * d->M : nullptr;
+    uint8_t *coll_row =
+        d->collapsed_trace ? d->collapsed_trace + static_cast<int64_t>(k) * d->M : nullptr;
+    // (the auxiliary filter finishes lnc / collapse after the resample: its
+    // trace rows are copied afterwards)
     if (planar && d->est_stride_p == 1 && d->est_stride_d == MN)
       rc = segmented_resample_fused(d->dtype, d->logw, d->M, d->N, d->keys, t, d->anc, d->lnc,
                                     d->collapsed, d->status, d->ws, d->ws_bytes, xout,
-                                    d->est_dim, est, est_f0, s, &fused);
+                                    d->est_dim, est, est_f0, apf ? nullptr : lnc_row,
+                                    apf ? nullptr : coll_row, s, &fused);
     else
       rc = pf_segmented_resample_ex(d->dtype, d->logw, d->M, d->N, nullptr, d->keys, t, d->anc,
                                     d->lnc, d->collapsed, d->status, d->ws, d->ws_bytes, nullptr,
@@ -158,15 +172,16 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
                                 d->exch_count, s);
       if (rc) return rc;
     }
-    if (d->lnc_trace &&
-        cudaMemcpyAsync(d->lnc_trace + static_cast<int64_t>(k) * d->M, d->lnc,
-                        d->M * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    const bool traced = fused && !apf;  // rows already written by the resampler
+    if (!traced && lnc_row &&
+        cudaMemcpyAsync(lnc_row, d->lnc, d->M * sizeof(double), cudaMemcpyDeviceToDevice, s) !=
+            cudaSuccess)
       return check_launch("pf_bank_run(lnc trace)");
-    if (d->collapsed_trace &&
-        cudaMemcpyAsync(d->collapsed_trace + static_cast<int64_t>(k) * d->M, d->collapsed,
-                        d->M * sizeof(uint8_t), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    if (!traced && coll_row &&
+        cudaMemcpyAsync(coll_row, d->collapsed, d->M * sizeof(uint8_t), cudaMemcpyDeviceToDevice,
+                        s) != cudaSuccess)
       return check_launch("pf_bank_run(collapse trace)");
-    if (ev) cudaEventRecord(ev[4 * i + 3], s);
+    if (ev) cudaEventRecordWithFlags(ev[4 * i + 3], s, rec_flags);
     cur ^= 1;
   }
   (void)MN;

@@ -67,7 +67,7 @@ int segmented_resample_fused(pf_dtype dtype, const void *logw, int64_t M, int64_
                              const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
                              uint8_t *collapsed, uint32_t *status, void *ws, size_t ws_bytes,
                              const void *x, int dim, double *est, int64_t est_stride,
-                             cudaStream_t s, bool *fused);
+                             double *lnc_tr, uint8_t *coll_tr, cudaStream_t s, bool *fused);
 
 // multi-GPU exchange (comm.cu): all-reduce(sum) of count doubles at buf on
 // the communicator's side stream, ordered after the work enqueued on s

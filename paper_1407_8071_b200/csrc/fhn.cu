@@ -459,235 +459,6 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
   }
 }
 
-// ---- warp-specialised production kernel (fp32, Philox) -------------------
-// Same particle-per-CTA layout, strips and counters as fhn_fast_kernel, but
-// the Gaussian increments are made by NRW dedicated RNG warps one Euler step
-// AHEAD into a double-buffered shared array, while the compute warps run the
-// stencil.  Philox4x32-10's 32x32->64 multiplies (IMAD.WIDE: a quarter-rate
-// instruction on the FMA-heavy pipe) and Box-Muller's lg2/sqrt/sin/cos (MUFU:
-// one warp instruction per 8 cycles per SMSP) of step k+1 then overlap the
-// FFMA/LDS work of step k on other warps, instead of each warp alternating
-// IMAD-bound, MUFU-bound and FFMA-bound phases in lock-step between the
-// per-step barriers (tools/probes/pipe_probe.cu measured the pipe rates;
-// profiles/r02_ncu_fhn_*.txt the effect).
-//
-// Draws: block b = node pair (row pair p = b / COLS, column b % COLS) with
-// counter (particle, step, b, kPurposeFhn) - exactly fhn_fast_kernel's - and
-// the same word -> normal map; the RNG warps store the scaled increments
-// (sig_v z, sig_w z) per compute thread as a 2R-float record [v rows | w rows]
-// read with 128-bit loads.
-constexpr int kWsRngWarps = 4;
-
-template <int ROWS, int COLS, int R>
-struct FhnWsGeom {
-  static constexpr int W = fhn_pitch(COLS, R);
-  static constexpr int P = (ROWS + 2) * W;
-  static constexpr int NSEG = ROWS / R;
-  static constexpr int NCT = NSEG * COLS;              // compute threads
-  static constexpr int NCW = (NCT + 31) / 32;          // compute warps
-  static constexpr int THREADS = (NCW + kWsRngWarps) * 32;
-  static constexpr int NRT = kWsRngWarps * 32;         // RNG threads
-  static constexpr int NPAIR = (ROWS / 2) * COLS;      // Philox blocks per step
-  static constexpr int BPT = (NPAIR + NRT - 1) / NRT;  // blocks per RNG thread
-  static constexpr int REC = 2 * R;                    // floats per compute thread
-  static constexpr int ZS = NCT * REC;                 // floats per step buffer
-  static constexpr size_t SMEM = (2 * P + 2 * ZS) * sizeof(float);
-  static_assert(ROWS % R == 0 && R % 2 == 0, "strips must tile the rows in Philox pairs");
-  static_assert(REC % 4 == 0, "128-bit increment records");
-};
-
-template <int ROWS, int COLS, int R>
-__global__ void __launch_bounds__(FhnWsGeom<ROWS, COLS, R>::THREADS, 2) fhn_ws_kernel(
-    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
-    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
-    int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
-    uint32_t *__restrict__ status) {
-  using G = FhnWsGeom<ROWS, COLS, R>;
-  constexpr int W = G::W, P = G::P, NODES = ROWS * COLS;
-  extern __shared__ __align__(16) float ws_smem[];
-  float *vsp = ws_smem;           // [2][P] v planes
-  float *zb = ws_smem + 2 * P;    // [2][ZS] increment records
-  __shared__ double red;
-  __shared__ int bad;
-  const int tid = threadIdx.x;
-  const bool rng = tid >= G::NCW * 32;
-  const int rt = tid - G::NCW * 32;  // RNG thread id
-  // compute-thread geometry
-  const int seg = tid / COLS;
-  const int col = tid - seg * COLS;
-  const bool active = !rng && tid < G::NCT;
-  const int row0 = seg * R;
-  const int lo = col == 0 ? 0 : -1;
-  const int ro = col == COLS - 1 ? 0 : 1;
-  const int base = (row0 + 1) * W + col;
-  const float *zrec = zb + tid * G::REC;
-  // RNG-thread blocks: record offset of each block's (v, w) increment pairs
-  int zoff[G::BPT];
-#pragma unroll
-  for (int i = 0; i < G::BPT; ++i) {
-    const int b = i * G::NRT + rt;
-    const int pair = b / COLS, bcol = b - pair * COLS;
-    const int bseg = pair / (R / 2), q = pair - bseg * (R / 2);
-    zoff[i] = (bseg * COLS + bcol) * G::REC + 2 * q;
-  }
-  const float s2v = -1.3862943611198906f * c.sig_v * c.sig_v;
-  const float s2w = -1.3862943611198906f * c.sig_w * c.sig_w;
-  const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
-
-  for (int64_t p = blockIdx.x; p < MN; p += gridDim.x) {
-    const int64_t f = p / N;
-    const uint32_t j = static_cast<uint32_t>(p - f * N);
-    const Key2 key = load_key(keys, f);
-    float v[R], w[R];
-    if (tid == 0) bad = 0;
-    PhiloxPreT pre[G::BPT];
-    PhiloxUni uni;
-    PhiloxKeys rk;
-    // one step's increments into buffer `buf` (RNG warps)
-    auto produce = [&](uint32_t step, int buf) {
-      const uint32_t c1k0 = step ^ key.k0;
-      float *z = zb + buf * G::ZS;
-#pragma unroll
-      for (int i = 0; i < G::BPT; ++i) {
-        if (i * G::NRT + rt < G::NPAIR) {
-          const uint4 rr = philox10_t(pre[i], uni, c1k0, rk);
-          float av, cv, sv, aw, cw, sw;
-          box_muller_rad_trig(rr.x, rr.y, s2v, av, cv, sv);
-          box_muller_rad_trig(rr.z, rr.w, s2w, aw, cw, sw);
-          *reinterpret_cast<float2 *>(z + zoff[i]) = make_float2(av * cv, av * sv);
-          *reinterpret_cast<float2 *>(z + zoff[i] + R) = make_float2(aw * cw, aw * sw);
-        }
-      }
-    };
-    if (rng) {
-      uni = philox_uni_t(j, kPurposeFhn, key);
-      rk = philox_round_keys(key);
-#pragma unroll
-      for (int i = 0; i < G::BPT; ++i)
-        pre[i] = philox_pre_t(j, static_cast<uint32_t>(i * G::NRT + rt), kPurposeFhn, key);
-      if (c.n_sub > 0) produce(step0, 0);
-    } else {
-      const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
-      const float *xs = xin + src * 2 * static_cast<int64_t>(NODES);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        v[r] = 0.f;
-        w[r] = 0.f;
-        if (active) {
-          const int node = (row0 + r) * COLS + col;
-          v[r] = __ldg(xs + node);
-          w[r] = __ldg(xs + NODES + node);
-          vsp[base + r * W] = v[r];
-        }
-      }
-    }
-    __syncthreads();
-
-    // Euler step k: compute warps from plane/buffer PAR, RNG warps make k+1
-    auto euler = [&](int k, auto par_c) {
-      constexpr int PAR = decltype(par_c)::value;
-      if (rng) {
-        if (k + 1 < c.n_sub) produce(step0 + k + 1, PAR ^ 1);
-      } else if (active) {
-        const float *cur = vsp + PAR * P + base;
-        float *nxt = vsp + (PAR ^ 1) * P + base;
-        float zz[G::REC];
-        const float4 *zr = reinterpret_cast<const float4 *>(zrec + PAR * G::ZS);
-#pragma unroll
-        for (int i = 0; i < G::REC / 4; ++i) {
-          const float4 q4 = zr[i];
-          zz[4 * i] = q4.x;
-          zz[4 * i + 1] = q4.y;
-          zz[4 * i + 2] = q4.z;
-          zz[4 * i + 3] = q4.w;
-        }
-        float up = row0 == 0 ? v[0] : cur[-W];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const float *cell = cur + r * W;
-          const float u = v[r];
-          const float dn = row0 + r == ROWS - 1 ? u : (r < R - 1 ? v[r + 1] : cell[W]);
-          const float nb = ((up + dn) + cell[lo]) + cell[ro];
-          // u + dt p3(u) - 4 dt c u (host-folded cubic) - dt w + dt c nb + sig_v z
-          float un = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
-          un = fmaf(-c.dt, w[r], un);
-          un = fmaf(c.dtc, nb, un);
-          un += zz[r];
-          w[r] = fmaf(c.wc, w[r], fmaf(c.uc, u, c.c0)) + zz[R + r];
-          nxt[r * W] = un;
-          up = u;
-          v[r] = un;
-        }
-      }
-      __syncthreads();
-    };
-    int k = 0;
-    for (; k + 1 < c.n_sub; k += 2) {
-      euler(k, std::integral_constant<int, 0>{});
-      euler(k + 1, std::integral_constant<int, 1>{});
-    }
-    if (k < c.n_sub) euler(k, std::integral_constant<int, 0>{});
-
-    // epilogue: divergence flag, store, electrode log-likelihood
-    if (active) {
-      bool fin = true;
-      float *xd = xout + p * 2 * static_cast<int64_t>(NODES);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int node = (row0 + r) * COLS + col;
-        fin = fin && isfinite(v[r]) && isfinite(w[r]);
-        xd[node] = v[r];
-        xd[NODES + node] = w[r];
-      }
-      if (!fin) bad = 1;
-    }
-    if (tid < 32) {
-      const float *fv = vsp + (c.n_sub & 1) * P;
-      double acc = 0.0;
-      for (int i = tid; i < c.n_obs; i += 32) {
-        const int n = __ldg(obs_idx + i);
-        const int rr = n / COLS;
-        const double rsd = __ldg(y + i) - static_cast<double>(fv[(rr + 1) * W + (n - rr * COLS)]);
-        acc = fma(rsd, rsd, acc);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-      if (tid == 0) red = acc;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      logw[p] = static_cast<float>(c.obs_coef * red);
-      if (bad) atomicOr(status + f, PF_ST_DIVERGED);
-    }
-    __syncthreads();
-  }
-}
-
-template <int ROWS, int COLS, int R>
-static int launch_fhn_ws(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
-                         const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
-                         int32_t N, const uint32_t *keys, uint32_t t, uint32_t *status,
-                         cudaStream_t s) {
-  using G = FhnWsGeom<ROWS, COLS, R>;
-  auto kern = fhn_ws_kernel<ROWS, COLS, R>;
-  static const int per_sm = [&] {
-    if (G::SMEM > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(G::SMEM));
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, G::THREADS, G::SMEM);
-    return n < 1 ? 1 : n;
-  }();
-  int sms = kSmCount, dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t grid = std::min<int64_t>(MN, static_cast<int64_t>(sms) * per_sm);
-  kern<<<static_cast<unsigned>(grid), G::THREADS, G::SMEM, s>>>(
-      static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
-      static_cast<float *>(logw), MN, N, fc, keys, t, status);
-  return check_launch("pf_fhn_interval(warp-specialised)");
-}
-
 // accel.fhn_euler_block (general form, fp64, per-node drive), one thread per
 // node, reference order.
 __global__ void fhn_block_op_kernel(const double *__restrict__ U, const double *__restrict__ V,
@@ -831,8 +602,8 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   if (c.sig_v == 0.0 && c.sig_w == 0.0)  // the auxiliary filter's point prediction
     return launch_fhn_fast_t<30, 50, false, 3, 1, true>(fc, x_in, anc, x_out, y, obs_idx, logw,
                                                         MN, N, keys, t, tape, status, s);
-  return launch_fhn_ws<30, 50, kFhnRows>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t,
-                                         status, s);
+  return launch_fhn_fast_t<30, 50, false, 2, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                                keys, t, tape, status, s);
 }
 
 }  // namespace pf

@@ -179,6 +179,8 @@ struct EstFuse {
   int64_t mn;
   double *est;  // filter f's row at est + f*stride
   int64_t stride;
+  double *lnc_tr;    // optional: this step's lnc trace row (lnc_tr[f] = lnc[f] after)
+  uint8_t *coll_tr;  // optional: this step's collapse trace row
 };
 constexpr int kEstMaxDim = 8;
 
@@ -199,6 +201,29 @@ __device__ __forceinline__ void est_block_write(double (&acc)[kEstMaxDim], int d
     double sum = s_red[threadIdx.x];
     for (int w = 1; w < THREADS / 32; ++w) sum = __dadd_rn(sum, s_red[w * kEstMaxDim + threadIdx.x]);
     dst[threadIdx.x] = __dmul_rn(sum, invN);
+  }
+}
+
+// The exponential spacing of element i is word (i & 3) of Philox block
+// (i >> 2, t, 0, kPurposeResample) (spacing_exp_fast).  wd[h] = the word of
+// element i + h for h < min(IPT, 4); i % IPT == 0, so for IPT < 4 the run
+// lies inside one block but need not start at its first word.
+template <int IPT>
+__device__ __forceinline__ void spacing_words(Key2 key, uint32_t t, int i, uint32_t *wd) {
+  const uint4 r = philox10(make_uint4(static_cast<uint32_t>(i >> 2), t, 0u, kPurposeResample), key);
+  if constexpr (IPT >= 4) {
+    wd[0] = r.x;
+    wd[1] = r.y;
+    wd[2] = r.z;
+    wd[3] = r.w;
+  } else if constexpr (IPT == 2) {
+    const bool upper = (i & 2) != 0;
+    wd[0] = upper ? r.z : r.x;
+    wd[1] = upper ? r.w : r.y;
+  } else {
+    static_assert(IPT == 1, "IPT must be 1, 2 or a multiple of 4");
+    const int w = i & 3;
+    wd[0] = w == 0 ? r.x : w == 1 ? r.y : w == 2 ? r.z : r.w;
   }
 }
 
@@ -300,6 +325,8 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
     if (tid == 0) {
       collapsed[f] = nan ? 0 : 1;
       if (nan) atomicOr(status + f, PF_ST_NAN_WEIGHT);
+      if (ef.lnc_tr) ef.lnc_tr[f] = lnc[f];
+      if (ef.coll_tr) ef.coll_tr[f] = nan ? 0 : 1;
     }
     return;
   }
@@ -325,10 +352,8 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
     double erun = 0.0;
 #pragma unroll
     for (int q = 0; q < IPT; q += 4) {
-      const uint4 r = philox10(make_uint4(static_cast<uint32_t>((i0 + q) >> 2), t, 0u,
-                                          kPurposeResample),
-                               key);
-      const uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+      uint32_t wd[4];
+      spacing_words<IPT>(key, t, i0 + q, wd);
 #pragma unroll
       for (int h = 0; h < 4 && q + h < IPT; ++h) {
         const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
@@ -376,10 +401,8 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
       double erun = 0.0;
 #pragma unroll
       for (int q = 0; q < IPT; q += 4) {
-        const uint4 r = philox10(make_uint4(static_cast<uint32_t>((i0 + q) >> 2), t, 0u,
-                                            kPurposeResample),
-                                 key);
-        const uint32_t wd[4] = {r.x, r.y, r.z, r.w};
+        uint32_t wd[4];
+        spacing_words<IPT>(key, t, i0 + q, wd);
 #pragma unroll
         for (int h = 0; h < 4 && q + h < IPT; ++h) {
           const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
@@ -521,7 +544,10 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
     collapsed[f] = 0;
     // log_mean_raw = (m + log(total)) - log(N); lnc += log_mean_raw
     const double lmr = __dsub_rn(__dadd_rn(m, log(total)), log(static_cast<double>(N)));
-    lnc[f] = __dadd_rn(lnc[f], lmr);
+    const double l = __dadd_rn(lnc[f], lmr);
+    lnc[f] = l;
+    if (ef.lnc_tr) ef.lnc_tr[f] = l;
+    if (ef.coll_tr) ef.coll_tr[f] = 0;
   }
 }
 
@@ -1621,6 +1647,200 @@ __global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
   }
 }
 
+// ---- wide path, production with fp32 log weights: no materialised CDF ------
+// wide_tile_cum + wide2_partition + wide2_merge write and re-read an fp64 CDF
+// (16 B per particle of the 52 B the pipeline moved).  Here the partition
+// works on the per-tile CDF offsets (twoff) only, and each merge CTA
+// recomputes the CDF of the few weight tiles its uniforms fall into, in
+// shared memory, from the fp32 log weights - with exactly wide_tile_cum<float,
+// true>'s arithmetic (same fp32 runs, same 256-thread block scan, same
+// offsets), so the ancestors are identical to the materialised pipeline's.
+
+// CDF of weight tile `tile` (filter f, tile index tt) into s_c, transposed
+// (element e at s_c[(e % kRun) * kPad + e / kRun]: conflict-free stores);
+// returns the tile's element count.  All kTileThreads threads participate.
+__device__ __forceinline__ int tile_cdf_f32(const float *__restrict__ logw, int64_t N,
+                                            int64_t tpf, const WideWs &ws, int64_t f,
+                                            int64_t tt, double m, double total, double *s_c,
+                                            double *scratch) {
+  const int64_t tile = f * tpf + tt;
+  const int64_t i0 = tt * kTile;
+  const int n = static_cast<int>(N - i0 < kTile ? N - i0 : kTile);
+  const int r0 = threadIdx.x * kRun;
+  float lf[kRun];
+  load_run_f(logw + f * N + i0 + r0, n - r0, ((f * N + i0) & 3) == 0, lf);
+  const double mt = ws.tmax[tile];
+  const bool live = mt != -INFINITY;
+  const float mtf = static_cast<float>(mt);
+  const double scale = live ? exp(__dsub_rn(mt, m)) / total : 0.0;
+  double v[kRun];
+  float pf = 0.f;
+#pragma unroll
+  for (int q = 0; q < kRun; ++q) {
+    if (live) pf += exp_fast(lf[q] - mtf);
+    v[q] = static_cast<double>(pf) * scale;
+  }
+  double tot;
+  const double off = __dadd_rn(ws.twoff[tile], block_exclusive_scan(v[kRun - 1], scratch, &tot));
+#pragma unroll
+  for (int q = 0; q < kRun; ++q) s_c[q * kPad + threadIdx.x] = __dadd_rn(off, v[q]);
+  return n;
+}
+
+// Partition on tile offsets: for each u-tile end, the weight tile its answer
+// lies in.  The first tile is the last one whose CDF offset lies below the
+// tile's first uniform (minus a relative margin that covers the different
+// association of the in-tile scan); the last, the last whose offset lies at
+// or below the last uniform (plus the margin).
+template <int MODE>
+__global__ void wide3_partition(int64_t N, int64_t tpf, int64_t ntiles, WideWs ws,
+                                const double *__restrict__ u_tape) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= 2 * ntiles) return;
+  const int64_t tile = g >> 1;
+  const bool last = g & 1;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  if (ws.flag[f]) return;
+  const int64_t i0 = tt * kTile;
+  const int64_t n = N - i0 < kTile ? N - i0 : kTile;
+  double u;
+  if (MODE == 1) {
+    u = u_tape[f * N + i0 + (last ? n - 1 : 0)];
+  } else {
+    const double c = last ? __dadd_rn(ws.teoff[tile], ws.tesum[tile]) : ws.teoff[tile];
+    u = c / ws.cN[f];
+  }
+  const double *off = ws.twoff + f * tpf;
+  // count of tiles whose offset is < x (first) / <= x (last)
+  const double x = last ? u * (1.0 + 1e-12) : u * (1.0 - 1e-12);
+  int64_t lo = 0, hi = tpf;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (last ? !(off[mid] > x) : off[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  const int64_t tsel = lo > 0 ? lo - 1 : 0;
+  if (last)
+    ws.khi[tile] = tsel;
+  else
+    ws.klo[tile] = tsel;
+}
+
+template <int MODE, bool GATHER>
+__global__ void __launch_bounds__(kTileThreads, 4) wide3_merge(
+    const float *__restrict__ logw, int64_t N, int64_t tpf, WideWs ws,
+    const double *__restrict__ u_tape, const uint32_t *__restrict__ keys, uint32_t t,
+    int32_t *__restrict__ anc, const float *__restrict__ gx_in, float *__restrict__ gx_out,
+    int gdims, int64_t gMN) {
+  __shared__ double s_c[kRun * kPad];     // one weight tile's CDF (transposed)
+  __shared__ int32_t s_a[kRun * kPad];    // ancestors (transposed)
+  __shared__ double scratch[33];
+  const int64_t tile = blockIdx.x;
+  const int64_t f = tile / tpf, tt = tile - f * tpf;
+  const int64_t i0 = tt * kTile;
+  const int n = static_cast<int>(N - i0 < kTile ? N - i0 : kTile);
+  const int64_t base = f * N;
+  if (ws.flag[f]) {  // collapse / NaN: identity ancestors (filters.py:105-109)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      anc[base + i0 + i] = static_cast<int32_t>(base + i0 + i);
+      if (GATHER)
+        for (int d = 0; d < gdims; ++d)
+          gx_out[d * gMN + base + i0 + i] = gx_in[d * gMN + base + i0 + i];
+    }
+    return;
+  }
+  // this thread's run of sorted uniforms, in registers
+  const int r0 = threadIdx.x * kRun;
+  double u[kRun];
+  if (MODE == 1) {
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) u[q] = r0 + q < n ? u_tape[base + i0 + r0 + q] : 2.0;
+  } else {
+    spacing_run(load_key(keys, f), t, i0 + r0, N, u);
+    double run = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      run = __dadd_rn(run, u[q]);
+      u[q] = run;
+    }
+    double tot;
+    const double eoff = block_exclusive_scan(run, scratch, &tot);
+    const double scale = ws.tesum[tile] / tot, teoff = ws.teoff[tile];
+    const double inv = 1.0 / ws.cN[f];
+#pragma unroll
+    for (int q = 0; q < kRun; ++q)
+      u[q] = r0 + q < n ? fma(__dadd_rn(eoff, u[q]), scale, teoff) * inv : 2.0;
+  }
+  const double m = ws.m[f], total = ws.total[f];
+  const int64_t t_lo = ws.klo[tile], t_hi = ws.khi[tile];
+  auto cs = [&](int i) { return s_c[(i & (kRun - 1)) * kPad + (i >> 3)]; };
+  static_assert(kRun == 8, "cs() index map assumes runs of 8");
+  int32_t a[kRun];
+  uint32_t done = 0;
+  int kl = 0;  // this thread's position inside the current tile
+  // walk the window tiles (normally 1-2); past t_hi only if a uniform is
+  // still unanswered (defensive: the margin makes that unreachable)
+  for (int64_t wt = t_lo; wt < tpf; ++wt) {
+    __syncthreads();  // previous tile consumed
+    const int len = tile_cdf_f32(logw, N, tpf, ws, f, wt, m, total, s_c, scratch);
+    __syncthreads();
+    const bool last = wt == tpf - 1;
+    const double cmax = cs(len - 1);
+    const int64_t e0 = wt * kTile;
+    if (wt != t_lo) kl = 0;
+#pragma unroll
+    for (int q = 0; q < kRun; ++q) {
+      if ((done >> q) & 1u) continue;
+      if (r0 + q >= n) {
+        a[q] = static_cast<int32_t>(base);
+        done |= 1u << q;
+        continue;
+      }
+      if (!(u[q] <= cmax) && !last) break;  // this and later uniforms: later tiles
+      kl = advance_to<int>(cs, kl, len, u[q]);
+      const int64_t k = e0 + kl;
+      a[q] = static_cast<int32_t>(base + (k < N - 1 ? k : N - 1));  // clamp (accel.py:183)
+      done |= 1u << q;
+    }
+    if (__syncthreads_and(done == 0xffu)) break;  // block-uniform exit
+    (void)t_hi;
+  }
+#pragma unroll
+  for (int q = 0; q < kRun; ++q) s_a[q * kPad + threadIdx.x] = a[q];
+  __syncthreads();
+  if (GATHER && gdims == 3) {
+    int32_t ai[kRun];
+#pragma unroll
+    for (int h = 0; h < kRun; ++h) {
+      const int e = threadIdx.x + h * kTileThreads;
+      ai[h] = e < n ? s_a[(e % kRun) * kPad + e / kRun] : 0;
+      if (e < n) anc[base + i0 + e] = ai[h];
+    }
+    float v[3][kRun];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int h = 0; h < kRun; ++h)
+        v[d][h] = threadIdx.x + h * kTileThreads < n ? __ldg(gx_in + d * gMN + ai[h]) : 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int h = 0; h < kRun; ++h) {
+        const int e = threadIdx.x + h * kTileThreads;
+        if (e < n) gx_out[d * gMN + base + i0 + e] = v[d][h];
+      }
+    return;
+  }
+  for (int e = threadIdx.x; e < n; e += kTileThreads) {
+    const int32_t ai = s_a[(e % kRun) * kPad + e / kRun];
+    anc[base + i0 + e] = ai;
+    if (GATHER)
+      for (int d = 0; d < gdims; ++d) gx_out[d * gMN + base + i0 + e] = __ldg(gx_in + d * gMN + ai);
+  }
+}
+
 // 3-plane fp32 gather, 4 consecutive particles per thread: one int4 ancestor
 // load, 12 independent gathered loads in flight, three float4 stores.
 __global__ void __launch_bounds__(256) gather3_kernel(const float *__restrict__ xin,
@@ -1678,17 +1898,24 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
                        double *, uint8_t *, uint32_t *, const float *, float *, int, int64_t,
                        EstFuse);
     K kern;
-    int threads;
+    int threads, ipt;
     const bool g = gx_in != nullptr;
 #define PF_PICK(TH, I)                                                                        \
   {                                                                                           \
     threads = TH;                                                                             \
+    ipt = I;                                                                                  \
     kern = u_tape ? (g ? resample_bank_kernel<TW, 1, TH, I, true>                             \
                        : resample_bank_kernel<TW, 1, TH, I, false>)                           \
                   : (g ? resample_bank_kernel<TW, 0, TH, I, true>                             \
                        : resample_bank_kernel<TW, 0, TH, I, false>);                          \
   }
-    if (N <= 256) PF_PICK(128, 2)
+    if (M < kSmCount && N > 256 && N <= 2048) {
+      // few filters (e.g. cfg0: 4 x 1000) leave most SMs idle and each CTA's
+      // serial run length is the latency: wide CTAs, 2 particles per thread
+      if (N <= 512) PF_PICK(256, 2)
+      else if (N <= 1024) PF_PICK(512, 2)
+      else PF_PICK(1024, 2)
+    } else if (N <= 256) PF_PICK(128, 2)
     else if (N <= 512) PF_PICK(128, 4)
     else if (N <= 1024) PF_PICK(128, 8)
     else if (N <= 2048) PF_PICK(256, 8)
@@ -1696,7 +1923,6 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
     else PF_PICK(512, 16)
 #undef PF_PICK
     // thread-major CDF slots: THREADS * IPT doubles (>= N)
-    const int ipt = N <= 256 ? 2 : N <= 512 ? 4 : N <= 1024 ? 8 : N <= 2048 ? 8 : 16;
     const size_t smem = static_cast<size_t>(threads) * ipt * (2 * sizeof(double) + 4);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1752,6 +1978,20 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
                                                                lnc, keys, t);
     }
     if constexpr (std::is_same<TW, float>::value) {
+      // production fp32 weights: no materialised CDF - partition on the tile
+      // offsets, the merge recomputes its tiles' CDF (wide3_*); the
+      // PF_RS_WIDE_* alternatives keep the materialised pipeline
+      if (!u_tape && !(flags & (PF_RS_WIDE_MERGE_PATH | PF_RS_WIDE_GATHER_SEPARATE))) {
+        wide3_partition<0><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape);
+        const bool g3 = gx_in != nullptr;
+        if (g3)
+          wide3_merge<0, true><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t,
+                                                           anc, gx_in, gx_out, gdims, M * N);
+        else
+          wide3_merge<0, false><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws, u_tape, keys, t,
+                                                            anc, nullptr, nullptr, 0, M * N);
+        return check_launch("pf_segmented_resample(wide, recomputed CDF)");
+      }
       if (!u_tape)
         wide_tile_cum<TW, true><<<nt, kTileThreads, 0, s>>>(logw, N, tpf, ws);
       else
@@ -1844,10 +2084,10 @@ int segmented_resample_fused(pf_dtype dtype, const void *logw, int64_t M, int64_
                              const uint32_t *keys, uint32_t t, int32_t *anc, double *lnc,
                              uint8_t *collapsed, uint32_t *status, void *ws, size_t ws_bytes,
                              const void *x, int dim, double *est, int64_t est_stride,
-                             cudaStream_t s, bool *fused) {
+                             double *lnc_tr, uint8_t *coll_tr, cudaStream_t s, bool *fused) {
   PF_REQUIRE(logw && anc && lnc && collapsed && status && keys && fused,
              "segmented_resample_fused: null");
-  const EstFuse ef{x, dim, M * N, est, est_stride};
+  const EstFuse ef{x, dim, M * N, est, est_stride, lnc_tr, coll_tr};
   if (dtype == PF_F64)
     return launch_resample<double>(logw, M, N, nullptr, keys, t, anc, lnc, collapsed, status, ws,
                                    ws_bytes, s, nullptr, nullptr, 0, 0u, &ef, fused);

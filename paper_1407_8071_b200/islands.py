@@ -49,6 +49,11 @@ class IslandBank:
         self.sharded = (world > 1 and shard is not False) or (shard is True and dist.initialized())
         if not self.sharded:
             rank, world = 0, 1
+        if n_islands < world:
+            # every rank takes this branch (same arguments), so all raise
+            # together before any collective - none is left waiting
+            raise ValueError(f"double bootstrap: {n_islands} islands cannot be sharded over "
+                             f"{world} ranks (need n_islands >= world size)")
         self.lo, self.hi = dist.shard_range(n_islands, rank, world)
         dev = torch.device("cuda", torch.cuda.current_device())
         kw = dict(device=dev)

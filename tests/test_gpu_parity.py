@@ -508,26 +508,37 @@ def _offspring_counts(lw, reps, flags, seed):
 
 
 @pytest.mark.parametrize("M,N,flags", [(64, 1024, 0), (2, 20000, 0), (2, 20000, 1),
-                                       (1, 1 << 20, 0), (1, (1 << 22) + 77, 0)])
+                                       (1, 1 << 20, 0), (1, (1 << 22) + 77, 0),
+                                       # every bank-kernel tile shape: 2 particles per
+                                       # thread (N <= 256; and the wide CTAs of few-filter
+                                       # banks, M < #SMs), 4, 8 and 16 per thread
+                                       (300, 64, 0), (200, 256, 0), (4, 1000, 0),
+                                       (3, 2000, 0), (5, 300, 0), (160, 512, 0),
+                                       (150, 4096, 0)])
 def test_production_resampling_is_multinomial(M, N, flags):
     """Offspring counts follow multinomial(N, w) (test_resampling.py:40-67
-    analogue): chi-square over 64 equal-mass bins per filter at 0.1 %."""
+    analogue): chi-square over B equal-mass bins per filter; the sum over a
+    bank's filters (df = M (B-1)) at 1e-4 and every filter at a Bonferroni
+    1e-4 / M - sensitive to a small systematic bias of the uniform stream."""
     from scipy import stats
 
     rng = np.random.default_rng(N + M)
     lw = rng.standard_normal((M, N)).astype(np.float32)
     w = np.exp(lw.astype(np.float64) - lw.max(axis=1, keepdims=True))
     w /= w.sum(axis=1, keepdims=True)
-    reps = 40
+    reps = 40 if N >= 1024 else max(40, (40 * 1024) // N)
     counts = _offspring_counts(lw, reps, flags, seed=3)
     assert np.all(counts.sum(axis=1) == reps * N)
-    B = 64
+    B = 64 if N >= 1024 else 16
+    chis = []
     for f in range(M):
         edges = np.searchsorted(np.cumsum(w[f]), np.linspace(0, 1, B + 1)[1:-1])
         obs = np.add.reduceat(counts[f], np.r_[0, edges])
         exp_ = np.add.reduceat(w[f], np.r_[0, edges]) * reps * N
-        chi2 = float(((obs - exp_) ** 2 / exp_).sum())
-        assert chi2 < stats.chi2.ppf(0.999, df=B - 1), (f, chi2)
+        chis.append(float(((obs - exp_) ** 2 / exp_).sum()))
+    chis = np.array(chis)
+    assert chis.sum() < stats.chi2.ppf(1 - 1e-4, df=M * (B - 1)), (chis.sum(), M * (B - 1))
+    assert chis.max() < stats.chi2.ppf(1 - 1e-4 / M, df=B - 1), (int(chis.argmax()), chis.max())
 
 
 def test_production_wide_chunked_filter_totals():
