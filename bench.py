@@ -531,7 +531,10 @@ def run_ours(args, cfg):
     M, N = cfg["M"], cfg["N"]
     if M % world:
         raise SystemExit(f"M={M} not divisible by {world} GPUs")
-    T = args.warmup + args.steps
+    # W warm-up + K timed intervals, then K more with CUDA events around the
+    # propagate kernel (its duration, for the roofline, without event nodes
+    # inside the timed region)
+    T = args.warmup + 2 * args.steps
     model, obs = _make_model_and_obs(cfg, T)
     n_sub = getattr(model, "substeps", 1)
     lo, hi = pdist.shard_range(M, rank, world)
@@ -553,31 +556,31 @@ def run_ours(args, cfg):
             raise SystemExit("multi-GPU bench needs the native NCCL exchange (pf_comm)")
         bank.set_exchange(comm, M * est_dim)
 
-    # warm-up, then K timed intervals in one native call (pf_bank_run); CUDA
-    # events around each propagate launch (same stream) give the dominant
-    # kernel's duration inside the timed region
+    # warm-up, then K timed intervals in one native call (pf_bank_run)
     bank.run_native(0, args.warmup)
     if comm is not None:
         comm.join()
-    bank.prepare_timing(args.steps)  # timing events outside the region
     # launch-bound banks: the K intervals as one prebuilt CUDA graph
-    graph = bank.capture(args.warmup, args.steps, slot=0) if bank.use_graph and comm is None \
-        else None
+    graph = bank.capture(args.warmup, args.steps) if bank.use_graph and comm is None else None
     _barrier(world)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kern_list = []
     with ClockSampler(local) as clocks:
         start.record()
-        # events recorded into the prepared pool: no host wait inside the region
         if graph is not None:
             graph.launch()
         else:
-            bank.run_native(args.warmup, args.steps, slot=0)
+            bank.run_native(args.warmup, args.steps)
         if comm is not None:  # the last observation's exchange is part of the step
             comm.join()
         end.record()
         torch.cuda.synchronize()
+    # the dominant kernel's duration: K more intervals, CUDA events around
+    # each propagate launch on its stream (prepared pool, no host waits)
+    bank.prepare_timing(args.steps)
+    bank.run_native(args.warmup + args.steps, args.steps, slot=0)
     kern_list = bank.pool_propagate_ms(args.steps)
+    if comm is not None:
+        comm.join()
     _barrier(world)
     local_s = start.elapsed_time(end) / 1e3
     elapsed = _max_over_ranks(local_s, world)
@@ -649,10 +652,10 @@ def run_ours(args, cfg):
     # release the timed bank so the caching allocator can serve the e2e call
     used_graph = graph is not None
     del graph, bank, est_full
-    # one untimed call over the warm-up observations (first-use costs: lazy
-    # module loading of the e2e path, allocator growth), then the timed call
-    warm = pf.run_ensemble(model, obs[: max(args.warmup, 1)], "bootstrap", M, N, 7,
-                           dtype=cfg["dtype"], estimate="projection")
+    # one untimed call of the same shape (first-use costs: lazy module
+    # loading of the e2e path, allocator growth), then the timed call
+    warm = pf.run_ensemble(model, e2e_obs, "bootstrap", M, N, 7, dtype=cfg["dtype"],
+                           estimate="projection")
     del warm
     torch.cuda.synchronize()
     _barrier(world)
@@ -792,7 +795,7 @@ def run_variant(args, cfg):
         if variant == "double-bf" else \
         (lambda o: pf.run_ensemble(model, o, variant, M, N, 7, dtype=cfg["dtype"],
                                    estimate="projection"))
-    call(obs[: max(args.warmup, 1)])  # untimed warm-up call
+    call(e2e_obs)  # untimed warm-up call (same shapes as the timed one)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     out = call(e2e_obs)

@@ -252,6 +252,10 @@ int pf_segmented_resample(pf_dtype logw_dtype, const void *logw, int64_t M, int6
  * pass instead of fusing it into the merge's write-out. */
 #define PF_RS_WIDE_MERGE_PATH 2u
 #define PF_RS_WIDE_GATHER_SEPARATE 4u
+/* fp32 log weights, production: no materialised fp64 CDF - the merge
+ * recomputes the CDF of the weight tiles its uniforms fall into (less HBM
+ * traffic, more instructions; same ancestors). */
+#define PF_RS_WIDE_RECOMPUTE 8u
 int pf_segmented_resample_ex(pf_dtype logw_dtype, const void *logw, int64_t M, int64_t N,
                              const double *u_tape, const uint32_t *keys, uint32_t t,
                              int32_t *anc_out, double *lnc, uint8_t *collapsed, uint32_t *status,

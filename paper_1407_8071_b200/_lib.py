@@ -27,6 +27,7 @@ PF_ST_NAN_WEIGHT = 2
 PF_RS_REFERENCE_ORDER = 1
 PF_RS_WIDE_MERGE_PATH = 2
 PF_RS_WIDE_GATHER_SEPARATE = 4
+PF_RS_WIDE_RECOMPUTE = 8
 PF_KERNEL_GENERIC = 1
 PF_F32 = 0
 PF_F64 = 1

@@ -1978,10 +1978,12 @@ static int launch_resample(const void *logw_v, int64_t M, int64_t N, const doubl
                                                                lnc, keys, t);
     }
     if constexpr (std::is_same<TW, float>::value) {
-      // production fp32 weights: no materialised CDF - partition on the tile
-      // offsets, the merge recomputes its tiles' CDF (wide3_*); the
-      // PF_RS_WIDE_* alternatives keep the materialised pipeline
-      if (!u_tape && !(flags & (PF_RS_WIDE_MERGE_PATH | PF_RS_WIDE_GATHER_SEPARATE))) {
+      // PF_RS_WIDE_RECOMPUTE: no materialised CDF - partition on the tile
+      // offsets, the merge recomputes its tiles' CDF (wide3_*).  Same
+      // ancestors; 2.4 instead of 3.4 GB per 2^26-particle step, but the
+      // merge recomputes ~2 tiles per uniform tile and measures slower (1.29
+      // vs 0.84 ms at cfg1c), so it is opt-in
+      if (!u_tape && (flags & PF_RS_WIDE_RECOMPUTE)) {
         wide3_partition<0><<<grid_for(2 * nt, 256), 256, 0, s>>>(N, tpf, nt, ws, u_tape);
         const bool g3 = gx_in != nullptr;
         if (g3)
@@ -2132,7 +2134,7 @@ int pf_segmented_resample_ex(pf_dtype logw_dtype, const void *logw, int64_t M, i
   PF_REQUIRE(!x_in || (x_out && dims >= 1 && x_in != x_out),
              "pf_segmented_resample_ex: gather needs x_out != x_in and dims >= 1");
   PF_REQUIRE((flags & ~(PF_RS_REFERENCE_ORDER | PF_RS_WIDE_MERGE_PATH |
-                        PF_RS_WIDE_GATHER_SEPARATE)) == 0,
+                        PF_RS_WIDE_GATHER_SEPARATE | PF_RS_WIDE_RECOMPUTE)) == 0,
              "pf_segmented_resample_ex: unknown flags");
   const cudaStream_t s = as_stream(stream);
   if (logw_dtype == PF_F64)

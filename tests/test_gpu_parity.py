@@ -719,3 +719,35 @@ def test_native_slot_timing_matches_one_call():
         res.append((bank.est.cpu().numpy(), bank.lnc_tr.cpu().numpy()))
     assert np.array_equal(res[0][0], res[1][0])
     assert np.array_equal(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("M,N,sigma", [(1, 1 << 20, 1.0), (1, 1 << 20, 10.0), (3, 70001, 3.0),
+                                       (2, 20000, 30.0)])
+def test_wide_pipeline_variants_identical(M, N, sigma):
+    """The wide production pipeline's alternatives - merge path instead of the
+    per-thread search, the gather as its own pass, and the CDF recomputed in
+    the merge instead of materialised (PF_RS_WIDE_*) - give bit-identical
+    ancestors, lnc and gathered states."""
+    rng = np.random.default_rng(int(sigma) + N)
+    lw = torch.from_numpy((rng.standard_normal(M * N) * sigma).astype(np.float32)).cuda()
+    x = torch.from_numpy(rng.standard_normal((3, M * N)).astype(np.float32)).cuda()
+    keys = torch.from_numpy(pf.philox.filter_keys(11, M).view(np.int32)).cuda()
+    wsb = _lib.load().pf_resample_workspace_bytes(M, N)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    outs = []
+    for flags in (0, _lib.PF_RS_WIDE_MERGE_PATH, _lib.PF_RS_WIDE_GATHER_SEPARATE,
+                  _lib.PF_RS_WIDE_RECOMPUTE):
+        anc = torch.empty(M * N, dtype=torch.int32, device="cuda")
+        lnc = torch.zeros(M, dtype=torch.float64, device="cuda")
+        coll = torch.zeros(M, dtype=torch.uint8, device="cuda")
+        st = torch.zeros(M, dtype=torch.int32, device="cuda")
+        xo = torch.empty_like(x)
+        _lib.call("pf_segmented_resample_ex", _lib.PF_F32, _lib.ptr(lw), M, N, None,
+                  _lib.ptr(keys), 5, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll), _lib.ptr(st),
+                  _lib.ptr(ws), wsb, _lib.ptr(x), _lib.ptr(xo), 3, flags, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        outs.append((anc.cpu().numpy(), lnc.cpu().numpy(), xo.cpu().numpy()))
+        assert np.all(np.diff(outs[-1][0].reshape(M, N), axis=1) >= 0)
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
