@@ -148,3 +148,26 @@ def test_library_binds_every_symbol_now(lib):
     from paper_1407_8071_b200 import _lib
 
     ctypes.CDLL(_lib.LIB_PATH, mode=os.RTLD_NOW)
+
+
+def test_nccl_bound_at_run_time(lib):
+    """pf_comm_* binds the libnccl.so.2 torch already loaded (no link-time
+    NCCL dependency; one NCCL per process)."""
+    import torch  # noqa: F401  (loads libnccl.so.2)
+
+    assert lib.pf_comm_available() == 1
+    assert lib.pf_comm_nccl_version() >= 21800
+    import subprocess
+
+    out = subprocess.run(["readelf", "-d", str(lib._name)], capture_output=True, text=True).stdout
+    assert "libnccl" not in out
+
+
+def test_kernel_flags_are_per_call():
+    """No process-wide kernel switches: the library's sources read no
+    environment variables (the generic/fast choice is the *_ex calls' flags
+    argument; the static CUDA runtime's own getenv use is not ours)."""
+    import glob
+
+    for path in glob.glob(os.path.join(REPO, "paper_1407_8071_b200", "csrc", "*.cu*")):
+        assert "getenv" not in open(path).read(), path

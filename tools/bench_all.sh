@@ -1,8 +1,10 @@
 #!/bin/bash
 # Round bench pass (GPU box): every bench.py workload with its CPU baseline,
 # the reference arm on the default workload, then the cfg1 sigma = 10 cases.
+#   bash tools/bench_all.sh [round-prefix, default r02]
 set -u
-out=gpurun_out/bench
+R=${1:-r02}
+out=gpurun_out/bench_$R
 mkdir -p $out
 for c in cfg4 cfg3 cfg2 cfg2m256 cfg1b cfg1c cfg0 net cfg4apf cfg2apf netapf dbf; do
   python bench.py --config $c > $out/$c.log 2>&1 || echo "FAILED $c" >> $out/failures.txt
