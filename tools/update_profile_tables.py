@@ -2,7 +2,7 @@
 summaries (profiles/r01_ncu_<kernel>_<config>.txt, written by ncu_summary.py)
 and the cfg1c launch list (the whole wide pipeline per step).
 
-    python tools/update_profile_tables.py [round-prefix, default r01]
+    python tools/update_profile_tables.py [round-prefix, default r02]
 """
 import csv
 import json
@@ -12,7 +12,7 @@ from collections import defaultdict
 
 ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles")
 CAPTURES = {"cfg4": "fhn_fast_cfg4", "cfg2": "lorenz_fast_cfg2", "cfg1b": "resample_bank_cfg1b",
-            "net": "fhnnet_fast_net", "cfg1c": "wide2_merge_cfg1c"}
+            "net": "fhnnet_fast_net", "cfg1c": "wide2_merge_cfg1c", "cfg0": "lorenz_small_cfg0"}
 UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -43,7 +43,7 @@ def wide_pipeline_bytes(csv_path):
     return int(total / steps)
 
 
-def main(prefix="r01"):
+def main(prefix="r02"):
     traffic = json.load(open(os.path.join(ROOT, "traffic.json")))
     pipes = json.load(open(os.path.join(ROOT, "pipes.json")))
     for cfg, cap in CAPTURES.items():
