@@ -166,28 +166,32 @@ def test_fhn_one_step_noise_law(dtype, flags):
     assert np.abs(c).max() < 5.5 / np.sqrt(n / 2)
 
 
-@pytest.mark.parametrize("N", [1024, 1000])  # block-uniform key kernel / per-thread key
-def test_lorenz_fast_one_substep_noise_law(N):
-    """Lorenz fp32 production kernel, one substep: (noisy - noise-free) /
-    (noise_scale * sqrt(dt)) is iid N(0, 1) per coordinate, uncorrelated
-    across coordinates and successive observation times."""
+@pytest.mark.parametrize("M,N,dtype", [(512, 1024, torch.float32),   # block-uniform key kernel
+                                       (512, 1000, torch.float32),   # per-thread key
+                                       (512, 1024, torch.float64),   # fp64 thread kernel
+                                       (16, 1000, torch.float64)])   # fp64 warp-per-particle
+def test_lorenz_one_substep_noise_law(M, N, dtype):
+    """Lorenz production kernels (fp32 fast, fp64 thread and small-bank warp
+    kernels), one substep: (noisy - noise-free) / (noise_scale * sqrt(dt)) is
+    iid N(0, 1) per coordinate, uncorrelated across coordinates, successive
+    observation times and neighbouring particles."""
     truth0, _, obs = orc.lorenz_truth(seed=8, n_obs=2)
-    M = 512
     MN = M * N
     base = dict(substeps=1, obs_var=2.0, observe="x1x3", prior_mean=tuple(truth0))
     gm = pf.Lorenz63Model(noise_scale=0.5, **base)
     g0 = pf.Lorenz63Model(noise_scale=0.0, **base)
     rng = np.random.default_rng(3)
     pt = np.asarray(truth0) + rng.normal(size=3)
-    x0 = torch.from_numpy(np.repeat(pt[:, None], MN, axis=1)).float().cuda().contiguous()
+    x0 = torch.from_numpy(np.repeat(pt[:, None], MN, axis=1)).to(dtype).cuda().contiguous()
+    code = _lib.PF_F32 if dtype == torch.float32 else _lib.PF_F64
     keys = torch.from_numpy(pf.philox.filter_keys(9, M).view(np.int32)).cuda()
     dy = torch.from_numpy(obs[0].copy()).cuda()
 
     def run(model, t):
         xo = torch.empty_like(x0)
-        lw = torch.empty(MN, dtype=torch.float32, device="cuda")
+        lw = torch.empty(MN, dtype=dtype, device="cuda")
         st = torch.zeros(M, dtype=torch.int32, device="cuda")
-        _lib.call("pf_lorenz_propagate_weight_ex", model.params(), _lib.PF_F32, _lib.ptr(x0),
+        _lib.call("pf_lorenz_propagate_weight_ex", model.params(), code, _lib.ptr(x0),
                   None, _lib.ptr(xo), _lib.ptr(dy), _lib.ptr(lw), M, N, _lib.ptr(keys), t, None,
                   _lib.ptr(st), 0, _lib.stream_ptr())
         torch.cuda.synchronize()
@@ -198,7 +202,7 @@ def test_lorenz_fast_one_substep_noise_law(N):
     z1 = (run(gm, 1) - det) / sig
     z2 = (run(gm, 2) - det) / sig
     # the fp32 state near |x| ~ 30 carries ~2e-6 absolute rounding: 1e-4 of sig
-    _z_checks(z1, "lorenz")
+    _z_checks(z1, f"lorenz {dtype}")
     n = z1.shape[0]
     for name, (a, b) in {"x1~x2": (z1[:, :1], z1[:, 1:2]), "x2~x3": (z1[:, 1:2], z1[:, 2:]),
                          "t vs t+1": (z1, z2),
