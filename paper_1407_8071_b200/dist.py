@@ -164,6 +164,8 @@ def native_comm():
         return None
     key = (world(), id(dist.group.WORLD))
     if key not in _NATIVE:
+        for stale in _NATIVE.values():  # a previous process group's communicator
+            stale.close()
         _NATIVE.clear()
         _NATIVE[key] = NativeComm()
     return _NATIVE[key]
