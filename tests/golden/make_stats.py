@@ -84,7 +84,7 @@ def _fhn_task(seed):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workers", type=int, default=os.cpu_count())
-    ap.add_argument("--lz-seeds", type=int, default=1024)
+    ap.add_argument("--lz-seeds", type=int, default=4096)
     ap.add_argument("--fhn-seeds", type=int, default=128)
     ap.add_argument("--reuse-fhn", action="store_true")
     args = ap.parse_args()

@@ -65,18 +65,20 @@ def test_cfg0_mse_vs_high_particle_proxy_matches_reference():
     production (Philox) mode, scored against a J = 2^17 posterior-mean proxy
     (bench.py:77-86 compute_reference) and compared seed-for-seed in
     distribution with the UNMODIFIED reference: 1024 reference seeds
-    (tests/golden/stats.npz, make_stats.py) vs 2048 GPU seeds, each one
-    run_ensemble(model, obs, 'bootstrap', 4, 1000, seed) (replicates batched
-    as one bank, replicates.ensemble_replicates).  Per-seed MSE has CV ~0.9,
-    so the rule is the two-sample 3-sigma one (the 5 % band is reported);
-    the variance and bias^2 terms of the decomposition are compared too."""
+    (tests/golden/stats.npz, make_stats.py: 4096 seeds) vs 4096 GPU seeds,
+    each one run_ensemble(model, obs, 'bootstrap', 4, 1000, seed) (replicates
+    batched as one bank, replicates.ensemble_replicates).  Per-seed MSE has
+    CV ~0.97, so at 4096 + 4096 seeds one standard error of the difference
+    is ~1.7 % of the MSE: the north star's 5 % band and the two-sample
+    3-sigma rule are both asserted; the variance and bias^2 terms of the
+    decomposition are compared too."""
     st = _stats()
     truth_seed, T, M, N = (int(v) for v in st["meta"][:4])
     proxy = st["lz_proxy"]
     truth0, _, obs = orc.lorenz_truth(seed=truth_seed, n_obs=T)
     gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
                           prior_mean=tuple(truth0), prior_var=1.0)
-    S = 2048
+    S = 4096
     batch = replicates.ensemble_replicates(gm, obs, "bootstrap", M, N,
                                               [100_000 + s for s in range(S)],
                                               dtype="float64")
@@ -90,6 +92,7 @@ def test_cfg0_mse_vs_high_particle_proxy_matches_reference():
           f"{mse_c.mean():.6f} ({mse_c.size} seeds) diff {100 * rel:+.2f}% "
           f"({d / se:+.2f} sigma); within 5%: {abs(rel) <= 0.05}")
     assert abs(d) <= 3.0 * se
+    assert abs(rel) <= 0.05
     # decomposition: variance term (per-seed spread about the seed mean) ...
     em_g = est.mean(axis=0)
     var_g = ((est - em_g) ** 2).mean(axis=(1, 2))

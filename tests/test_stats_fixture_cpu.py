@@ -20,7 +20,7 @@ def test_fixture_shapes_and_sizes():
     assert (T, M, N) == (500, 4, 1000)  # BASELINE cfg0
     assert pm * pn >= 100_000  # J >= 1e5 proxy
     assert ST["lz_proxy"].shape == (T, 3)
-    assert ST["lz_mse"].size >= 256 and ST["lz_var_s"].size == ST["lz_mse"].size
+    assert ST["lz_mse"].size >= 4096 and ST["lz_var_s"].size == ST["lz_mse"].size
     assert ST["fhn_mse"].size >= 64
 
 
