@@ -556,6 +556,9 @@ def run_ours(args, cfg):
         if comm is None:
             raise SystemExit("multi-GPU bench needs the native NCCL exchange (pf_comm)")
         bank.set_exchange(comm, M * est_dim)
+        sys.stderr.write(f"[bench] rank {rank}/{world} (GPU {local}): NCCL "
+                         f"{comm.nccl_version} communicator of {comm.size} ranks, filters "
+                         f"[{lo}, {hi}) of {M}\n")
 
     # warm-up, then K timed intervals in one native call (pf_bank_run)
     bank.run_native(0, args.warmup)
@@ -662,6 +665,7 @@ def run_ours(args, cfg):
     e2e_obs = obs[: args.steps]
     # release the timed bank so the caching allocator can serve the e2e call
     used_graph = graph is not None
+    comm_version = comm.nccl_version if comm is not None else None
     del graph, bank, est_full
     # one untimed call of the same shape (first-use costs: lazy module
     # loading of the e2e path, allocator growth), then the timed call
@@ -702,6 +706,9 @@ def run_ours(args, cfg):
                            else "state < L2; compute-bound kernel"},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
                 "cuda_graph": used_graph,
+                "nccl": {"ranks": world, "version": comm_version,
+                         "exchange": "native pf_comm all-reduce per observation"}
+                if world > 1 else None,
                 # per step: propagate + resample (+ the estimate pass unless the
                 # planar-state estimate is fused into the bank resampler)
                 "gpu_launches": (2 if cfg["kind"] == "lorenz" and N <= 8192 else 3) *
@@ -910,8 +917,8 @@ def launch_ranks(n):
     """`bench.py --gpus N` outside torchrun: re-exec this command under
     torch.distributed.run with N ranks (one per GPU, NCCL), after checking
     that N GPUs are visible - a box with fewer GPUs fails loudly instead of
-    silently measuring one rank.  NCCL_DEBUG=INFO (init subsystem) puts the
-    communicator lines, with their rank counts, on stderr."""
+    silently measuring one rank.  NCCL_DEBUG=INFO (init subsystem, written to
+    stderr) logs the communicator lines with their rank counts."""
     import torch
 
     have = torch.cuda.device_count()
@@ -923,6 +930,8 @@ def launch_ranks(n):
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    # NCCL logs to stdout by default; keep stdout for the JSON line
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
            os.path.abspath(__file__)] + sys.argv[1:]
