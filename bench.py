@@ -44,6 +44,13 @@ CONFIGS = {
                  desc="Lorenz-63, M=4096 x N=1024 (M*N=2^22), 40 Euler steps/obs, fp32"),
     "cfg2m256": dict(kind="lorenz", M=256, N=16384, dtype="float32",
                      desc="Lorenz-63, M=256 x N=16384 (M*N=2^22), 40 Euler steps/obs, fp32"),
+    # the rest of BASELINE cfg2's M sweep: 16 filters of 2^18 and the
+    # centralised filter of 2^22 particles (device-wide resampling; M=1 does
+    # not shard - replicas only)
+    "cfg2m16": dict(kind="lorenz", M=16, N=1 << 18, dtype="float32",
+                    desc="Lorenz-63, M=16 x N=2^18 (M*N=2^22), 40 Euler steps/obs, fp32"),
+    "cfg2m1": dict(kind="lorenz", M=1, N=1 << 22, dtype="float32",
+                   desc="Lorenz-63, centralised M=1 x N=2^22, 40 Euler steps/obs, fp32"),
     "cfg1b": dict(kind="resample", M=1 << 16, N=1 << 10, dtype="float32",
                   desc="resampling microbench: bank M=2^16 x N=2^10, fp32 logw ~ N(0, sigma^2), "
                        "logsumexp + multinomial + 3-float ancestor gather"),
@@ -894,7 +901,7 @@ def _ncu_pipes(config):
         return pipes[config]
     # the same kernel as a captured config at another bank size: its warp
     # instructions scale with the particle-steps per launch
-    src = {"cfg3": "cfg4", "cfg2m256": "cfg2"}.get(config)
+    src = {"cfg3": "cfg4", "cfg2m256": "cfg2", "cfg2m16": "cfg2", "cfg2m1": "cfg2"}.get(config)
     if src is None or src not in pipes:
         return None
     scaled = dict(pipes[src])

@@ -268,6 +268,15 @@ int pf_segmented_resample_ex(pf_dtype logw_dtype, const void *logw, int64_t M, i
 int pf_filter_estimate(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,
                        int32_t dim, const int32_t *anc, int64_t M, int64_t N, double *est_out,
                        void *stream);
+/* The same estimate for wide filters with dim <= 8 (e.g. the centralised
+ * M=1 x N=2^22 Lorenz filter): fixed chunks of 16384 particles summed by one
+ * CTA each, then the chunk partials in chunk order - bit-reproducible,
+ * independent of M and the GPU count.  ws: pf_estimate_workspace_bytes(M, N,
+ * dim) bytes (0 -> the one-CTA-per-filter kernel, ws unused). */
+size_t pf_estimate_workspace_bytes(int64_t M, int64_t N, int32_t dim);
+int pf_filter_estimate_ws(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,
+                          int32_t dim, const int32_t *anc, int64_t M, int64_t N, double *est_out,
+                          int64_t est_stride, void *ws, size_t ws_bytes, void *stream);
 
 /* pf_filter_estimate writing filter f's row at est_out + f*est_stride. */
 int pf_filter_estimate_strided(pf_dtype dtype, const void *x, int64_t stride_p, int64_t stride_d,

@@ -127,6 +127,9 @@ SIGNATURES = {
                                           c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_u32, c_vp,
                                           c_vp, c_u32, c_vp]),
     "pf_resample_workspace_bytes": (c_sz, [c_i64, c_i64]),
+    "pf_estimate_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
+    "pf_filter_estimate_ws": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_i32, c_vp, c_i64,
+                                             c_i64, c_vp, c_i64, c_vp, c_sz, c_vp]),
     "pf_segmented_resample": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_u32,
                                              c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pf_segmented_resample_ex": (ctypes.c_int, [ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_u32,

@@ -131,7 +131,10 @@ class FilterBank:
         self.status = torch.zeros(self.M, dtype=torch.int32, **kw)
         k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint32).reshape(self.M, 2))
         self.keys = torch.from_numpy(k.view(np.int32)).to(dev)
-        ws = _lib.load().pf_resample_workspace_bytes(self.M, self.N)
+        # one scratch for the resampler and, after it, the chunked estimate
+        # partials of wide filters (pf_filter_estimate_ws)
+        ws = max(_lib.load().pf_resample_workspace_bytes(self.M, self.N),
+                 _lib.load().pf_estimate_workspace_bytes(self.M, self.N, self.est_dim))
         self.ws_bytes = int(ws)
         self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, **kw)
         if est_buffer is None:
@@ -478,8 +481,9 @@ class FilterBank:
             self.post_resample(k, t)
         est_base = self.est[k].data_ptr() + self.est_row * self.est_width * 8
         sp, sd = self.est_strides
-        _lib.call("pf_filter_estimate_strided", self.code, _lib.ptr(xout), sp, sd, self.est_dim,
-                  _lib.ptr(self.anc), self.M, self.N, _lib.c_vp(est_base), self.est_width, s)
+        _lib.call("pf_filter_estimate_ws", self.code, _lib.ptr(xout), sp, sd, self.est_dim,
+                  _lib.ptr(self.anc), self.M, self.N, _lib.c_vp(est_base), self.est_width,
+                  _lib.ptr(self.ws), self.ws_bytes, s)
         if self.est_bits:
             _lib.call("pf_bits_estimate", _lib.ptr(self.q[1 - self.cur]), self.model.nodes,
                       self.est_bits, _lib.ptr(self.anc), self.M, self.N,

@@ -155,8 +155,10 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
     }
     const int64_t est_f = est_f0;
     if (!fused) {
-      rc = pf_filter_estimate_strided(d->dtype, xout, d->est_stride_p, d->est_stride_d,
-                                      d->est_dim, d->anc, d->M, d->N, est, est_f, stream);
+      // the resampler is done with the workspace: wide filters use it for
+      // their chunked estimate partials
+      rc = pf_filter_estimate_ws(d->dtype, xout, d->est_stride_p, d->est_stride_d, d->est_dim,
+                                 d->anc, d->M, d->N, est, est_f, d->ws, d->ws_bytes, stream);
       if (rc) return rc;
     }
     if (d->model == PF_MODEL_FHNNET && d->est_bits > 0) {

@@ -751,3 +751,35 @@ def test_wide_pipeline_variants_identical(M, N, sigma):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("N", [65536, 70001, 1 << 20])
+def test_chunked_wide_estimate(N):
+    """pf_filter_estimate_ws (wide filters, dim <= 8): the posterior mean of
+    the resampled set (core.py:154-156 via filters.py:188) within 1e-12 of an
+    fp64 reference sum, bit-identical for a filter whether it sits alone or in
+    a bank (the chunk order depends on N only)."""
+    rng = np.random.default_rng(N)
+    M, dim = 3, 3
+    x = torch.from_numpy(rng.standard_normal((dim, M * N)).astype(np.float32)).cuda()
+    anc = torch.from_numpy(np.sort(rng.integers(0, N, (M, N)), axis=1).astype(np.int32)
+                           + (np.arange(M) * N)[:, None].astype(np.int32)).reshape(-1).cuda()
+
+    def est(xs, an, m):
+        wsb = _lib.load().pf_estimate_workspace_bytes(m, N, dim)
+        assert wsb > 0
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        out = torch.empty((m, dim), dtype=torch.float64, device="cuda")
+        _lib.call("pf_filter_estimate_ws", _lib.PF_F32, _lib.ptr(xs), 1, m * N, dim, _lib.ptr(an),
+                  m, N, _lib.ptr(out), dim, _lib.ptr(ws), wsb, _lib.stream_ptr())
+        return out.cpu().numpy()
+
+    e = est(x, anc, M)
+    xh = x.cpu().numpy().astype(np.float64)
+    ah = anc.cpu().numpy().reshape(M, N)
+    want = np.stack([xh[:, ah[f]].mean(axis=1) for f in range(M)])
+    assert np.max(np.abs(e - want)) < 1e-12 * max(1.0, np.abs(want).max()) + 1e-15
+    # filter 1 alone (its own rows, ancestors re-based) gives the same bits
+    x1 = x[:, N:2 * N].contiguous()
+    a1 = (anc[N:2 * N] - N).contiguous()
+    assert np.array_equal(est(x1, a1, 1)[0], e[1])
