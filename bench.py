@@ -552,7 +552,7 @@ def run_ours(args, cfg):
     est_full = torch.zeros((T, M, est_dim), dtype=torch.float64, device=dev)
     bank = pf.FilterBank(model, hi - lo, N, keys[lo:hi], T, dtype=cfg["dtype"],
                          filter_offset=lo, estimate="projection", est_buffer=est_full,
-                         est_row_offset=lo)
+                         est_row_offset=lo, kernel_flags=args.kernel_flags)
     bank.load_observations(obs)
     bank.init()
     comm = None
@@ -624,7 +624,7 @@ def run_ours(args, cfg):
         pipes = _ncu_pipes(args.config)
         roof = _issue_roofline(pipes, kern_ms) or {"bound": "issue", "achieved": None,
                                                     "frac": None, "unit": "warp-inst/s"}
-        roof["kernel"] = "fhn_fast_kernel<30,50,6> (fp32, Philox)"
+        roof["kernel"] = "fhn_cm_kernel<30,50,6> (fp32, Philox; column-major strip slots)"
         roof["algorithmic"] = (f"{pipes['warp_inst_per_launch']:.4g} warp instructions per "
                                f"launch (ncu smsp__inst_executed.sum, same launch) / live "
                                f"kernel time" if pipes else "no committed ncu count")
@@ -792,7 +792,7 @@ def run_variant(args, cfg):
         # the noisy second-stage propagate is the production lattice kernel
         # (cfg4's capture): issue roofline, as run_ours
         roof = _issue_roofline(_ncu_pipes("cfg4"), kern_ms) or {"bound": "issue", "frac": None}
-        roof["kernel"] = "fhn_fast_kernel (second-stage propagate)"
+        roof["kernel"] = "fhn_cm_kernel (second-stage propagate)"
         roof["algorithmic"] = "cfg4's ncu warp-instruction count per launch / live kernel time"
         ach = M * N * n_sub * FHN_BYTES_PER_PS / (kern_ms / 1e3) / 1e9
         roof["streaming_model"] = {"achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -954,6 +954,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sigma", type=float, default=1.0, help="cfg1 log-weight std")
+    ap.add_argument("--kernel-flags", type=int, default=0,
+                    help="PF_KERNEL_* for the propagate kernels (comparison runs only)")
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no e2e / CPU baseline): for ncu captures")
     args = ap.parse_args()

@@ -206,6 +206,10 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
  * one, with the same Philox counters and draw layout - the comparison tests
  * pin the fast kernels against it. */
 #define PF_KERNEL_GENERIC 1u
+/* PF_KERNEL_ALT: the production kernel's alternative layout where one exists
+ * (FH-N lattice: the row-major shared plane instead of column-major strip
+ * slots) - bit-identical results, kept for comparison. */
+#define PF_KERNEL_ALT 2u
 int pf_lorenz_propagate_weight_ex(const pf_lorenz_params *p, pf_dtype dtype, const void *x_in,
                                   const int32_t *anc, void *x_out, const double *y,
                                   void *logw_out, int64_t M, int64_t N, const uint32_t *keys,

@@ -459,6 +459,200 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
   }
 }
 
+// ---- production kernel with column-major strip slots (fp32, Philox) --------
+// fhn_fast_kernel's decomposition, RNG and arithmetic, bit for bit, with the
+// shared v plane laid out so that every neighbour read is vectorised: each
+// (strip, column) owns an 8-float slot [R=6 rows | up halo | down halo] at
+// col * kCmPitch + seg * 8 (32-byte aligned; pitch 44 = 12 mod 32 makes the
+// quarter-warp 128-bit accesses conflict-free).  Per Euler step a thread
+// reads its left and right neighbours' strips with LDS.128 + LDS.64 each and
+// its vertical neighbours from its own halo (LDS.64), writes its new strip
+// with STS.128 + STS.64 and its boundary rows into the adjacent strips'
+// halos: 5 loads + 4 stores instead of 14 + 6.
+constexpr int kCmPitch = 44;
+
+template <int ROWS, int COLS, int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
+    const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
+    const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
+    int64_t MN, int32_t N, FhnFast c, const uint32_t *__restrict__ keys, uint32_t t,
+    uint32_t *__restrict__ status) {
+  static_assert(R == 6 && ROWS % R == 0, "6-row strips tiling the lattice");
+  constexpr int NSEG = ROWS / R;
+  static_assert(NSEG * 8 <= kCmPitch, "strip slots must fit the column pitch");
+  constexpr int P = COLS * kCmPitch;
+  constexpr int NODES = ROWS * COLS;
+  extern __shared__ __align__(16) float cms[];  // [2][P]
+  __shared__ double red;
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  const int seg = tid / COLS;
+  const int col = tid - seg * COLS;
+  const bool active = seg < NSEG;
+  const int row0 = seg * R;
+  const int own = col * kCmPitch + seg * 8;
+  const int lft = (col == 0 ? col : col - 1) * kCmPitch + seg * 8;  // ghost = self at the edges
+  const int rgt = (col == COLS - 1 ? col : col + 1) * kCmPitch + seg * 8;
+  const bool top = seg == 0, bottom = seg == NSEG - 1;
+  // halo targets: the down halo of the strip above / up halo of the strip
+  // below; the top / bottom strip writes into its column's pad instead
+  // (branch-free stores)
+  const int pad = col * kCmPitch + NSEG * 8;
+  const int h_above = top ? pad : own - 1;
+  const int h_below = bottom ? pad + 1 : own + 14;
+  const float s2v = -1.3862943611198906f * c.sig_v * c.sig_v;
+  const float s2w = -1.3862943611198906f * c.sig_w * c.sig_w;
+  const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
+
+  // a strip's new values into plane `pl`: its slot + the adjacent halos
+  auto put = [&](float *pl, const float *vv) {
+    *reinterpret_cast<float4 *>(pl + own) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    *reinterpret_cast<float2 *>(pl + own + 4) = make_float2(vv[4], vv[5]);
+    pl[h_above] = vv[0];
+    pl[h_below] = vv[5];
+  };
+
+  for (int64_t p = blockIdx.x; p < MN; p += gridDim.x) {
+    const int64_t f = p / N;
+    const uint32_t j = static_cast<uint32_t>(p - f * N);
+    const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
+    const float *xs = xin + src * 2 * static_cast<int64_t>(NODES);
+    if (tid == 0) bad = 0;
+    const Key2 key = load_key(keys, f);
+    float v[R], w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      v[r] = 0.f;
+      w[r] = 0.f;
+      if (active) {
+        const int node = (row0 + r) * COLS + col;
+        v[r] = __ldg(xs + node);
+        w[r] = __ldg(xs + NODES + node);
+      }
+    }
+    if (active) put(cms, v);
+    __syncthreads();
+
+    PhiloxPreT pre[R / 2];
+    const PhiloxUni uni = philox_uni_t(j, kPurposeFhn, key);
+    const PhiloxKeys rk = philox_round_keys(key);
+#pragma unroll
+    for (int q = 0; q < R / 2; ++q)
+      pre[q] = philox_pre_t(j, static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col), kPurposeFhn,
+                            key);
+    auto euler = [&](int k, auto par_c) {
+      constexpr int PAR = decltype(par_c)::value;
+      if (active) {
+        const float *cur = cms + PAR * P;
+        float *nxt = cms + (PAR ^ 1) * P;
+        const float4 l4 = *reinterpret_cast<const float4 *>(cur + lft);
+        const float2 l2 = *reinterpret_cast<const float2 *>(cur + lft + 4);
+        const float4 r4 = *reinterpret_cast<const float4 *>(cur + rgt);
+        const float2 r2 = *reinterpret_cast<const float2 *>(cur + rgt + 4);
+        const float2 hl = *reinterpret_cast<const float2 *>(cur + own + 6);
+        const float L[R] = {l4.x, l4.y, l4.z, l4.w, l2.x, l2.y};
+        const float Rt[R] = {r4.x, r4.y, r4.z, r4.w, r2.x, r2.y};
+        float up = top ? v[0] : hl.x;
+        const float dn_last = bottom ? v[R - 1] : hl.y;
+        const uint32_t c1k0 = (step0 + k) ^ key.k0;
+        float vn[R];
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q) {
+          float av, aw, tv[2], tw[2];
+          const uint4 rr = philox10_t(pre[q], uni, c1k0, rk);
+          box_muller_rad_trig(rr.x, rr.y, s2v, av, tv[0], tv[1]);
+          box_muller_rad_trig(rr.z, rr.w, s2w, aw, tw[0], tw[1]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 2 * q + h;
+            const float u = v[r];
+            const float dn = r < R - 1 ? v[r + 1] : dn_last;
+            const float nb = ((up + dn) + L[r]) + Rt[r];
+            float un = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
+            un = fmaf(-c.dt, w[r], un);
+            un = fmaf(c.dtc, nb, un);
+            un = fmaf(av, tv[h], un);
+            w[r] = fmaf(aw, tw[h], fmaf(c.wc, w[r], fmaf(c.uc, u, c.c0)));
+            vn[r] = un;
+            up = u;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = vn[r];
+        put(nxt, v);
+      }
+      __syncthreads();
+    };
+    int k = 0;
+    for (; k + 1 < c.n_sub; k += 2) {
+      euler(k, std::integral_constant<int, 0>{});
+      euler(k + 1, std::integral_constant<int, 1>{});
+    }
+    if (k < c.n_sub) euler(k, std::integral_constant<int, 0>{});
+
+    // epilogue: divergence flag, store, electrode log-likelihood
+    if (active) {
+      bool fin = true;
+      float *xd = xout + p * 2 * static_cast<int64_t>(NODES);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int node = (row0 + r) * COLS + col;
+        fin = fin && isfinite(v[r]) && isfinite(w[r]);
+        xd[node] = v[r];
+        xd[NODES + node] = w[r];
+      }
+      if (!fin) bad = 1;
+    }
+    if (tid < 32) {
+      const float *fv = cms + (c.n_sub & 1) * P;
+      double acc = 0.0;
+      for (int i = tid; i < c.n_obs; i += 32) {
+        const int n = __ldg(obs_idx + i);
+        const int rr = n / COLS, cc = n - rr * COLS;
+        const int sg = rr / R;
+        const double rsd =
+            __ldg(y + i) - static_cast<double>(fv[cc * kCmPitch + sg * 8 + (rr - sg * R)]);
+        acc = fma(rsd, rsd, acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+      if (tid == 0) red = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      logw[p] = static_cast<float>(c.obs_coef * red);
+      if (bad) atomicOr(status + f, PF_ST_DIVERGED);
+    }
+    __syncthreads();
+  }
+}
+
+template <int ROWS, int COLS, int MINB>
+static int launch_fhn_cm(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
+                         const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
+                         int32_t N, const uint32_t *keys, uint32_t t, uint32_t *status,
+                         cudaStream_t s) {
+  constexpr size_t smem = 2 * static_cast<size_t>(COLS) * kCmPitch * sizeof(float);
+  auto kern = fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB>;
+  static const int per_sm = [] {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB>,
+                                                  256, smem);
+    return n < 1 ? 1 : n;
+  }();
+  int sms = kSmCount, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(MN, static_cast<int64_t>(sms) * per_sm);
+  kern<<<static_cast<unsigned>(grid), 256, smem, s>>>(
+      static_cast<const float *>(x_in), anc, static_cast<float *>(x_out), y, obs_idx,
+      static_cast<float *>(logw), MN, N, fc, keys, t, status);
+  return check_launch("pf_fhn_interval(column-major)");
+}
+
 // accel.fhn_euler_block (general form, fp64, per-node drive), one thread per
 // node, reference order.
 __global__ void fhn_block_op_kernel(const double *__restrict__ U, const double *__restrict__ V,
@@ -570,7 +764,7 @@ static bool fhn_fast_supported(const pf_fhn_params *p) {
 static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *anc, void *x_out,
                            const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                            int32_t N, const uint32_t *keys, uint32_t t, const double *tape,
-                           uint32_t *status, cudaStream_t s) {
+                           uint32_t *status, cudaStream_t s, uint32_t flags) {
   FhnFast fc;
   fc.rows = c.rows;
   fc.cols = c.cols;
@@ -602,8 +796,11 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   if (c.sig_v == 0.0 && c.sig_w == 0.0)  // the auxiliary filter's point prediction
     return launch_fhn_fast_t<30, 50, false, 3, 1, true>(fc, x_in, anc, x_out, y, obs_idx, logw,
                                                         MN, N, keys, t, tape, status, s);
-  return launch_fhn_fast_t<30, 50, false, 2, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
-                                                keys, t, tape, status, s);
+  if (flags & PF_KERNEL_ALT)  // the row-major plane variant (same draws and arithmetic)
+    return launch_fhn_fast_t<30, 50, false, 2, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
+                                                  keys, t, tape, status, s);
+  return launch_fhn_cm<30, 50, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t, status,
+                                  s);
 }
 
 }  // namespace pf
@@ -639,7 +836,7 @@ int pf_fhn_interval_ex(const pf_fhn_params *p, pf_dtype dtype, const void *x_in,
   const cudaStream_t s = as_stream(stream);
   if (dtype == PF_F32 && fhn_fast_supported(p) && !(flags & PF_KERNEL_GENERIC))
     return launch_fhn_fast(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32, keys, t, z_tape,
-                           status, s);
+                           status, s, flags);
   if (dtype == PF_F64)
     return z_tape ? launch_fhn<double, 1>(c, x_in, anc, x_out, y, obs_idx, logw_out, MN, n32,
                                           keys, t, z_tape, status, s)

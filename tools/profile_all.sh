@@ -18,7 +18,7 @@ cap() {  # name regex config [skip]
   gzip -f $out/${R}_ncu_$1_sass.csv
   rm -f $out/$1.ncu-rep
 }
-cap fhn_fast_cfg4 fhn_fast_kernel cfg4
+cap fhn_cm_cfg4 fhn_cm_kernel cfg4
 cap lorenz_fast_cfg2 lorenz_fast_kernel cfg2
 cap resample_bank_cfg1b resample_bank_kernel cfg1b
 cap wide2_merge_cfg1c wide2_merge cfg1c

@@ -11,7 +11,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles")
-CAPTURES = {"cfg4": "fhn_fast_cfg4", "cfg2": "lorenz_fast_cfg2", "cfg1b": "resample_bank_cfg1b",
+CAPTURES = {"cfg4": "fhn_cm_cfg4", "cfg2": "lorenz_fast_cfg2", "cfg1b": "resample_bank_cfg1b",
             "net": "fhnnet_fast_net", "cfg1c": "wide2_merge_cfg1c", "cfg0": "lorenz_small_cfg0"}
 UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
