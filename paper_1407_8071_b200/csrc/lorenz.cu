@@ -219,15 +219,25 @@ __global__ void __launch_bounds__(256) lorenz_fast_kernel(
     }
   };
   if (nch > 0) {
-    uint4 cur[3], nxt[3];
-    draws(0, cur);
-    for (int k4 = 0; k4 + 1 < nch; ++k4) {  // full chunks: only the last can be partial
-      draws(k4 + 1, nxt);
-      chunk(cur, 4);
-#pragma unroll
-      for (int q = 0; q < 3; ++q) cur[q] = nxt[q];
+    // two draw buffers in ping-pong (the loop is unrolled by two chunks, so
+    // no register copies between chunks); only the last chunk can be partial
+    uint4 ra[3], rb[3];
+    draws(0, ra);
+    int k4 = 0;
+    for (; k4 + 2 < nch; k4 += 2) {
+      draws(k4 + 1, rb);
+      chunk(ra, 4);
+      draws(k4 + 2, ra);
+      chunk(rb, 4);
     }
-    chunk(cur, c.n_sub - 4 * (nch - 1));
+    const int last = c.n_sub - 4 * (nch - 1);
+    if (k4 + 1 < nch) {
+      draws(k4 + 1, rb);
+      chunk(ra, 4);
+      chunk(rb, last);
+    } else {
+      chunk(ra, last);
+    }
   }
   if (!live) return;
   if (!(isfinite(x1) && isfinite(x2) && isfinite(x3))) atomicOr(status + f, PF_ST_DIVERGED);
