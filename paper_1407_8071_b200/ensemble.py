@@ -53,19 +53,6 @@ class EnsembleOutput:
         )
 
 
-class _LazySeeds:
-    """The per-filter SeedSequences of an ensemble, spawned on first use
-    (spawning costs ~10 us per filter; banks have thousands)."""
-
-    def __init__(self, master_seed, n_filters):
-        self.master, self.n, self._seeds = master_seed, n_filters, None
-
-    def __getitem__(self, f):
-        if self._seeds is None:
-            self._seeds = philox.filter_seeds(self.master, self.n)
-        return self._seeds[f]
-
-
 class _EnsembleFilterOutput(FilterOutput):
     """FilterOutput whose ``seed`` (the filter's SeedSequence child,
     ensemble.py:96-99) is resolved lazily."""
@@ -73,7 +60,7 @@ class _EnsembleFilterOutput(FilterOutput):
     @property
     def seed(self):
         s = self.__dict__["_seed"]
-        if isinstance(s, tuple) and isinstance(s[0], _LazySeeds):
+        if isinstance(s, tuple) and isinstance(s[0], philox.FilterSeeds):
             s = s[0][s[1]]
             self.__dict__["_seed"] = s
         return s
@@ -155,7 +142,7 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     if not use_exch:
         rank, world = 0, 1
     lo, hi = dist.shard_range(n_filters, rank, world) if world > 1 else (0, n_filters)
-    keys = philox.filter_keys(master_seed, n_filters)
+    keys, seeds = philox.filter_keys_and_seeds(master_seed, n_filters)
     started = time.perf_counter()
     dev = torch.device("cuda", torch.cuda.current_device())
     est_dim = estimate_width(model, estimate)
@@ -227,7 +214,7 @@ def run_ensemble(model, observations, variant: str, n_filters: int, n_particles:
     est_h = est_full.cpu().numpy()
     lnc_h = lnc_full.cpu().numpy()
     coll_h = coll_full.cpu().numpy()
-    outputs = _FilterOutputs(variant, n_particles, _LazySeeds(master_seed, n_filters), est_h,
+    outputs = _FilterOutputs(variant, n_particles, seeds, est_h,
                              lnc_h, coll_h, secs)
     filter_seconds = np.full(n_filters, float(secs.sum()))
     return EnsembleOutput(variant, n_filters, n_particles, master_seed, outputs,

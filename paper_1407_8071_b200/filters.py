@@ -162,13 +162,20 @@ def run_filter(model: StateSpaceModel, observations, variant: str, n_particles: 
                       estimate=estimate, variant=variant)
     bank.load_observations(obs)
     bank.init()
-    events = [torch.cuda.Event(enable_timing=True) for _ in range(obs.shape[0] + 1)]
-    events[0].record()
-    for k in range(obs.shape[0]):
-        bank.step(k)
-        events[k + 1].record()
+    if bank._native_ok():
+        # the whole record in one native call (pf_bank_run), per-step device times
+        bank.run_native(0, obs.shape[0], time_steps=True)
+        secs = bank.last_step_ms.astype(np.float64) / 1e3
+    else:  # oracle mode (tape): the per-step hook loop
+        events = [torch.cuda.Event(enable_timing=True) for _ in range(obs.shape[0] + 1)]
+        events[0].record()
+        for k in range(obs.shape[0]):
+            bank.step(k)
+            events[k + 1].record()
+        secs = None
     torch.cuda.synchronize()
     bank.check_status()
+    if secs is None:
+        secs = _bank_seconds(events)
     return FilterOutput(variant, n_particles, seed, bank.est[:, 0, :].cpu().numpy(),
-                        bank.lnc_tr[:, 0].cpu().numpy(), _bank_seconds(events),
-                        bank.collapse_steps()[0])
+                        bank.lnc_tr[:, 0].cpu().numpy(), secs, bank.collapse_steps()[0])

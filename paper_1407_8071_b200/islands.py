@@ -42,7 +42,7 @@ class IslandBank:
             raise ValueError("at most 4096 islands")
         ss = philox.as_seed_sequence(seed)
         children = ss.spawn(n_islands + 1)
-        keys = np.stack([philox.seed_key(c) for c in children[:n_islands]]).astype(np.uint32)
+        keys = philox.seed_keys(children[:n_islands])
         self.M, self.N, self.period, self.T = n_islands, n_particles, island_period, n_steps
         self.tape = tape
         rank, world = dist.world()

@@ -66,7 +66,7 @@ def filter_replicates(model, observations, variant: str, n_particles: int, seeds
                       dtype=None, estimate: str = "full") -> ReplicateBatch:
     """R = len(seeds) independent ``run_filter(model, obs, variant, n, seed_r)``."""
     obs = _validate(observations, variant, model)
-    keys = np.stack([philox.seed_key(s) for s in seeds]).astype(np.uint32)
+    keys = philox.seed_keys(seeds)
     R, T = keys.shape[0], obs.shape[0]
     dim = estimate_width(model, estimate)
     est = np.empty((R, T, dim))

@@ -78,6 +78,50 @@ def test_seed_keys_follow_the_reference_seed_tree():
     assert np.array_equal(philox.seed_key(philox.filter_seeds(5, 1)[0]), ks[0])
 
 
+@pytest.mark.parametrize("entropy", [0, 1, 5, 7107, 2**32, 2**40 + 3, 12345678901234567890,
+                                     [3, 1, 4, 1, 5, 9, 2, 6]])
+def test_vectorised_seed_keys_equal_numpy_seed_sequence(entropy):
+    """philox.child_keys / seed_keys restate numpy's SeedSequence hashing;
+    they must equal generate_state(2) of the objects numpy builds."""
+    import copy
+
+    from paper_1407_8071_b200 import philox
+
+    root = np.random.SeedSequence(entropy)
+    parents = [root, root.spawn(2)[1], root.spawn(3)[2].spawn(5)[4],
+               np.random.SeedSequence(entropy, spawn_key=(2**33, 7))]
+    for par in parents:
+        for extra in (0, 3):
+            p2 = copy.deepcopy(par)
+            if extra:
+                p2.spawn(extra)
+            start = p2.n_children_spawned
+            want = np.stack([c.generate_state(2, np.uint32) for c in p2.spawn(41)])
+            assert np.array_equal(philox.child_keys(par, start, 41), want)
+    seeds = [root] + parents[1:] + np.random.SeedSequence(entropy).spawn(5) + [9, 2**70]
+    want = np.stack([philox.seed_key(s) for s in seeds])
+    assert np.array_equal(philox.seed_keys(seeds), want)
+
+
+def test_ensemble_seeds_advance_a_seed_sequence_master_like_the_reference():
+    """ensemble.py:56-60: the filters of run_ensemble(master=ss) are
+    ss.spawn(M), which advances ss; the filter outputs carry those children."""
+    from paper_1407_8071_b200 import philox
+
+    ss = np.random.SeedSequence(11)
+    ss.spawn(2)
+    keys, seeds = philox.filter_keys_and_seeds(ss, 4)
+    assert ss.n_children_spawned == 6
+    ref = np.random.SeedSequence(11).spawn(6)[2:]
+    for f in range(4):
+        assert seeds[f].spawn_key == ref[f].spawn_key
+        assert np.array_equal(keys[f], ref[f].generate_state(2, np.uint32))
+    # an int master is not advanced (there is no object) and starts at child 0
+    k5, s5 = philox.filter_keys_and_seeds(5, 3)
+    assert s5[2].spawn_key == (2,)
+    assert np.array_equal(k5, philox.filter_keys(5, 3))
+
+
 def test_product_fails_loudly_without_cuda():
     import torch
 
