@@ -406,6 +406,20 @@ def cpu_resample_baseline(cfg, sigma, budget_s=10.0):
                       f"(numpy + C merge)"}
 
 
+def _wide_launches(N, flags):
+    """Kernels of one wide (N > 8192) production resample (launch_resample):
+    tile stats + filter totals (gamma + 3 chunk kernels when N > 2^21, else
+    one) + tile CDF + partition + merge; the merge-path / separate-gather
+    variants add the gather pass, the recomputing variant drops the tile CDF."""
+    chunked = (N + 2047) // 2048 > 1024
+    n = 8 if chunked else 5
+    if flags & (2 | 4):
+        n += 1
+    if flags & 8:
+        n -= 1
+    return n
+
+
 def run_resample(args, cfg):
     import torch
 
@@ -438,7 +452,8 @@ def run_resample(args, cfg):
     def step(k):
         _lib.call("pf_segmented_resample_ex", _lib.PF_F32, _lib.ptr(logw), Ml, N, None,
                   _lib.ptr(keys), k + 1, _lib.ptr(anc), _lib.ptr(lnc), _lib.ptr(coll),
-                  _lib.ptr(st), _lib.ptr(ws), wsb, _lib.ptr(x_in), _lib.ptr(x_out), 3, 0, s)
+                  _lib.ptr(st), _lib.ptr(ws), wsb, _lib.ptr(x_in), _lib.ptr(x_out), 3,
+                  args.kernel_flags, s)  # cfg1: --kernel-flags are PF_RS_* flags
 
     for k in range(args.warmup):
         step(k)
@@ -521,7 +536,8 @@ def run_resample(args, cfg):
                         "api": f"pf_segmented_resample_ex on pinned host log-weights -> host "
                                f"ancestors, {chunks} filter chunk(s) pipelined over H2D / "
                                f"compute / D2H streams"},
-                "gpu_launches": (1 if N <= 8192 else 10) * args.steps,
+                "gpu_launches": (1 if N <= 8192 else _wide_launches(N, args.kernel_flags))
+                * args.steps,
                 "clocks": clocks.summary()}
         print(json.dumps(line))
     return 0

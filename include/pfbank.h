@@ -210,6 +210,11 @@ int pf_lorenz_propagate_weight(const pf_lorenz_params *p, pf_dtype dtype, const 
  * (FH-N lattice: the row-major shared plane instead of column-major strip
  * slots) - bit-identical results, kept for comparison. */
 #define PF_KERNEL_ALT 2u
+/* PF_KERNEL_PACKED: the production kernel issued on packed fp32 pairs
+ * (sm_100a FFMA2/FADD2/FMUL2: 10 % fewer instructions for the FH-N lattice)
+ * - bit-identical results; measured slower (FFMA2 occupies the FMA-heavy
+ * pipe the Philox IMAD.WIDE needs), kept for comparison. */
+#define PF_KERNEL_PACKED 4u
 int pf_lorenz_propagate_weight_ex(const pf_lorenz_params *p, pf_dtype dtype, const void *x_in,
                                   const int32_t *anc, void *x_out, const double *y,
                                   void *logw_out, int64_t M, int64_t N, const uint32_t *keys,

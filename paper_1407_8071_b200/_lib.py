@@ -30,6 +30,7 @@ PF_RS_WIDE_GATHER_SEPARATE = 4
 PF_RS_WIDE_RECOMPUTE = 8
 PF_KERNEL_GENERIC = 1
 PF_KERNEL_ALT = 2
+PF_KERNEL_PACKED = 4
 PF_F32 = 0
 PF_F64 = 1
 

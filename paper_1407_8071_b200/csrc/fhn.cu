@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include <type_traits>
 #include "philox.cuh"
+#include "f32x2.cuh"
 
 namespace pf {
 
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
 // halos: 5 loads + 4 stores instead of 14 + 6.
 constexpr int kCmPitch = 44;
 
-template <int ROWS, int COLS, int R, int MINB>
+template <int ROWS, int COLS, int R, int MINB, bool X2>
 __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
     const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
@@ -540,8 +541,92 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
     for (int q = 0; q < R / 2; ++q)
       pre[q] = philox_pre_t(j, static_cast<uint32_t>(((row0 >> 1) + q) * COLS + col), kPurposeFhn,
                             key);
+    // X2: the same per-lane arithmetic on packed row pairs (2q, 2q+1) -
+    // FFMA2/FADD2/FMUL2, bit-identical to the scalar form, ~25 fewer issue
+    // slots per thread-step (PF_KERNEL_PACKED; not faster, see the launcher).  The vertical sums up+dn stay scalar FADDs whose
+    // results land directly in pair registers (no register moves).
+    f2_t vp[R / 2], wp[R / 2];
+    if constexpr (X2) {
+#pragma unroll
+      for (int q = 0; q < R / 2; ++q) {
+        vp[q] = f2_pack(v[2 * q], v[2 * q + 1]);
+        wp[q] = f2_pack(w[2 * q], w[2 * q + 1]);
+      }
+    }
+    const f2_t s2vw = f2_pack(s2v, s2w);
     auto euler = [&](int k, auto par_c) {
       constexpr int PAR = decltype(par_c)::value;
+      if constexpr (X2) {
+        if (active) {
+          const float *cur = cms + PAR * P;
+          float *nxt = cms + (PAR ^ 1) * P;
+          const ulonglong2 l4 = *reinterpret_cast<const ulonglong2 *>(cur + lft);
+          const f2_t l2 = *reinterpret_cast<const f2_t *>(cur + lft + 4);
+          const ulonglong2 r4 = *reinterpret_cast<const ulonglong2 *>(cur + rgt);
+          const f2_t r2 = *reinterpret_cast<const f2_t *>(cur + rgt + 4);
+          const float2 hl = *reinterpret_cast<const float2 *>(cur + own + 6);
+          const f2_t L2[R / 2] = {l4.x, l4.y, l2};
+          const f2_t R2[R / 2] = {r4.x, r4.y, r2};
+          float vs[R];
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) {
+            vs[2 * q] = f2_lo(vp[q]);
+            vs[2 * q + 1] = f2_hi(vp[q]);
+          }
+          const float up0 = top ? vs[0] : hl.x;
+          const float dn5 = bottom ? vs[R - 1] : hl.y;
+          // up + dn of every row (row r: v[r-1] + v[r+1]), packed per pair
+          f2_t S[R / 2];
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) {
+            const float u0 = q == 0 ? up0 : vs[2 * q - 1];
+            const float d1 = q == R / 2 - 1 ? dn5 : vs[2 * q + 2];
+            S[q] = f2_pack(u0 + vs[2 * q + 1], vs[2 * q] + d1);
+          }
+          const uint32_t c1k0 = (step0 + k) ^ key.k0;
+          f2_t vn[R / 2];
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) {
+            const uint4 rr = philox10_t(pre[q], uni, c1k0, rk);
+            // box_muller_rad_trig on the v words (x, y) and the w words (z, w)
+            const f2_t uu = f2_fma(f2_pack(static_cast<float>(rr.x), static_cast<float>(rr.z)),
+                                   f2_bcast(2.3283064365386963e-10f),
+                                   f2_bcast(1.1641532182693481e-10f));
+            const f2_t lg = f2_mul(f2_pack(lg2_approx(f2_lo(uu)), lg2_approx(f2_hi(uu))), s2vw);
+            const float av = sqrt_approx(f2_lo(lg)), aw = sqrt_approx(f2_hi(lg));
+            const f2_t xx = f2_pack(__uint_as_float((rr.y & 0x007fffffu) | 0x40000000u),
+                                    __uint_as_float((rr.w & 0x007fffffu) | 0x40000000u));
+            const f2_t ang =
+                f2_fma(xx, f2_bcast(3.14159265358979f), f2_bcast(-9.42477796076938f));
+            const f2_t tv = f2_pack(cos_approx(f2_lo(ang)), sin_approx(f2_lo(ang)));
+            const f2_t tw = f2_pack(cos_approx(f2_hi(ang)), sin_approx(f2_hi(ang)));
+            const f2_t u = vp[q];
+            const f2_t nb = f2_add(f2_add(S[q], L2[q]), R2[q]);
+            f2_t un = f2_fma(f2_fma(f2_fma(f2_bcast(c.a3), u, f2_bcast(c.a2)), u, f2_bcast(c.a1)),
+                             u, f2_bcast(c.a0));
+            un = f2_fma(f2_bcast(-c.dt), wp[q], un);
+            un = f2_fma(f2_bcast(c.dtc), nb, un);
+            un = f2_fma(f2_bcast(av), tv, un);
+            wp[q] = f2_fma(f2_bcast(aw), tw,
+                           f2_fma(f2_bcast(c.wc), wp[q], f2_fma(f2_bcast(c.uc), u, f2_bcast(c.c0))));
+            vn[q] = un;
+          }
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q) vp[q] = vn[q];
+          // three 8-byte stores: a 16-byte store would pin vp[0], vp[1] to
+          // one register quad and cost register moves every step
+#pragma unroll
+          for (int q = 0; q < R / 2; ++q)
+            asm volatile("st.volatile.shared.b64 [%0], %1;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(nxt + own + 2 * q))),
+                         "l"(vp[q])
+                         : "memory");
+          nxt[h_above] = f2_lo(vp[0]);
+          nxt[h_below] = f2_hi(vp[R / 2 - 1]);
+        }
+        __syncthreads();
+        return;
+      }
       if (active) {
         const float *cur = cms + PAR * P;
         float *nxt = cms + (PAR ^ 1) * P;
@@ -589,6 +674,15 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
       euler(k + 1, std::integral_constant<int, 1>{});
     }
     if (k < c.n_sub) euler(k, std::integral_constant<int, 0>{});
+    if constexpr (X2) {
+#pragma unroll
+      for (int q = 0; q < R / 2; ++q) {
+        v[2 * q] = f2_lo(vp[q]);
+        v[2 * q + 1] = f2_hi(vp[q]);
+        w[2 * q] = f2_lo(wp[q]);
+        w[2 * q + 1] = f2_hi(wp[q]);
+      }
+    }
 
     // epilogue: divergence flag, store, electrode log-likelihood
     if (active) {
@@ -627,19 +721,19 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
   }
 }
 
-template <int ROWS, int COLS, int MINB>
+template <int ROWS, int COLS, int MINB, bool X2>
 static int launch_fhn_cm(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
                          const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                          int32_t N, const uint32_t *keys, uint32_t t, uint32_t *status,
                          cudaStream_t s) {
   constexpr size_t smem = 2 * static_cast<size_t>(COLS) * kCmPitch * sizeof(float);
-  auto kern = fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB>;
+  auto kern = fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2>;
   static const int per_sm = [] {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB>,
+      cudaFuncSetAttribute(fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2>,
                                                   256, smem);
     return n < 1 ? 1 : n;
   }();
@@ -799,8 +893,16 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   if (flags & PF_KERNEL_ALT)  // the row-major plane variant (same draws and arithmetic)
     return launch_fhn_fast_t<30, 50, false, 2, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                   keys, t, tape, status, s);
-  return launch_fhn_cm<30, 50, 2>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t, status,
-                                  s);
+  // PF_KERNEL_PACKED: the same arithmetic on FFMA2/FADD2/FMUL2 pairs
+  // (bit-identical, 25.3e9 instead of 28.2e9 warp instructions per cfg4
+  // launch, but 40.5 vs 40.3 ms: a packed op holds both FMA pipes, so the
+  // Philox IMAD.WIDE on the heavy pipe waits more - math-pipe throttle 6.6 ->
+  // 12.5 % of stalls, profiles/r02_exp_fhn_ffma2.txt)
+  if (flags & PF_KERNEL_PACKED)
+    return launch_fhn_cm<30, 50, 2, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t,
+                                          status, s);
+  return launch_fhn_cm<30, 50, 2, false>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t,
+                                         status, s);
 }
 
 }  // namespace pf

@@ -211,12 +211,14 @@ def test_lorenz_one_substep_noise_law(M, N, dtype):
         assert np.abs(c).max() < 5.0 / np.sqrt(a.shape[0]), (name, c)
 
 
+@pytest.mark.parametrize("flags", [_lib.PF_KERNEL_ALT, _lib.PF_KERNEL_PACKED])
 @pytest.mark.parametrize("n_sub,t", [(50, 1), (3, 9), (1, 2)])
-def test_fhn_column_major_kernel_bit_identical_to_row_major(n_sub, t):
+def test_fhn_column_major_kernel_bit_identical_to_row_major(n_sub, t, flags):
     """The production lattice kernel's column-major strip slots
     (fhn_cm_kernel) and the row-major plane (fhn_fast_kernel, PF_KERNEL_ALT)
     run the same draws and arithmetic: bit-identical states, log weights and
-    flags."""
+    flags.  So does the same kernel issued on packed fp32 pairs
+    (PF_KERNEL_PACKED: FFMA2/FADD2/FMUL2) instead of scalar instructions."""
     m3, _, obs = orc.fhn_truth(seed=3, n_obs=1)
     gm = pf.FhnLatticeModel(stim_row=m3.stim_row, stim_col=m3.stim_col)
     M, N = 3, 80
@@ -224,6 +226,6 @@ def test_fhn_column_major_kernel_bit_identical_to_row_major(n_sub, t):
     anc = torch.from_numpy(np.sort(np.random.default_rng(4).integers(0, M * N, M * N))
                            .astype(np.int32)).cuda()
     a = fhn_interval(gm, x0, anc, obs[0], M, N, t, n_sub=n_sub)
-    b = fhn_interval(gm, x0, anc, obs[0], M, N, t, n_sub=n_sub, flags=_lib.PF_KERNEL_ALT)
+    b = fhn_interval(gm, x0, anc, obs[0], M, N, t, n_sub=n_sub, flags=flags)
     for u, v in zip(a, b):
         assert np.array_equal(u, v)

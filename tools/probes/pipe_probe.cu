@@ -210,6 +210,88 @@ __global__ void k_fadd_reg(float *out, float a, float b) {
   if (s == 1.2345f) out[0] = s;
 }
 
+
+// packed fp32 pairs (sm_100a FFMA2 / FADD2 / FMUL2): 2 lane-ops per issue
+__global__ void k_ffma2_reg(float *out, float a, float b) {
+  unsigned long long x[kChains];
+  for (int c = 0; c < kChains; ++c) {
+    const float f = threadIdx.x + c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(x[c]) : "f"(f));
+  }
+  unsigned long long aa, bb;
+  const float fa = a + threadIdx.x * 1e-9f;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(fa));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(b));
+  for (int i = 0; i < kIters; ++i) {
+    CHAINS(asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[c]) : "l"(aa), "l"(bb)));
+  }
+  float s = 0;
+  for (int c = 0; c < kChains; ++c) s += __uint_as_float(static_cast<uint32_t>(x[c]));
+  if (s == 1.2345f) out[0] = s;
+}
+
+// FFMA2 with a scalar (broadcast) multiplier from the constant bank
+__global__ void k_ffma2_bcast(float *out, float a, float b) {
+  unsigned long long x[kChains];
+  for (int c = 0; c < kChains; ++c) {
+    const float f = threadIdx.x + c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(x[c]) : "f"(f));
+  }
+  unsigned long long aa, bb;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(b));
+  for (int i = 0; i < kIters; ++i) {
+    CHAINS(asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[c]) : "l"(aa), "l"(bb)));
+  }
+  float s = 0;
+  for (int c = 0; c < kChains; ++c) s += __uint_as_float(static_cast<uint32_t>(x[c]));
+  if (s == 1.2345f) out[0] = s;
+}
+
+__global__ void k_fadd2_reg(float *out, float a, float b) {
+  unsigned long long x[kChains];
+  for (int c = 0; c < kChains; ++c) {
+    const float f = threadIdx.x + c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(x[c]) : "f"(f));
+  }
+  unsigned long long aa;
+  const float fa = a + threadIdx.x * 1e-9f;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(fa));
+  for (int i = 0; i < kIters; ++i) {
+    CHAINS(asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(x[c]) : "l"(aa)));
+  }
+  float s = 0;
+  for (int c = 0; c < kChains; ++c) s += __uint_as_float(static_cast<uint32_t>(x[c]));
+  if (s == 1.2345f) out[0] = s;
+}
+
+// FFMA2 interleaved 1:1 with IMAD.WIDE (both fma-pipe families)
+__global__ void k_mix_ffma2_imadw(float *out, float a, float b) {
+  unsigned long long x[kChains / 2];
+  uint32_t y[kChains / 2];
+  unsigned long long aa, bb;
+  const float fa = a + threadIdx.x * 1e-9f;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(fa));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bb) : "f"(b));
+  for (int c = 0; c < kChains / 2; ++c) {
+    const float f = threadIdx.x + c;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(x[c]) : "f"(f));
+    y[c] = threadIdx.x * 3 + c;
+  }
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains / 2; ++c) {
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[c]) : "l"(aa), "l"(bb));
+      uint64_t p;
+      asm volatile("mul.wide.u32 %0, %1, 3528531795;" : "=l"(p) : "r"(y[c]));
+      y[c] = static_cast<uint32_t>(p >> 32) + static_cast<uint32_t>(p);
+    }
+  }
+  float s = 0;
+  for (int c = 0; c < kChains / 2; ++c) s += __uint_as_float(static_cast<uint32_t>(x[c])) + y[c];
+  if (s == 1.2345f) out[0] = s;
+}
+
 template <typename K, typename A>
 void run(const char *name, K kern, A a, A b, float *out, int sms, double clk_ghz) {
   const int blocks = sms * 8, threads = 256;
@@ -240,6 +322,10 @@ int main() {
   run("ffma_reg", k_ffma_reg, 1.0000001f, 1e-7f, out, sms, ghz);
   run("ffma_imm", k_ffma_imm, 1.0000001f, 1e-7f, out, sms, ghz);
   run("ffma_cbank", k_ffma_cbank, 1.0000001f, 1e-7f, out, sms, ghz);
+  run("ffma2_reg", k_ffma2_reg, 1.0000001f, 1e-7f, out, sms, ghz);
+  run("ffma2_bcast", k_ffma2_bcast, 1.0000001f, 1e-7f, out, sms, ghz);
+  run("fadd2_reg", k_fadd2_reg, 1e-7f, 1e-7f, out, sms, ghz);
+  run("mix_ffma2_imadw", k_mix_ffma2_imadw, 1.0000001f, 1e-7f, out, sms, ghz);
   run("fmul_reg", k_fmul_reg, 1.0000001f, 1e-7f, out, sms, ghz);
   run("fadd_reg", k_fadd_reg, 1e-7f, 1e-7f, out, sms, ghz);
   run("imad_wide_imm", k_imad_wide, 3u, 5u, out, sms, ghz);
