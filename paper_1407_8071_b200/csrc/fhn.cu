@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
 // halos: 5 loads + 4 stores instead of 14 + 6.
 constexpr int kCmPitch = 44;
 
-template <int ROWS, int COLS, int R, int MINB, bool X2>
+template <int ROWS, int COLS, int R, int MINB, bool X2, bool PIPE = true>
 __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
     const float *__restrict__ xin, const int32_t *__restrict__ anc, float *__restrict__ xout,
     const double *__restrict__ y, const int32_t *__restrict__ obs_idx, float *__restrict__ logw,
@@ -554,6 +554,19 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
       }
     }
     const f2_t s2vw = f2_pack(s2v, s2w);
+    // PIPE: every Euler step's Philox words are generated one step ahead,
+    // in the same basic block as the previous step's MUFU Box-Muller and FMA
+    // stencil, so that ptxas interleaves the FMA-heavy (IMAD.WIDE) and XU
+    // streams instead of running all Philox rounds, then all MUFU, between
+    // two barriers (cfg4 40.1 -> 39.0 ms; issue-active 60.5 -> 64.4 %).  The
+    // last step's lookahead is discarded (a guard would split the block:
+    // 41.8 ms).  Carrying the Box-Muller factors one step ahead as well
+    // (18 floats instead of 12 words) measured 42.3 ms.
+    uint4 rpipe[R / 2];
+    if constexpr (PIPE) {
+#pragma unroll
+      for (int q = 0; q < R / 2; ++q) rpipe[q] = philox10_t(pre[q], uni, step0 ^ key.k0, rk);
+    }
     auto euler = [&](int k, auto par_c) {
       constexpr int PAR = decltype(par_c)::value;
       if constexpr (X2) {
@@ -587,7 +600,13 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
           f2_t vn[R / 2];
 #pragma unroll
           for (int q = 0; q < R / 2; ++q) {
-            const uint4 rr = philox10_t(pre[q], uni, c1k0, rk);
+            uint4 rr;
+            if constexpr (PIPE) {
+              rr = rpipe[q];
+              rpipe[q] = philox10_t(pre[q], uni, (step0 + k + 1) ^ key.k0, rk);
+            } else {
+              rr = philox10_t(pre[q], uni, c1k0, rk);
+            }
             // box_muller_rad_trig on the v words (x, y) and the w words (z, w)
             const f2_t uu = f2_fma(f2_pack(static_cast<float>(rr.x), static_cast<float>(rr.z)),
                                    f2_bcast(2.3283064365386963e-10f),
@@ -644,7 +663,13 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
 #pragma unroll
         for (int q = 0; q < R / 2; ++q) {
           float av, aw, tv[2], tw[2];
-          const uint4 rr = philox10_t(pre[q], uni, c1k0, rk);
+          uint4 rr;
+          if constexpr (PIPE) {
+            rr = rpipe[q];  // generated during the previous step
+            rpipe[q] = philox10_t(pre[q], uni, (step0 + k + 1) ^ key.k0, rk);
+          } else {
+            rr = philox10_t(pre[q], uni, c1k0, rk);
+          }
           box_muller_rad_trig(rr.x, rr.y, s2v, av, tv[0], tv[1]);
           box_muller_rad_trig(rr.z, rr.w, s2w, aw, tw[0], tw[1]);
 #pragma unroll
@@ -721,19 +746,19 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
   }
 }
 
-template <int ROWS, int COLS, int MINB, bool X2>
+template <int ROWS, int COLS, int MINB, bool X2, bool PIPE = true>
 static int launch_fhn_cm(const FhnFast &fc, const void *x_in, const int32_t *anc, void *x_out,
                          const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                          int32_t N, const uint32_t *keys, uint32_t t, uint32_t *status,
                          cudaStream_t s) {
   constexpr size_t smem = 2 * static_cast<size_t>(COLS) * kCmPitch * sizeof(float);
-  auto kern = fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2>;
+  auto kern = fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2, PIPE>;
   static const int per_sm = [] {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2>,
+      cudaFuncSetAttribute(fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2, PIPE>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2, PIPE>,
                                                   256, smem);
     return n < 1 ? 1 : n;
   }();
@@ -894,10 +919,10 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
     return launch_fhn_fast_t<30, 50, false, 2, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                   keys, t, tape, status, s);
   // PF_KERNEL_PACKED: the same arithmetic on FFMA2/FADD2/FMUL2 pairs
-  // (bit-identical, 25.3e9 instead of 28.2e9 warp instructions per cfg4
-  // launch, but 40.5 vs 40.3 ms: a packed op holds both FMA pipes, so the
-  // Philox IMAD.WIDE on the heavy pipe waits more - math-pipe throttle 6.6 ->
-  // 12.5 % of stalls, profiles/r02_exp_fhn_ffma2.txt)
+  // (bit-identical, ~10 % fewer warp instructions per cfg4 launch, but 39.4
+  // vs 39.0 ms: a packed op holds both FMA pipes, so the Philox IMAD.WIDE
+  // on the heavy pipe waits more; without the Philox lookahead 40.5 vs 40.3
+  // ms, math-pipe throttle 6.6 -> 12.5 % of stalls, profiles/r02_exp_fhn_ffma2.txt)
   if (flags & PF_KERNEL_PACKED)
     return launch_fhn_cm<30, 50, 2, true>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N, keys, t,
                                           status, s);
