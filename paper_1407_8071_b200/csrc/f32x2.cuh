@@ -18,13 +18,13 @@ __device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
 }
 __device__ __forceinline__ f2_t f2_bcast(float s) { return f2_pack(s, s); }
 __device__ __forceinline__ float f2_lo(f2_t a) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  float lo;
+  asm("{\n .reg .f32 h;\n mov.b64 {%0, h}, %1;\n}" : "=f"(lo) : "l"(a));
   return lo;
 }
 __device__ __forceinline__ float f2_hi(f2_t a) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  float hi;
+  asm("{\n .reg .f32 l;\n mov.b64 {l, %0}, %1;\n}" : "=f"(hi) : "l"(a));
   return hi;
 }
 // a * b + c per lane, one rounding
