@@ -776,17 +776,17 @@ def run_variant(args, cfg):
         raise SystemExit(f"{args.config}: single-GPU workload")
     M, N, variant = cfg["M"], cfg["N"], cfg["variant"]
     dbf = variant == "double-bf"
-    # double bootstrap: the timed K steps run as one CUDA graph captured from
-    # the step sequence, and a second (eager) pass of K steps times the
-    # propagate kernel - its per-step Python launches would otherwise set the
-    # pace (the GPU work per step is ~0.6 ms)
+    # double bootstrap: the timed K intervals as one prebuilt CUDA graph of the
+    # native island sequence (~16 short launches per interval), and K more
+    # intervals with events around each propagate for the kernel time
     T = args.warmup + (2 if dbf else 1) * args.steps
     model, obs = _make_model_and_obs(cfg, T)
     n_sub = getattr(model, "substeps", 1)
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-    if variant == "double-bf":
+    if dbf:  # the island step inside the native driver, as run_double_bootstrap
         runner = islands.IslandBank(model, M, N, cfg["period"], 7, T, dtype=cfg["dtype"])
         runner.start(obs)
+        runner.attach_native()
         bank, step = runner.bank, runner.step
     else:
         bank = pf.FilterBank(model, M, N, philox.filter_keys(7, M), T, dtype=cfg["dtype"],
@@ -794,7 +794,8 @@ def run_variant(args, cfg):
         bank.load_observations(obs)
         bank.init()
         step = bank.step
-    native = variant == "auxiliary"  # the whole apf_step sequence in pf_bank_run
+    # the whole apf_step / island sequence in pf_bank_run
+    native = variant == "auxiliary" or dbf
     if native:
         bank.run_native(0, args.warmup)
         bank.prepare_timing(args.steps)
@@ -807,20 +808,13 @@ def run_variant(args, cfg):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     kern_list = []
-    graph = None
-    if dbf:
-        bank.kernel_events = None
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):  # captures; executes nothing
-            for i in range(args.steps):
-                step(args.warmup + i)
-        torch.cuda.synchronize()
+    graph = bank.capture(args.warmup, args.steps) if dbf else None
     with ClockSampler(local) as clocks:
         start.record()
-        if native:
+        if graph is not None:
+            graph.launch()
+        elif native:
             kern_list = bank.run_native(args.warmup, args.steps, time_propagate=True)
-        elif graph is not None:
-            graph.replay()
         else:
             for i in range(args.steps):
                 bank.kernel_events = evs[i]  # events around this step's propagate launch
@@ -828,11 +822,9 @@ def run_variant(args, cfg):
         end.record()
         torch.cuda.synchronize()
     elapsed = start.elapsed_time(end) / 1e3
-    if graph is not None:  # kernel time: a second, eager pass with events
-        for i in range(args.steps):
-            bank.kernel_events = evs[i]
-            step(args.warmup + args.steps + i)
-        torch.cuda.synchronize()
+    if graph is not None:
+        bank.run_native(args.warmup + args.steps, args.steps, slot=0)
+        kern_list = bank.pool_propagate_ms(args.steps)
         del graph
     bank.check_status()
     ps_total = M * N * n_sub * args.steps
@@ -906,7 +898,7 @@ def run_variant(args, cfg):
             "gpu_launches": args.steps * 9 if variant == "auxiliary" else
             args.steps * 11 + 2 * ((args.warmup + args.steps) // cfg["period"]
                                    - args.warmup // cfg["period"]),
-            "cuda_graph": dbf,
+            "native_driver": native, "cuda_graph": dbf,
             "clocks": clocks.summary()}
     print(json.dumps(line))
     return 0

@@ -415,6 +415,32 @@ int pf_comm_join(pf_comm *c, void *stream);
 #define PF_MODEL_FHNNET 2
 #define PF_MODEL_HMM 3
 #define PF_MODEL_LGM 4
+/* Double bootstrap (filters.py:201-313) in the native driver, single process:
+ * the bank's M filters are the islands.  After each interval's resample the
+ * island log weights gain lnc - lnc_before (pf_island_accumulate); every
+ * `period` intervals (t % period == 0) the islands are resampled by them
+ * (one segment of M, island Philox key, time word t) and island m takes island
+ * idx[m]'s ancestors, lnc and collapse flag (pf_island_copy) - before the
+ * interval's estimate; after it, the pooled estimate row and the logmeanexp
+ * trace entry (pf_island_pool / pf_island_trace). */
+typedef struct pf_island_desc {
+  int32_t period;
+  const uint32_t *key; /* (2) island-level Philox key */
+  double *lw;          /* (M) accumulated island log weights */
+  double *lnc_old;     /* (M) scratch */
+  int32_t *idx;        /* (M) scratch: selected islands */
+  int32_t *anc_tmp;    /* (M*N) scratch */
+  double *lnc_tmp;     /* (M) scratch */
+  uint8_t *coll_tmp;   /* (M) scratch */
+  double *s_lnc;       /* (1) island-resample outputs */
+  uint8_t *s_coll;
+  uint32_t *s_status;
+  void *ws; /* pf_resample_workspace_bytes(1, M) bytes */
+  size_t ws_bytes;
+  double *pool;  /* (T, est_dim): pooled estimate of observation k at pool + k*est_dim */
+  double *trace; /* (T) */
+} pf_island_desc;
+
 typedef struct pf_bank_desc {
   int32_t model; /* PF_MODEL_* */
   pf_dtype dtype;
@@ -472,6 +498,8 @@ typedef struct pf_bank_desc {
   /* nonzero: pf_bank_run captures its n_steps >= 2 intervals into one CUDA
    * graph and launches it (launch-bound small banks; ignored with comm) */
   int32_t use_graph;
+  /* non-NULL: double bootstrap islands (variant 0, single process, no comm) */
+  const pf_island_desc *islands;
 } pf_bank_desc;
 int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
                 int32_t have_ancestors, void *stream);

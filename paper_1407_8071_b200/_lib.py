@@ -70,6 +70,13 @@ class LgmParams(ctypes.Structure):
                 ("prior_mean", c_vp), ("chol_p0", c_vp), ("obs_logconst", c_f64)]
 
 
+class IslandDesc(ctypes.Structure):
+    _fields_ = [("period", c_i32), ("key", c_vp), ("lw", c_vp), ("lnc_old", c_vp), ("idx", c_vp),
+                ("anc_tmp", c_vp), ("lnc_tmp", c_vp), ("coll_tmp", c_vp), ("s_lnc", c_vp),
+                ("s_coll", c_vp), ("s_status", c_vp), ("ws", c_vp), ("ws_bytes", c_sz),
+                ("pool", c_vp), ("trace", c_vp)]
+
+
 class BankDesc(ctypes.Structure):
     _fields_ = [("model", c_i32), ("dtype", ctypes.c_int), ("M", c_i64), ("N", c_i64),
                 ("lorenz", ctypes.POINTER(LorenzParams)), ("fhn", ctypes.POINTER(FhnParams)),
@@ -86,7 +93,8 @@ class BankDesc(ctypes.Structure):
                 ("variant", c_i32), ("params0", c_vp), ("lam", c_vp), ("anc1", c_vp),
                 ("anc_comp", c_vp), ("x_tmp", c_vp), ("q_tmp", c_vp), ("lnc_before", c_vp),
                 ("coll1", c_vp), ("kernel_flags", c_u32), ("comm", c_vp),
-                ("exch_count", c_i64), ("use_graph", c_i32)]
+                ("exch_count", c_i64), ("use_graph", c_i32),
+                ("islands", ctypes.POINTER(IslandDesc))]
 
 
 PF_MODEL_LORENZ = 0

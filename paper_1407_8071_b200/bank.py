@@ -152,6 +152,9 @@ class FilterBank:
         # optional callable(k, t) run after resampling, before the estimate
         # (double bootstrap island selection, islands.py)
         self.post_resample = None
+        # optional _lib.IslandDesc: the double bootstrap's island step inside
+        # the native driver (islands.IslandBank.run)
+        self.island_desc = None
         self._desc = None  # cached pf_bank_desc (buffers are fixed for the bank's lifetime)
         # oracle mode builds the CDF in the reference's exact order (bit-exact
         # ancestors); production mode uses the parallel scan
@@ -307,6 +310,8 @@ class FilterBank:
         d.collapsed_trace = self.coll_tr.data_ptr()
         d.kernel_flags = self.kernel_flags
         d.use_graph = 1 if self.use_graph else 0
+        if self.island_desc is not None:
+            d.islands = ctypes.pointer(self.island_desc)
         comm = getattr(self, "comm", None)
         if comm is not None:
             if self.est.shape[1] * self.est_width != self.exch_count or self.est_row < 0:

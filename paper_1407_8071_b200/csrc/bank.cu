@@ -70,6 +70,13 @@ int bank_validate(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cu
   PF_REQUIRE(d->x[0] && d->x[1] && d->logw && d->anc && d->lnc && d->collapsed && d->status &&
                  d->keys && d->obs && d->est,
              "pf_bank_run: null buffer");
+  PF_REQUIRE(!d->islands ||
+                 (d->variant == 0 && !d->comm && d->islands->period >= 1 && d->islands->key &&
+                  d->islands->lw && d->islands->lnc_old && d->islands->idx &&
+                  d->islands->anc_tmp && d->islands->lnc_tmp && d->islands->coll_tmp &&
+                  d->islands->s_lnc && d->islands->s_coll && d->islands->s_status &&
+                  d->islands->pool && d->islands->trace),
+             "pf_bank_run: islands need variant 0, no comm and every island buffer");
   PF_REQUIRE(d->variant != 1 || (d->params0 && d->lam && d->anc1 && d->anc_comp && d->x_tmp &&
                                  d->lnc_before && d->coll1 &&
                                  (d->model != PF_MODEL_FHNNET || d->q_tmp)),
@@ -123,6 +130,10 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
       if (rc) return rc;
       src_anc = d->anc_comp;
     }
+    const pf_island_desc *isl = d->islands;
+    if (isl && cudaMemcpyAsync(isl->lnc_old, d->lnc, d->M * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return check_launch("pf_bank_run(island lnc)");
     if (ev) cudaEventRecordWithFlags(ev[4 * i + 1], s, rec_flags);
     rc = bank_propagate(d, bank_params(d), xin, qin, src_anc, xout, qout, y, d->logw, t, stream);
     if (!rc && apf)  // second stage weights log w - lambda[anc1] (filters.py:143)
@@ -139,7 +150,8 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
         d->collapsed_trace ? d->collapsed_trace + static_cast<int64_t>(k) * d->M : nullptr;
     // (the auxiliary filter finishes lnc / collapse after the resample: its
     // trace rows are copied afterwards)
-    if (planar && d->est_stride_p == 1 && d->est_stride_d == MN)
+    // (islands: the estimate follows the island copy, so it is not fused)
+    if (planar && d->est_stride_p == 1 && d->est_stride_d == MN && !isl)
       rc = segmented_resample_fused(d->dtype, d->logw, d->M, d->N, d->keys, t, d->anc, d->lnc,
                                     d->collapsed, d->status, d->ws, d->ws_bytes, xout,
                                     d->est_dim, est, est_f0, apf ? nullptr : lnc_row,
@@ -151,6 +163,18 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
     if (rc) return rc;
     if (apf) {  // a second-stage collapse restores the pre-step lnc (filters.py:146-148)
       rc = pf_apf_finish(d->lnc, d->lnc_before, d->collapsed, d->coll1, d->M, stream);
+      if (rc) return rc;
+    }
+    if (isl) {  // double bootstrap: island weights, and the island step (filters.py:245-265)
+      rc = pf_island_accumulate(isl->lw, d->lnc, isl->lnc_old, d->M, stream);
+      if (!rc && t % static_cast<uint32_t>(isl->period) == 0) {
+        rc = pf_segmented_resample_ex(PF_F64, isl->lw, 1, d->M, nullptr, isl->key, t, isl->idx,
+                                      isl->s_lnc, isl->s_coll, isl->s_status, isl->ws,
+                                      isl->ws_bytes, nullptr, nullptr, 0, 0u, stream);
+        if (!rc)
+          rc = pf_island_copy(isl->idx, d->anc, d->lnc, d->collapsed, isl->lw, d->M, d->N,
+                              isl->anc_tmp, isl->lnc_tmp, isl->coll_tmp, stream);
+      }
       if (rc) return rc;
     }
     const int64_t est_f = est_f0;
@@ -172,6 +196,12 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
     if (d->comm && d->exch_count > 0) {
       rc = comm_allreduce_after(d->comm, d->est + static_cast<int64_t>(k) * d->est_step_stride,
                                 d->exch_count, s);
+      if (rc) return rc;
+    }
+    if (isl) {  // pooled estimate and logmeanexp trace of observation k
+      rc = pf_island_pool(est, est_f, d->M, d->est_dim, isl->lw,
+                          isl->pool + static_cast<int64_t>(k) * d->est_dim, stream);
+      if (!rc) rc = pf_island_trace(d->lnc, d->M, isl->trace + k, stream);
       if (rc) return rc;
     }
     const bool traced = fused && !apf;  // rows already written by the resampler

@@ -224,10 +224,41 @@ class IslandBank:
             dist.allreduce_disjoint(st)
         _lib.raise_status(st.cpu().numpy())
 
+    def native_ok(self) -> bool:
+        """The whole run can be one native call: single process, Philox
+        draws (tape mode keeps the Python steps and their island tapes)."""
+        return not self.sharded and self.tape is None
+
+    def attach_native(self):
+        """Hand the island step to the native bank driver (pf_island_desc):
+        per interval, island weights, the island resampling every period,
+        the pooled estimate and the trace - no Python between intervals."""
+        b = self.bank
+        d = _lib.IslandDesc()
+        d.period = self.period
+        d.key, d.lw, d.lnc_old = (self.island_key.data_ptr(), self.lw.data_ptr(),
+                                  self.lnc_old.data_ptr())
+        d.idx, d.anc_tmp = self.idx.data_ptr(), self.anc_tmp.data_ptr()
+        d.lnc_tmp, d.coll_tmp = self.lnc_tmp.data_ptr(), self.coll_tmp.data_ptr()
+        d.s_lnc, d.s_coll, d.s_status = (self.s_lnc.data_ptr(), self.s_coll.data_ptr(),
+                                         self.s_status.data_ptr())
+        d.ws, d.ws_bytes = self.ws.data_ptr(), self.ws_bytes
+        d.pool, d.trace = self.est.data_ptr(), self.trace.data_ptr()
+        b.island_desc = d
+        b.post_resample = None
+        b._desc = None
+
     def run(self, observations):
         import torch
 
         self.start(observations)
+        if self.native_ok():
+            self.attach_native()
+            self.bank.run_native(0, self.T, time_steps=True)
+            steps = range(self.period, self.T + 1, self.period)
+            self.island_steps.extend(steps)
+            self.check_status()
+            return self.bank.last_step_ms.astype(np.float64) / 1e3
         events = [torch.cuda.Event(enable_timing=True) for _ in range(self.T + 1)]
         events[0].record()
         for k in range(self.T):
