@@ -163,7 +163,8 @@ def test_ctypes_struct_layouts_match_c(tmp_path):
         pytest.skip("gcc not available")
     structs = {"pf_lorenz_params": _lib.LorenzParams, "pf_fhn_params": _lib.FhnParams,
                "pf_fhnnet_params": _lib.FhnNetParams, "pf_hmm_params": _lib.HmmParams,
-               "pf_lgm_params": _lib.LgmParams, "pf_bank_desc": _lib.BankDesc}
+               "pf_lgm_params": _lib.LgmParams, "pf_bank_desc": _lib.BankDesc,
+               "pf_island_desc": _lib.IslandDesc}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pfbank.h"',
              "int main(void) {"]
     for cname, cls in structs.items():
