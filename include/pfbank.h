@@ -495,8 +495,10 @@ typedef struct pf_bank_desc {
    * block) over comm; NULL / 0 = single process */
   pf_comm *comm;
   int64_t exch_count;
-  /* nonzero: pf_bank_run captures its n_steps >= 2 intervals into one CUDA
-   * graph and launches it (launch-bound small banks; ignored with comm) */
+  /* nonzero: pf_bank_run captures its intervals into one CUDA graph and
+   * launches it when n_steps >= 32 (1: the default threshold) or >= use_graph
+   * (> 1) - launch-bound small banks; shorter runs enqueue directly, since the
+   * capture and instantiation cost ~0.5 ms; ignored with comm */
   int32_t use_graph;
   /* non-NULL: double bootstrap islands (variant 0, single process, no comm) */
   const pf_island_desc *islands;

@@ -85,6 +85,10 @@ class FilterBank:
         # (pf_bank_desc.use_graph); graph=None picks it for banks of up to
         # 2^20 particles, whose intervals are tens of microseconds
         self.use_graph = bool(graph) if graph is not None else self.MN <= (1 << 20)
+        # graph=True: every run_native call of >= 2 intervals is one graph;
+        # graph=None: runs of >= 32 intervals (shorter ones enqueue directly -
+        # capture + instantiation cost ~0.5 ms)
+        self.graph_min_steps = 2 if graph else 0
         self.T = int(n_steps)
         self.dtype = _torch_dtype(dtype)
         self.code = _lib.dtype_code(self.dtype)
@@ -309,7 +313,7 @@ class FilterBank:
         d.lnc_trace = self.lnc_tr.data_ptr()
         d.collapsed_trace = self.coll_tr.data_ptr()
         d.kernel_flags = self.kernel_flags
-        d.use_graph = 1 if self.use_graph else 0
+        d.use_graph = (self.graph_min_steps or 1) if self.use_graph else 0
         if self.island_desc is not None:
             d.islands = ctypes.pointer(self.island_desc)
         comm = getattr(self, "comm", None)

@@ -224,6 +224,7 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
 
 // An instantiated CUDA graph of n_steps intervals (launch-bound banks: one
 // graph launch replaces ~4 launches per observation and their host costs).
+constexpr int32_t kGraphMinSteps = 32;
 struct pf_bank_graph {
   cudaGraphExec_t exec = nullptr;
   int32_t n_steps = 0;
@@ -331,7 +332,10 @@ int pf_bank_run(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur,
     ev = evs.e.data();
   }
   int rc;
-  if (d->use_graph && n_steps >= 2 && !d->comm) {
+  // a graph pays its capture + instantiation (~0.5 ms) back only over a run
+  // of intervals; short calls enqueue directly (measured: cfg0 shape)
+  const int32_t min_graph = d->use_graph > 1 ? d->use_graph : kGraphMinSteps;
+  if (d->use_graph && n_steps >= min_graph && !d->comm) {
     pf_bank_graph *g = nullptr;
     rc = graph_capture(d, k0, n_steps, cur, have_ancestors, s, ev, &g);
     if (rc != PF_OK) return rc;

@@ -74,7 +74,8 @@ def test_capture_then_launch_equals_run_native():
         outs.append(_state(bank))
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
-    # run_ensemble on a small bank goes through the graph path and matches
-    # the explicit stream-launched bank
+    # run_ensemble on a small bank (graph chosen automatically; this short run
+    # enqueues directly, longer ones go through a graph) matches the explicit
+    # stream-launched bank
     out = pf.run_ensemble(model, obs, "bootstrap", M, N, 9)
     assert np.array_equal(np.stack([o.estimates for o in out.filter_outputs], axis=1), outs[0][0])
