@@ -437,8 +437,10 @@ typedef struct pf_island_desc {
   uint32_t *s_status;
   void *ws; /* pf_resample_workspace_bytes(1, M) bytes */
   size_t ws_bytes;
-  double *pool;  /* (T, est_dim): pooled estimate of observation k at pool + k*est_dim */
-  double *trace; /* (T) */
+  double *pool;     /* (T, pool_dim): pooled estimate of observation k at pool + k*pool_dim */
+  double *trace;    /* (T) */
+  int32_t pool_dim; /* estimate columns pooled per island row (<= the row stride; the
+                       FH-N network's rows carry the history-bit means after the state) */
 } pf_island_desc;
 
 typedef struct pf_bank_desc {

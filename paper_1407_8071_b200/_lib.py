@@ -74,7 +74,7 @@ class IslandDesc(ctypes.Structure):
     _fields_ = [("period", c_i32), ("key", c_vp), ("lw", c_vp), ("lnc_old", c_vp), ("idx", c_vp),
                 ("anc_tmp", c_vp), ("lnc_tmp", c_vp), ("coll_tmp", c_vp), ("s_lnc", c_vp),
                 ("s_coll", c_vp), ("s_status", c_vp), ("ws", c_vp), ("ws_bytes", c_sz),
-                ("pool", c_vp), ("trace", c_vp)]
+                ("pool", c_vp), ("trace", c_vp), ("pool_dim", c_i32)]
 
 
 class BankDesc(ctypes.Structure):

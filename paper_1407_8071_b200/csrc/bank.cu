@@ -75,7 +75,9 @@ int bank_validate(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cu
                   d->islands->lw && d->islands->lnc_old && d->islands->idx &&
                   d->islands->anc_tmp && d->islands->lnc_tmp && d->islands->coll_tmp &&
                   d->islands->s_lnc && d->islands->s_coll && d->islands->s_status &&
-                  d->islands->pool && d->islands->trace),
+                  d->islands->pool && d->islands->trace && d->islands->pool_dim >= 1 &&
+                  (d->est_stride_f == 0 ? d->islands->pool_dim <= d->est_dim
+                                        : d->islands->pool_dim <= d->est_stride_f)),
              "pf_bank_run: islands need variant 0, no comm and every island buffer");
   PF_REQUIRE(d->variant != 1 || (d->params0 && d->lam && d->anc1 && d->anc_comp && d->x_tmp &&
                                  d->lnc_before && d->coll1 &&
@@ -199,8 +201,8 @@ int bank_enqueue(const pf_bank_desc *d, int32_t k0, int32_t n_steps, int32_t cur
       if (rc) return rc;
     }
     if (isl) {  // pooled estimate and logmeanexp trace of observation k
-      rc = pf_island_pool(est, est_f, d->M, d->est_dim, isl->lw,
-                          isl->pool + static_cast<int64_t>(k) * d->est_dim, stream);
+      rc = pf_island_pool(est, est_f, d->M, isl->pool_dim, isl->lw,
+                          isl->pool + static_cast<int64_t>(k) * isl->pool_dim, stream);
       if (!rc) rc = pf_island_trace(d->lnc, d->M, isl->trace + k, stream);
       if (rc) return rc;
     }

@@ -244,6 +244,7 @@ class IslandBank:
                                          self.s_status.data_ptr())
         d.ws, d.ws_bytes = self.ws.data_ptr(), self.ws_bytes
         d.pool, d.trace = self.est.data_ptr(), self.trace.data_ptr()
+        d.pool_dim = self.est.shape[1]  # model.dim_x, as step() pools
         b.island_desc = d
         b.post_resample = None
         b._desc = None

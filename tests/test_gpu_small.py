@@ -197,7 +197,7 @@ def test_hook_level_double_bootstrap_matches_reference(golden):
     assert abs(system.island_probs().sum() - 1.0) < 1e-12
 
 
-@pytest.mark.parametrize("kind", ["hmm", "lorenz"])
+@pytest.mark.parametrize("kind", ["hmm", "lorenz", "lorenz64", "fhnnet"])
 def test_double_bootstrap_native_driver_matches_python_steps(kind):
     """The island step inside the native bank driver (pf_island_desc: island
     weights, island resampling every period, pooled estimate and trace, one
@@ -206,8 +206,13 @@ def test_double_bootstrap_native_driver_matches_python_steps(kind):
     traces, island log weights and collapse record."""
     from paper_1407_8071_b200 import islands
 
+    dtype = "float32" if kind == "lorenz" else None
     if kind == "hmm":
         gm, obs, M, N, period = models.DiscreteHmm(**HMM), np.tile(HOBS, (4, 1)), 8, 64, 2
+    elif kind == "fhnnet":  # rows carry the history-bit means after the state means
+        gm = pf.FhnNetworkModel(J=8, n_zones=2, zone_width=2, stim_prob=0.05)
+        obs = pf.simulate.simulate(gm, 12, 4)[1]
+        M, N, period = 5, 128, 3
     else:
         from paper_1407_8071_b200.simulate import lorenz_truth
 
@@ -218,8 +223,7 @@ def test_double_bootstrap_native_driver_matches_python_steps(kind):
     T = obs.shape[0]
     runs = []
     for native in (True, False):
-        ib = islands.IslandBank(gm, M, N, period, 17, T, dtype="float32" if kind == "lorenz"
-                                else None)
+        ib = islands.IslandBank(gm, M, N, period, 17, T, dtype=dtype)
         if native:
             ib.run(obs)
         else:
