@@ -238,3 +238,31 @@ def test_double_bootstrap_native_driver_matches_python_steps(kind):
             assert a == b
         else:
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("M,period", [(1, 1), (4, 1), (4, 50), (3, 4)])
+def test_double_bootstrap_native_island_edge_cases(M, period):
+    """Native island step at the edges: one island, resampling every step,
+    never (period beyond the horizon), and a period that does not divide T:
+    identical to the Python step driver."""
+    from paper_1407_8071_b200 import islands
+
+    gm, obs = models.DiscreteHmm(**HMM), np.tile(HOBS, (3, 1))
+    T = obs.shape[0]
+    runs = []
+    for native in (True, False):
+        ib = islands.IslandBank(gm, M, 32, period, 23, T)
+        if native:
+            ib.run(obs)
+        else:
+            ib.start(obs)
+            for k in range(T):
+                ib.step(k)
+            torch.cuda.synchronize()
+        runs.append((ib.est.cpu().numpy(), ib.trace.cpu().numpy(), ib.lw.cpu().numpy(),
+                     ib.collapse_steps(), list(ib.island_steps)))
+    for a, b in zip(*runs):
+        if isinstance(a, list):
+            assert a == b
+        else:
+            assert np.array_equal(a, b)
