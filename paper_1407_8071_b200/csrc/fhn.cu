@@ -907,11 +907,14 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   if (tape)
     return launch_fhn_fast_t<30, 50, true, 3, 1>(fc, x_in, anc, x_out, y, obs_idx, logw, MN, N,
                                                  keys, t, tape, status, s);
-  // one particle per CTA, 2 CTAs/SM (102 registers: the Philox key schedule
-  // and the hoisted rounds stay in registers): cfg4 41.8 ms/interval vs 43.1
-  // at 3 CTAs/SM (78 registers, round keys rematerialised every step), 42.2
-  // at 4 CTAs/SM and 42.8 for two particles per CTA at 2 CTAs/SM.  The
-  // noise-free lookahead variant has no draws and keeps 3 CTAs/SM.
+  // one particle per CTA, 2 CTAs/SM: the Philox key schedule, the hoisted
+  // rounds and the next step's Philox words stay in registers (119).  cfg4:
+  // 39.0 ms/interval for the column-major kernel with the Philox lookahead
+  // (DESIGN §3); at 3 CTAs/SM ptxas rematerialises the round keys every step
+  // (80 registers, 44.6 ms; 43.1 vs 41.8 ms for the row-major kernel before
+  // the lookahead), 4 CTAs/SM and two particles per CTA measured slower too.
+  // The noise-free lookahead variant has no draws and runs at 4 CTAs/SM
+  // (56 registers; its column-major form measured 15.4 vs 14.1 ms).
   if (c.sig_v == 0.0 && c.sig_w == 0.0)  // the auxiliary filter's point prediction
     return launch_fhn_fast_t<30, 50, false, 3, 1, true>(fc, x_in, anc, x_out, y, obs_idx, logw,
                                                         MN, N, keys, t, tape, status, s);
