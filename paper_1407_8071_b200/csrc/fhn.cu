@@ -913,8 +913,8 @@ static int launch_fhn_fast(const FhnConsts &c, const void *x_in, const int32_t *
   // (DESIGN §3); at 3 CTAs/SM ptxas rematerialises the round keys every step
   // (80 registers, 44.6 ms; 43.1 vs 41.8 ms for the row-major kernel before
   // the lookahead), 4 CTAs/SM and two particles per CTA measured slower too.
-  // The noise-free lookahead variant has no draws and runs at 4 CTAs/SM
-  // (56 registers; its column-major form measured 15.4 vs 14.1 ms).
+  // The noise-free lookahead variant has no draws (56 registers; its
+  // column-major form measured 15.4 vs 14.1 ms).
   if (c.sig_v == 0.0 && c.sig_w == 0.0)  // the auxiliary filter's point prediction
     return launch_fhn_fast_t<30, 50, false, 3, 1, true>(fc, x_in, anc, x_out, y, obs_idx, logw,
                                                         MN, N, keys, t, tape, status, s);
