@@ -59,6 +59,11 @@ CONFIGS = {
                        "N(0, sigma^2), logsumexp + multinomial + 3-float ancestor gather"),
     "cfg0": dict(kind="lorenz", M=4, N=1000, dtype="float64",
                  desc="Lorenz-63, M=4 x N=1000, 40 Euler steps/obs, fp64"),
+    # one rank's share of cfg4 at 8 GPUs (8 of the 64 filters), on one GPU:
+    # the measured input of the scaling model; not a BASELINE line
+    "cfg4shard8": dict(kind="fhn", M=8, N=4096, dtype="float32",
+                       desc="FH-N 30x50 lattice, M=8 x N=4096 (one rank's share of cfg4 at 8 "
+                            "GPUs), 50 Euler steps/obs, fp32"),
     # the paper's own lattice (models/fhn.py:85-207): not a
     # BASELINE config; same metric, one Euler step per observation
     # SURVEY §8f rows on the same metric: the auxiliary filter (two-stage
@@ -947,7 +952,8 @@ def _ncu_pipes(config):
         return pipes[config]
     # the same kernel as a captured config at another bank size: its warp
     # instructions scale with the particle-steps per launch
-    src = {"cfg3": "cfg4", "cfg2m256": "cfg2", "cfg2m16": "cfg2", "cfg2m1": "cfg2"}.get(config)
+    src = {"cfg3": "cfg4", "cfg4shard8": "cfg4", "cfg2m256": "cfg2", "cfg2m16": "cfg2",
+           "cfg2m1": "cfg2"}.get(config)
     if src is None or src not in pipes:
         return None
     scaled = dict(pipes[src])
