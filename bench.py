@@ -64,6 +64,9 @@ CONFIGS = {
     "cfg4shard8": dict(kind="fhn", M=8, N=4096, dtype="float32",
                        desc="FH-N 30x50 lattice, M=8 x N=4096 (one rank's share of cfg4 at 8 "
                             "GPUs), 50 Euler steps/obs, fp32"),
+    "cfg2shard8": dict(kind="lorenz", M=512, N=1024, dtype="float32",
+                       desc="Lorenz-63, M=512 x N=1024 (one rank's share of cfg2 M=4096 at 8 "
+                            "GPUs), 40 Euler steps/obs, fp32"),
     # the paper's own lattice (models/fhn.py:85-207): not a
     # BASELINE config; same metric, one Euler step per observation
     # SURVEY §8f rows on the same metric: the auxiliary filter (two-stage
@@ -953,7 +956,7 @@ def _ncu_pipes(config):
     # the same kernel as a captured config at another bank size: its warp
     # instructions scale with the particle-steps per launch
     src = {"cfg3": "cfg4", "cfg4shard8": "cfg4", "cfg2m256": "cfg2", "cfg2m16": "cfg2",
-           "cfg2m1": "cfg2"}.get(config)
+           "cfg2m1": "cfg2", "cfg2shard8": "cfg2"}.get(config)
     if src is None or src not in pipes:
         return None
     scaled = dict(pipes[src])
