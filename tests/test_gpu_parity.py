@@ -587,9 +587,10 @@ def test_production_wide_chunked_filter_totals():
 
 
 def test_small_bank_warp_kernel_bit_identical():
-    """fp64 production banks below 2^15 particles run one warp per particle
-    (RNG in parallel, lane 0 runs the substep chain); the result is
-    bit-identical to the thread-per-particle kernel (PF_KERNEL_GENERIC)."""
+    """fp64 production banks below 2^15 particles run one warp per two
+    particles (RNG in parallel over the lanes, lanes 0-1 run the two substep
+    chains); the result is bit-identical to the thread-per-particle kernel
+    (PF_KERNEL_GENERIC)."""
     truth0, _, obs = orc.lorenz_truth(seed=8, n_obs=6)
     gm = pf.Lorenz63Model(substeps=40, obs_var=2.0, noise_scale=0.5, observe="x1x3",
                           prior_mean=tuple(truth0), prior_var=1.0)
