@@ -253,6 +253,8 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
   // 1. load + max (NaN detection: np.max propagates NaN, core.py:132)
   double lw[IPT];
   float lf[IPT];
+  double u[IPT];
+  double erun64 = 0.0;  // fp64 / tape path: the thread's spacing run (production)
   double mx = -INFINITY;
   int nan = 0;
   // VEC: whole runs in range and 16-byte aligned -> vector loads/stores
@@ -298,6 +300,22 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
       lw[q] = i < N ? static_cast<double>(__ldg(logw + base + i)) : -INFINITY;
     }
   }
+  // production draws: this thread's exponential spacings are independent of
+  // the weights - generated here, while the log-weight loads are in flight
+  if constexpr (MODE == 0) {
+    const Key2 key = load_key(keys, f);
+#pragma unroll
+    for (int q = 0; q < IPT; q += 4) {
+      uint32_t wd[4];
+      spacing_words<IPT>(key, t, i0 + q, wd);
+#pragma unroll
+      for (int h = 0; h < 4 && q + h < IPT; ++h) {
+        const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
+        erun64 = __dadd_rn(erun64, e);
+        u[q + h] = erun64;
+      }
+    }
+  }
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
     if (i0 + q >= N) lw[q] = -INFINITY;
@@ -335,7 +353,6 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
   // 3. w = e / total (IEEE division, core.py:136; production fp32 inputs:
   // reciprocal multiply), CDF = offset + local run
   double total, run = 0.0;
-  double u[IPT];
   if constexpr (kFastExp) {
     // production fp32: the thread's unnormalised weight runs and its
     // unnormalised exponential spacings (resampling.py:21-26) are scanned
@@ -386,37 +403,27 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
       run = __dadd_rn(run, __ddiv_rn(lw[q], total));
       lw[q] = run;  // local inclusive prefix
     }
-    double wtot;
-    const double off = block_exclusive_scan(run, scratch, &wtot);
-#pragma unroll
-    for (int q = 0; q < IPT; ++q)
-      if (i0 + q < N) s_cum[q * THREADS + tid] = __dadd_rn(off, lw[q]);
-
-    // 4. this thread's sorted uniforms (resampling.py:21-26)
-    if (MODE == 1) {
+    // 4. this thread's sorted uniforms (resampling.py:21-26); production: the
+    // CDF runs and the spacing runs in one block scan of pairs (each
+    // component in block_exclusive_scan's association)
+    double off;
+    if constexpr (MODE == 1) {
+      double wtot;
+      off = block_exclusive_scan(run, scratch, &wtot);
 #pragma unroll
       for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __ldg(u_tape + base + i0 + q) : 2.0;
     } else {
-      const Key2 key = load_key(keys, f);
-      double erun = 0.0;
-#pragma unroll
-      for (int q = 0; q < IPT; q += 4) {
-        uint32_t wd[4];
-        spacing_words<IPT>(key, t, i0 + q, wd);
-#pragma unroll
-        for (int h = 0; h < 4 && q + h < IPT; ++h) {
-          const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
-          erun = __dadd_rn(erun, e);
-          u[q + h] = erun;
-        }
-      }
-      double etot;
-      const double eoff = block_exclusive_scan(erun, scratch, &etot);
-      const double cN = __dadd_rn(etot, spacing_exp_fast(key, t, N));  // c[N]
+      double2 tot2;
+      const double2 off2 = block_exclusive_scan2(make_double2(run, erun64), scratch2, &tot2);
+      off = off2.x;
+      const double cN = __dadd_rn(tot2.y, spacing_exp_fast(load_key(keys, f), t, N));  // c[N]
       const double inv = 1.0 / cN;  // production draws: reciprocal multiply
 #pragma unroll
-      for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __dadd_rn(eoff, u[q]) * inv : 2.0;
+      for (int q = 0; q < IPT; ++q) u[q] = i0 + q < N ? __dadd_rn(off2.y, u[q]) * inv : 2.0;
     }
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+      if (i0 + q < N) s_cum[q * THREADS + tid] = __dadd_rn(off, lw[q]);
   }
   __syncthreads();  // s_cum complete
 
