@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
   double lw[IPT];
   float lf[IPT];
   double u[IPT];
-  double erun64 = 0.0;  // fp64 / tape path: the thread's spacing run (production)
+  double erun64 = 0.0;  // the thread's exponential-spacing run (production draws)
   double mx = -INFINITY;
   int nan = 0;
   // VEC: whole runs in range and 16-byte aligned -> vector loads/stores
@@ -274,6 +274,22 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
     } else {
 #pragma unroll
       for (int q = 0; q < IPT; ++q) lf[q] = i0 + q < N ? __ldg(logw + base + i0 + q) : -INFINITY;
+    }
+    // the thread's exponential spacings (independent of the weights) while
+    // the log-weight loads are in flight
+    {
+      const Key2 key = load_key(keys, f);
+#pragma unroll
+      for (int q = 0; q < IPT; q += 4) {
+        uint32_t wd[4];
+        spacing_words<IPT>(key, t, i0 + q, wd);
+#pragma unroll
+        for (int h = 0; h < 4 && q + h < IPT; ++h) {
+          const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
+          erun64 = __dadd_rn(erun64, e);
+          u[q + h] = erun64;
+        }
+      }
     }
     float mf = -INFINITY;
 #pragma unroll
@@ -366,21 +382,9 @@ __global__ void __launch_bounds__(THREADS, THREADS == 128 ? 8 : 1) resample_bank
       lw[q] = static_cast<double>(pf);
     }
     const Key2 key = load_key(keys, f);
-    double erun = 0.0;
-#pragma unroll
-    for (int q = 0; q < IPT; q += 4) {
-      uint32_t wd[4];
-      spacing_words<IPT>(key, t, i0 + q, wd);
-#pragma unroll
-      for (int h = 0; h < 4 && q + h < IPT; ++h) {
-        const double e = i0 + q + h < N ? spacing_exp_fast_word(wd[h]) : 0.0;
-        erun = __dadd_rn(erun, e);
-        u[q + h] = erun;
-      }
-    }
     double2 tot2;
     const double2 off2 =
-        block_exclusive_scan2(make_double2(static_cast<double>(pf), erun), scratch2, &tot2);
+        block_exclusive_scan2(make_double2(static_cast<double>(pf), erun64), scratch2, &tot2);
     total = tot2.x;
     const double inv_total = 1.0 / total;
 #pragma unroll
