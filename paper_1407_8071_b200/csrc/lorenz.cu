@@ -18,6 +18,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 namespace pf {
 
@@ -42,6 +43,24 @@ __device__ __forceinline__ void lorenz_substep(T &x1, T &x2, T &x3, T z1, T z2, 
                       A::mul(sq, A::mul(ns, z2)));
   const T n3 = A::add(A::add(x3, A::mul(dt, A::sub(A::mul(x1, x2), A::mul(b, x3)))),
                       A::mul(sq, A::mul(ns, z3)));
+  x1 = n1;
+  x2 = n2;
+  x3 = n3;
+}
+
+// fp64 production substep (Philox draws, so there is no reference bit pattern
+// to reproduce): the fp32 production form in double - fused multiply-adds,
+// 11 instead of 23 fp64 operations and a 4- instead of 6-deep dependency
+// chain per substep.  Tape (oracle) mode and the L1 operator keep
+// lorenz_substep's exact reference order.
+__device__ __forceinline__ void lorenz_substep_fma(double &x1, double &x2, double &x3, double z1,
+                                                   double z2, double z3, const LorenzConsts &c) {
+  const double cz = c.sq * c.ns;
+  const double n1 = fma(cz, z1, fma(-c.dts, x1 - x2, x1));
+  const double t2 = fma(-x1, x3, fma(c.r, x1, -x2));
+  const double n2 = fma(cz, z2, fma(c.dt, t2, x2));
+  const double t3 = fma(-c.b, x3, x1 * x2);
+  const double n3 = fma(cz, z3, fma(c.dt, t3, x3));
   x1 = n1;
   x2 = n2;
   x3 = n3;
@@ -142,8 +161,13 @@ __global__ void __launch_bounds__(256) lorenz_pw_kernel(
         z[2 * q] = g.x;
         z[2 * q + 1] = g.y;
       }
-      lorenz_substep<T>(x1, x2, x3, T(z[0]), T(z[1]), T(z[2]), c);
-      if (k0 + 1 < c.n_sub) lorenz_substep<T>(x1, x2, x3, T(z[3]), T(z[4]), T(z[5]), c);
+      if constexpr (std::is_same<T, double>::value) {
+        lorenz_substep_fma(x1, x2, x3, z[0], z[1], z[2], c);
+        if (k0 + 1 < c.n_sub) lorenz_substep_fma(x1, x2, x3, z[3], z[4], z[5], c);
+      } else {
+        lorenz_substep<T>(x1, x2, x3, T(z[0]), T(z[1]), T(z[2]), c);
+        if (k0 + 1 < c.n_sub) lorenz_substep<T>(x1, x2, x3, T(z[3]), T(z[4]), T(z[5]), c);
+      }
     }
   }
 
@@ -334,7 +358,7 @@ __global__ void __launch_bounds__(32 * (8 / K)) lorenz_small_kernel(
     if (chain) {
       const double *z = s_z[w][lane];
       for (int k = 0; k < nk; ++k)
-        lorenz_substep<double>(x1, x2, x3, z[3 * k], z[3 * k + 1], z[3 * k + 2], c);
+        lorenz_substep_fma(x1, x2, x3, z[3 * k], z[3 * k + 1], z[3 * k + 2], c);
     }
   }
   if (chain) {
