@@ -1435,7 +1435,15 @@ __global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
   const int64_t i0 = tt * kTile;
   const int n = static_cast<int>(N - i0 < kTile ? N - i0 : kTile);
   const int64_t base = f * N;
-  if (ws.flag[f]) {  // collapse / NaN: identity ancestors (filters.py:105-109)
+  // the filter flag, the CDF window bounds and (production) the thread's
+  // exponential spacings are independent: their loads and the Philox / lg2
+  // work overlap instead of running back to back
+  const int fl = ws.flag[f];
+  const int64_t lo = ws.klo[tile], hi = ws.khi[tile];
+  const int r0 = threadIdx.x * kRun;
+  double u[kRun];
+  if (MODE == 0) spacing_run(load_key(keys, f), t, i0 + r0, N, u);
+  if (fl) {  // collapse / NaN: identity ancestors (filters.py:105-109)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       anc[base + i0 + i] = static_cast<int32_t>(base + i0 + i);
       if (GATHER)
@@ -1445,7 +1453,6 @@ __global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
     return;
   }
   const double *cum = ws.cum + base;
-  const int64_t lo = ws.klo[tile], hi = ws.khi[tile];
   const int64_t wlen = hi - lo + 1;
   const bool chunked = wlen <= 16 * static_cast<int64_t>(kWin);
   // start the first CDF chunk's copy into shared memory now; it lands while
@@ -1461,13 +1468,10 @@ __global__ void __launch_bounds__(kTileThreads, SEARCH ? 4 : 3) wide2_merge(
     cp_async_commit();
   }
   // this thread's run of sorted uniforms, in registers
-  const int r0 = threadIdx.x * kRun;
-  double u[kRun];
   if (MODE == 1) {
 #pragma unroll
     for (int q = 0; q < kRun; ++q) u[q] = r0 + q < n ? u_tape[base + i0 + r0 + q] : 2.0;
   } else {
-    spacing_run(load_key(keys, f), t, i0 + r0, N, u);
     double run = 0.0;
 #pragma unroll
     for (int q = 0; q < kRun; ++q) {
