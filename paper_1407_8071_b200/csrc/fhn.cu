@@ -483,9 +483,9 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
   static_assert(NSEG * 8 <= kCmPitch, "strip slots must fit the column pitch");
   constexpr int P = COLS * kCmPitch;
   constexpr int NODES = ROWS * COLS;
-  extern __shared__ __align__(16) float cms[];  // [2][P]
-  __shared__ double red;
-  __shared__ int bad;
+  extern __shared__ __align__(16) float cms[];  // [2][P] planes, then the electrode tables
+  __shared__ double red[8];                     // per-warp electrode sums
+  __shared__ int badw[8];                       // per-warp divergence flags
   const int tid = threadIdx.x;
   const int seg = tid / COLS;
   const int col = tid - seg * COLS;
@@ -513,12 +513,76 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
     pl[h_below] = vv[5];
   };
 
+  // Electrode log-likelihood, fhn.py:207 (-0.5/obs_var * sum (y - v)^2), taken
+  // from the registers of the thread that owns each observed node: the
+  // observation is the same for every particle of the launch, so each thread
+  // tabulates once per CTA, per strip row r, the number of electrodes on its
+  // node (cnt_r), -2 * the sum of their y (nb_r) and, over its strip, the sum
+  // of y^2 (cy): its share of the sum is cy + sum_r v_r (cnt_r v_r + nb_r)
+  // (fp64; duplicated electrodes allowed).  All warps share the epilogue
+  // instead of one warp walking the electrodes over the shared plane while
+  // the other seven wait at a barrier (~3 % of cfg4's stall samples).
+  double *s_nb = reinterpret_cast<double *>(cms + 2 * P);  // [R][256]
+  double *s_cnt = s_nb + R * 256;                           // [R][256]
+  double *s_cy = s_cnt + R * 256;                           // [256]
+  uint32_t *s_msk = reinterpret_cast<uint32_t *>(s_cy + 256);  // [256] rows with electrodes
+  {
+    double cy = 0.0;
+    uint32_t msk = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      s_nb[r * 256 + tid] = 0.0;
+      s_cnt[r * 256 + tid] = 0.0;
+    }
+    if (active) {
+      for (int i = 0; i < c.n_obs; ++i) {
+        const int n = __ldg(obs_idx + i);
+        const int rr = n / COLS;
+        if (n - rr * COLS == col && rr >= row0 && rr < row0 + R) {
+          const double yv = __ldg(y + i);
+          s_nb[(rr - row0) * 256 + tid] -= 2.0 * yv;
+          s_cnt[(rr - row0) * 256 + tid] += 1.0;
+          cy = fma(yv, yv, cy);
+          msk |= 1u << (rr - row0);
+        }
+      }
+    }
+    s_cy[tid] = cy;
+    s_msk[tid] = msk;  // read back by this thread only: no barrier
+  }
+  // this thread's share of the electrode sum and the divergence flag of the
+  // new state, reduced per warp into red / badw (all 256 threads call it)
+  auto ll_part = [&](const float *vv, const float *ww) {
+    double acc = 0.0;
+    bool fin = true;
+    if (active) {
+      const uint32_t msk = s_msk[tid];
+      if (msk) {
+        acc = s_cy[tid];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if ((msk >> r) & 1u) {
+            const double x = vv[r];
+            acc = fma(x, fma(s_cnt[r * 256 + tid], x, s_nb[r * 256 + tid]), acc);
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) fin = fin && isfinite(vv[r]) && isfinite(ww[r]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    const bool all_fin = __all_sync(0xffffffffu, fin);
+    if ((tid & 31) == 0) {
+      red[tid >> 5] = acc;
+      badw[tid >> 5] = all_fin ? 0 : 1;
+    }
+  };
+
   for (int64_t p = blockIdx.x; p < MN; p += gridDim.x) {
     const int64_t f = p / N;
     const uint32_t j = static_cast<uint32_t>(p - f * N);
     const int64_t src = anc ? static_cast<int64_t>(__ldg(anc + p)) : p;
     const float *xs = xin + src * 2 * static_cast<int64_t>(NODES);
-    if (tid == 0) bad = 0;
     const Key2 key = load_key(keys, f);
     float v[R], w[R];
 #pragma unroll
@@ -709,40 +773,31 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
       }
     }
 
-    // epilogue: divergence flag, store, electrode log-likelihood
+    // epilogue: per-warp electrode shares and flags, one barrier, the state,
+    // the log weight (red / badw are next written after the next particle's
+    // prologue barrier)
+    ll_part(v, w);
+    __syncthreads();
     if (active) {
-      bool fin = true;
       float *xd = xout + p * 2 * static_cast<int64_t>(NODES);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int node = (row0 + r) * COLS + col;
-        fin = fin && isfinite(v[r]) && isfinite(w[r]);
         xd[node] = v[r];
         xd[NODES + node] = w[r];
       }
-      if (!fin) bad = 1;
     }
-    if (tid < 32) {
-      const float *fv = cms + (c.n_sub & 1) * P;
-      double acc = 0.0;
-      for (int i = tid; i < c.n_obs; i += 32) {
-        const int n = __ldg(obs_idx + i);
-        const int rr = n / COLS, cc = n - rr * COLS;
-        const int sg = rr / R;
-        const double rsd =
-            __ldg(y + i) - static_cast<double>(fv[cc * kCmPitch + sg * 8 + (rr - sg * R)]);
-        acc = fma(rsd, rsd, acc);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-      if (tid == 0) red = acc;
-    }
-    __syncthreads();
     if (tid == 0) {
-      logw[p] = static_cast<float>(c.obs_coef * red);
+      double acc = red[0];
+      int bad = badw[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) {
+        acc += red[i];
+        bad |= badw[i];
+      }
+      logw[p] = static_cast<float>(c.obs_coef * acc);
       if (bad) atomicOr(status + f, PF_ST_DIVERGED);
     }
-    __syncthreads();
   }
 }
 
@@ -751,7 +806,9 @@ static int launch_fhn_cm(const FhnFast &fc, const void *x_in, const int32_t *anc
                          const double *y, const int32_t *obs_idx, void *logw, int64_t MN,
                          int32_t N, const uint32_t *keys, uint32_t t, uint32_t *status,
                          cudaStream_t s) {
-  constexpr size_t smem = 2 * static_cast<size_t>(COLS) * kCmPitch * sizeof(float);
+  // two v planes + the electrode tables (2 x kFhnRows x 256 + 256 doubles, 256 masks)
+  constexpr size_t smem = 2 * static_cast<size_t>(COLS) * kCmPitch * sizeof(float) +
+                          (2 * kFhnRows + 1) * 256 * sizeof(double) + 256 * sizeof(uint32_t);
   auto kern = fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2, PIPE>;
   static const int per_sm = [] {
     if (smem > 48 * 1024)

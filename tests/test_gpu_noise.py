@@ -216,8 +216,9 @@ def test_lorenz_one_substep_noise_law(M, N, dtype):
 def test_fhn_column_major_kernel_bit_identical_to_row_major(n_sub, t, flags):
     """The production lattice kernel's column-major strip slots
     (fhn_cm_kernel) and the row-major plane (fhn_fast_kernel, PF_KERNEL_ALT)
-    run the same draws and arithmetic: bit-identical states, log weights and
-    flags.  So does the same kernel issued on packed fp32 pairs
+    run the same draws and arithmetic: bit-identical states and flags, log
+    weights to fp32 rounding (the electrode sum is taken in another fp64
+    order).  So does the same kernel issued on packed fp32 pairs
     (PF_KERNEL_PACKED: FFMA2/FADD2/FMUL2) instead of scalar instructions."""
     m3, _, obs = orc.fhn_truth(seed=3, n_obs=1)
     gm = pf.FhnLatticeModel(stim_row=m3.stim_row, stim_col=m3.stim_col)
@@ -227,5 +228,57 @@ def test_fhn_column_major_kernel_bit_identical_to_row_major(n_sub, t, flags):
                            .astype(np.int32)).cuda()
     a = fhn_interval(gm, x0, anc, obs[0], M, N, t, n_sub=n_sub)
     b = fhn_interval(gm, x0, anc, obs[0], M, N, t, n_sub=n_sub, flags=flags)
-    for u, v in zip(a, b):
-        assert np.array_equal(u, v)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
+    if flags == _lib.PF_KERNEL_PACKED:
+        assert np.array_equal(a[1], b[1])
+    else:
+        # the column-major kernel sums the electrode residuals per owning
+        # thread (fp64, another order): equal to fp32 rounding
+        assert np.allclose(a[1], b[1], rtol=2.5e-7, atol=0), np.abs(a[1] / b[1] - 1).max()
+
+
+@pytest.mark.parametrize("case", ["dups_edges", "many", "one"])
+@pytest.mark.parametrize("n_sub", [50, 1, 0])
+def test_fhn_column_major_electrode_sum_any_electrode_set(case, n_sub):
+    """The production kernel sums each electrode's residual in the thread
+    that owns the node (tables built once per CTA).  Electrode sets other
+    than the BASELINE 10x10 subgrid - duplicated nodes, lattice corners and
+    strip-boundary rows, 128 random nodes, a single one - and the no-step
+    interval give the same log weights as the generic kernel (which walks
+    the electrodes in order over the new plane)."""
+    m3, _, obs = orc.fhn_truth(seed=3, n_obs=1)
+    gm = pf.FhnLatticeModel(stim_row=m3.stim_row, stim_col=m3.stim_col)
+    rng = np.random.default_rng(11)
+    nodes = gm.rows * gm.cols
+    idx = {"dups_edges": np.array([0, 49, 1450, 1499, 5 * 50 + 7, 6 * 50 + 7, 0, 1499, 0,
+                                   11 * 50 + 20, 12 * 50 + 20, 777]),
+           "many": rng.integers(0, nodes, 128),  # the ABI's maximum, duplicates likely
+           "one": np.array([6 * 50 + 3])}[case].astype(np.int32)
+    y = rng.uniform(-0.2, 1.0, idx.size)
+    M, N = 2, 64
+    x0 = torch.from_numpy(_random_lattice_states(gm, M * N, 9)).float().cuda()
+    anc = torch.arange(M * N, dtype=torch.int32, device="cuda")
+    res = []
+    for flags in (0, _lib.PF_KERNEL_GENERIC):
+        xo = torch.empty_like(x0)
+        lw = torch.empty(M * N, dtype=torch.float32, device="cuda")
+        st = torch.zeros(M, dtype=torch.int32, device="cuda")
+        keys = torch.from_numpy(pf.philox.filter_keys(5, M).view(np.int32)).cuda()
+        p = gm.params(n_sub=n_sub)
+        p.n_obs = int(idx.size)
+        d_idx = torch.from_numpy(idx.copy()).cuda()
+        d_y = torch.from_numpy(y.copy()).cuda()
+        _lib.call("pf_fhn_interval_ex", p, _lib.PF_F32, _lib.ptr(x0), _lib.ptr(anc), _lib.ptr(xo),
+                  _lib.ptr(d_y), _lib.ptr(d_idx), _lib.ptr(lw), M, N, _lib.ptr(keys), 3, None,
+                  _lib.ptr(st), flags, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        res.append((xo.cpu().numpy().astype(np.float64), lw.cpu().numpy().astype(np.float64),
+                    st.cpu().numpy()))
+    (xa, la, sa), (xb, lb, sb) = res
+    assert norm_rel(xa, xb) < 1e-4
+    assert np.array_equal(sa, sb) and not sa.any()
+    assert np.allclose(la, lb, rtol=1e-4, atol=0), np.abs(la / lb - 1).max()
+    if n_sub == 0:  # no Euler step: the log weight of the gathered input itself
+        v = x0.cpu().numpy().astype(np.float64)[:, idx]
+        want = -0.5 / gm.obs_var * ((y[None, :] - v) ** 2).sum(axis=1)
+        assert np.allclose(la, want, rtol=1e-6, atol=0)
