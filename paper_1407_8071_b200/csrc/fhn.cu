@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
 // with STS.128 + STS.64 and its boundary rows into the adjacent strips'
 // halos: 5 loads + 4 stores instead of 14 + 6.
 constexpr int kCmPitch = 44;
+__host__ __device__ constexpr int cm_plane(int cols) { return cols * kCmPitch + 64; }
 
 template <int ROWS, int COLS, int R, int MINB, bool X2, bool PIPE = true>
 __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
@@ -481,26 +482,34 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
   static_assert(R == 6 && ROWS % R == 0, "6-row strips tiling the lattice");
   constexpr int NSEG = ROWS / R;
   static_assert(NSEG * 8 <= kCmPitch, "strip slots must fit the column pitch");
-  constexpr int P = COLS * kCmPitch;
+  constexpr int P = cm_plane(COLS);  // plane stride: the slots + the idle threads' scratch
   constexpr int NODES = ROWS * COLS;
+  static_assert(256 - NSEG * COLS >= 0 && (256 - NSEG * COLS) * 8 <= P - COLS * kCmPitch,
+                "idle threads' scratch slots");
   extern __shared__ __align__(16) float cms[];  // [2][P] planes, then the electrode tables
   __shared__ double red[8];                     // per-warp electrode sums
   __shared__ int badw[8];                       // per-warp divergence flags
+  __shared__ uint32_t s_zero;
   const int tid = threadIdx.x;
+  if (tid == 0) s_zero = 0;  // ordered before any read by the first prologue barrier
   const int seg = tid / COLS;
   const int col = tid - seg * COLS;
   const bool active = seg < NSEG;
   const int row0 = seg * R;
-  const int own = col * kCmPitch + seg * 8;
-  const int lft = (col == 0 ? col : col - 1) * kCmPitch + seg * 8;  // ghost = self at the edges
-  const int rgt = (col == COLS - 1 ? col : col + 1) * kCmPitch + seg * 8;
+  // The 256 - NSEG*COLS idle threads run every Euler step too, on zeros in
+  // a scratch slot of their own past the lattice (neighbours = themselves,
+  // halos inside the slot): the step needs no `active` branch (BSSY/BSYNC
+  // reconvergence per step).
+  const int own = active ? col * kCmPitch + seg * 8 : COLS * kCmPitch + (tid - NSEG * COLS) * 8;
+  const int lft = !active ? own : (col == 0 ? col : col - 1) * kCmPitch + seg * 8;  // ghost = self at the edges
+  const int rgt = !active ? own : (col == COLS - 1 ? col : col + 1) * kCmPitch + seg * 8;
   const bool top = seg == 0, bottom = seg == NSEG - 1;
   // halo targets: the down halo of the strip above / up halo of the strip
   // below; the top / bottom strip writes into its column's pad instead
   // (branch-free stores)
   const int pad = col * kCmPitch + NSEG * 8;
-  const int h_above = top ? pad : own - 1;
-  const int h_below = bottom ? pad + 1 : own + 14;
+  const int h_above = !active ? own + 6 : top ? pad : own - 1;
+  const int h_below = !active ? own + 7 : bottom ? pad + 1 : own + 14;
   const float s2v = -1.3862943611198906f * c.sig_v * c.sig_v;
   const float s2w = -1.3862943611198906f * c.sig_w * c.sig_w;
   const uint32_t step0 = (t - 1u) * static_cast<uint32_t>(c.n_sub);
@@ -595,7 +604,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
         w[r] = __ldg(xs + NODES + node);
       }
     }
-    if (active) put(cms, v);
+    put(cms, v);
     __syncthreads();
 
     PhiloxPreT pre[R / 2];
@@ -633,8 +642,18 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
     }
     auto euler = [&](int k, auto par_c) {
       constexpr int PAR = decltype(par_c)::value;
+      // The next step's Philox counter goes through a volatile shared load
+      // of 0 issued after this step's barrier.  With the step body free of
+      // branches, ptxas would otherwise hoist the lookahead Philox of both
+      // unrolled steps into the first (128 registers; 39.7 ms per cfg4
+      // interval instead of 37.7).
+      uint32_t zero;
+      asm volatile("ld.volatile.shared.u32 %0, [%1];"
+                   : "=r"(zero)
+                   : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_zero))));
+      const uint32_t knext = (step0 + k + 1 + zero) ^ key.k0;
       if constexpr (X2) {
-        if (active) {
+        {
           const float *cur = cms + PAR * P;
           float *nxt = cms + (PAR ^ 1) * P;
           const ulonglong2 l4 = *reinterpret_cast<const ulonglong2 *>(cur + lft);
@@ -667,7 +686,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
             uint4 rr;
             if constexpr (PIPE) {
               rr = rpipe[q];
-              rpipe[q] = philox10_t(pre[q], uni, (step0 + k + 1) ^ key.k0, rk);
+              rpipe[q] = philox10_t(pre[q], uni, knext, rk);
             } else {
               rr = philox10_t(pre[q], uni, c1k0, rk);
             }
@@ -710,7 +729,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
         __syncthreads();
         return;
       }
-      if (active) {
+      {
         const float *cur = cms + PAR * P;
         float *nxt = cms + (PAR ^ 1) * P;
         const float4 l4 = *reinterpret_cast<const float4 *>(cur + lft);
@@ -730,7 +749,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
           uint4 rr;
           if constexpr (PIPE) {
             rr = rpipe[q];  // generated during the previous step
-            rpipe[q] = philox10_t(pre[q], uni, (step0 + k + 1) ^ key.k0, rk);
+            rpipe[q] = philox10_t(pre[q], uni, knext, rk);
           } else {
             rr = philox10_t(pre[q], uni, c1k0, rk);
           }
@@ -757,7 +776,15 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
       }
       __syncthreads();
     };
+    // unrolled by four (37.4 vs 37.7 ms per cfg4 interval unrolled by two;
+    // passing the Box-Muller noise scale through the fence as well: 38.5)
     int k = 0;
+    for (; k + 3 < c.n_sub; k += 4) {
+      euler(k, std::integral_constant<int, 0>{});
+      euler(k + 1, std::integral_constant<int, 1>{});
+      euler(k + 2, std::integral_constant<int, 0>{});
+      euler(k + 3, std::integral_constant<int, 1>{});
+    }
     for (; k + 1 < c.n_sub; k += 2) {
       euler(k, std::integral_constant<int, 0>{});
       euler(k + 1, std::integral_constant<int, 1>{});
@@ -807,7 +834,7 @@ static int launch_fhn_cm(const FhnFast &fc, const void *x_in, const int32_t *anc
                          int32_t N, const uint32_t *keys, uint32_t t, uint32_t *status,
                          cudaStream_t s) {
   // two v planes + the electrode tables (2 x kFhnRows x 256 + 256 doubles, 256 masks)
-  constexpr size_t smem = 2 * static_cast<size_t>(COLS) * kCmPitch * sizeof(float) +
+  constexpr size_t smem = 2 * static_cast<size_t>(cm_plane(COLS)) * sizeof(float) +
                           (2 * kFhnRows + 1) * 256 * sizeof(double) + 256 * sizeof(uint32_t);
   auto kern = fhn_cm_kernel<ROWS, COLS, kFhnRows, MINB, X2, PIPE>;
   static const int per_sm = [] {
