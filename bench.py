@@ -369,13 +369,16 @@ def run_reference_arm(args, cfg):
     wall = time.perf_counter() - t0
     value = float(np.median(vals))
     cb["value"] = value
+    ref_config = {"workload": args.config, "desc": cfg["desc"]}
+    if cfg.get("variant", "bootstrap") == "bootstrap" and cfg["kind"] in _KIND_SHAPE:
+        ref_config = _bank_config(args, cfg, args.gpus, *_KIND_SHAPE[cfg["kind"]])
     unit = "particles/s" if resample else "particle-steps/s"
     metric = "particles/s (logsumexp + multinomial resampling + gather)" if resample else METRIC
     line = {"impl": "reference", "metric": metric, "value": value, "unit": unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "desc": cfg["desc"]},
+            "config": ref_config,
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -746,12 +749,7 @@ def run_ours(args, cfg):
                 "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg["dtype"] ==
                 "float32" else "f64", "data": "synthetic",
-                "config": {"workload": args.config, "desc": cfg["desc"], "M": M, "N": N,
-                           "euler_steps_per_obs": n_sub, "parallelism": f"filters/{world}",
-                           "l2": "inputs larger than L2 (state "
-                                 f"{2 * M * N * _state_bytes(model):.3g} B, double-buffered)"
-                           if cfg["kind"] in ("fhn", "fhnnet")
-                           else "state < L2; compute-bound kernel"},
+                "config": _bank_config(args, cfg, world, n_sub, _state_bytes(model)),
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
                 "cuda_graph": used_graph,
                 "nccl": {"ranks": world, "version": comm_version,
@@ -912,6 +910,21 @@ def run_variant(args, cfg):
     return 0
 
 
+def _bank_config(args, cfg, world, n_sub, state_bytes):
+    """`config` of a bootstrap-bank line - the same dict on both arms."""
+    M, N = cfg["M"], cfg["N"]
+    return {"workload": args.config, "desc": cfg["desc"], "M": M, "N": N,
+            "euler_steps_per_obs": n_sub, "parallelism": f"filters/{world}",
+            "l2": "inputs larger than L2 (state "
+                  f"{2 * M * N * state_bytes:.3g} B, double-buffered)"
+            if cfg["kind"] in ("fhn", "fhnnet") else "state < L2; compute-bound kernel"}
+
+
+# the reference arm names the same workload without building the GPU model:
+# (Euler steps per observation, device bytes of one fp32 particle) by model kind
+_KIND_SHAPE = {"fhn": (50, 2 * 30 * 50 * 4), "lorenz": (40, 3 * 4)}
+
+
 def _state_bytes(model):
     """Device bytes of one fp32 particle."""
     if model.kind == "fhnnet":
@@ -927,6 +940,9 @@ def _ncu_traffic(config):
         return None
 
 
+DISPATCH_SLOTS = {"imad_wide": 3.2, "mufu": 1.5, "other": 1.0}
+
+
 def _issue_roofline(pipes, kern_ms, sm_mhz=1965.0):
     """Second roofline for the issue-bound kernels: warp instructions per launch
     (committed ncu count of the same launch) / the live kernel time, against
@@ -935,10 +951,28 @@ def _issue_roofline(pipes, kern_ms, sm_mhz=1965.0):
         return None
     achieved = pipes["warp_inst_per_launch"] / (kern_ms / 1e3)
     peak = 148 * 4 * sm_mhz * 1e6
-    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
+    roof = {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp-inst/s",
             "frac": achieved / peak, "peak_source": "148 SMs x 4 schedulers x 1 warp-inst/clk "
                                                    f"x {sm_mhz:.0f} MHz",
             "source": "smsp__inst_executed.sum (profiles/pipes.json) / live kernel time"}
+    if "imad_wide_per_launch" in pipes:
+        # Dispatch-slot model measured by tools/probes/pipe_probe.cu on this B200
+        # (profiles/r02_pipe_probe.txt): in mixes of independent chains the time per
+        # group is additive - IMAD.WIDE.U32 holds an SMSP's dispatch for ~3.2 clocks,
+        # a MUFU for ~1.5, every other instruction for ~1 - so the Philox multiplies
+        # cost issue slots no other warp can use.
+        scale = pipes["warp_inst_per_launch"] / pipes.get("warp_inst_captured",
+                                                          pipes["warp_inst_per_launch"])
+        slots = (pipes["warp_inst_per_launch"]
+                 + scale * (DISPATCH_SLOTS["imad_wide"] - 1.0) * pipes["imad_wide_per_launch"]
+                 + scale * (DISPATCH_SLOTS["mufu"] - 1.0) * pipes["mufu_per_launch"])
+        roof["dispatch_model"] = {
+            "frac": slots / (kern_ms / 1e3) / peak, "slots_per_launch": slots,
+            "slots": DISPATCH_SLOTS,
+            "note": "secondary: dispatch slots (warp instructions weighted by the clocks each "
+                    "opcode holds the SMSP dispatch port, pipe_probe mixes) / live kernel time "
+                    "/ peak; the fraction of the kernel time the instruction mix itself needs"}
+    return roof
 
 
 def _ncu_pipes(config):
@@ -962,6 +996,7 @@ def _ncu_pipes(config):
     scaled = dict(pipes[src])
     ratio = (CONFIGS[config]["M"] * CONFIGS[config]["N"]) / (CONFIGS[src]["M"] *
                                                              CONFIGS[src]["N"])
+    scaled["warp_inst_captured"] = pipes[src]["warp_inst_per_launch"]
     scaled["warp_inst_per_launch"] = pipes[src]["warp_inst_per_launch"] * ratio
     scaled["source"] = f"{src} capture scaled by particle-steps per launch ({ratio:.4g})"
     return scaled

@@ -292,6 +292,106 @@ __global__ void k_mix_ffma2_imadw(float *out, float a, float b) {
   if (s == 1.2345f) out[0] = s;
 }
 
+
+// MUFU.LG2 with NW IMAD.WIDE per MUFU on independent chains: do the XU pipe
+// (8 clocks per warp MUFU) and the FMA-heavy pipe (4 clocks per warp
+// IMAD.WIDE) overlap?  NW = 2 is the ratio of the Philox + Box-Muller
+// kernels (8 + 8 clocks per group if they overlap, 16 if they serialise).
+template <int NW>
+__global__ void k_mix_mufu_imadw(float *out, float a, float b) {
+  float x[4];
+  uint32_t y[4][NW > 0 ? NW : 1];
+  for (int c = 0; c < 4; ++c) {
+    x[c] = 2.f + threadIdx.x + c;
+    for (int w = 0; w < NW; ++w) y[c][w] = threadIdx.x * 3 + c + 17 * w;
+  }
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      asm volatile("lg2.approx.ftz.f32 %0, %0;" : "+f"(x[c]));
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        uint64_t p;
+        asm volatile("mul.wide.u32 %0, %1, 3528531795;" : "=l"(p) : "r"(y[c][w]));
+        y[c][w] = static_cast<uint32_t>(p >> 32) ^ static_cast<uint32_t>(p);
+      }
+    }
+  }
+  float s = 0;
+  for (int c = 0; c < 4; ++c) {
+    s += x[c];
+    for (int w = 0; w < NW; ++w) s += y[c][w];
+  }
+  if (s == 1.2345f) out[0] = s;
+}
+
+// The production kernels' per-step instruction mix on independent chains,
+// per group: MU MUFU, 2 IMAD.WIDE each followed by the xor of its halves,
+// NX more LOP3, NF FFMA.  fhn_cm_kernel issues MUFU : IMAD.WIDE : LOP3 :
+// FFMA/FADD/FMUL = 24 : 49 : 67 : 96 per thread-step (1 : 2 : 3 : 4),
+// lorenz_fast_kernel 6 : 12 : 15 : 20 (1 : 2 : 2.5 : 3.3): the issue rate the
+// mix reaches without barriers, shared memory or dependent chains, at full
+// occupancy and at the FH-N kernel's 4 warps per SMSP.
+template <int MU, int NX, int NF>
+__global__ void k_mix_fhn(float *out, float a, float b) {
+  float x[4], f[4][NF > 0 ? NF : 1];
+  uint32_t y[4][2], z[4];
+  const float fa = 1.0000001f + threadIdx.x * 1e-9f, fb = 1e-7f;
+  for (int c = 0; c < 4; ++c) {
+    x[c] = 2.f + threadIdx.x + c;
+    z[c] = threadIdx.x * 5 + c;
+    for (int w = 0; w < 2; ++w) y[c][w] = threadIdx.x * 3 + c + 17 * w;
+    for (int w = 0; w < NF; ++w) f[c][w] = threadIdx.x + c + w;
+  }
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (MU) asm volatile("lg2.approx.ftz.f32 %0, %0;" : "+f"(x[c]));
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        uint64_t p;
+        asm volatile("mul.wide.u32 %0, %1, 3528531795;" : "=l"(p) : "r"(y[c][w]));
+        y[c][w] = static_cast<uint32_t>(p >> 32) ^ static_cast<uint32_t>(p);
+#pragma unroll
+        for (int q = w * NF / 2; q < (w + 1) * NF / 2; ++q)
+          asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[c][q]) : "f"(fa), "f"(fb));
+      }
+#pragma unroll
+      for (int q = 0; q < NX; ++q)
+        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(z[c]) : "r"(y[c][0]), "r"(y[c][1]));
+    }
+  }
+  float s = 0;
+  for (int c = 0; c < 4; ++c) {
+    s += x[c] + z[c];
+    for (int w = 0; w < 2; ++w) s += y[c][w];
+    for (int w = 0; w < NF; ++w) s += f[c][w];
+  }
+  if (s == 1.2345f) out[0] = s;
+}
+
+// groups of `ops` instructions, 4 groups per iteration; blocks_per_sm sets
+// the occupancy (256-thread blocks)
+template <typename K>
+void run_mix(const char *name, K kern, int ops, int blocks_per_sm, float *out, int sms,
+             double clk_ghz) {
+  const int blocks = sms * blocks_per_sm, threads = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  kern<<<blocks, threads>>>(out, 1.f, 1.f);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 3; ++r) kern<<<blocks, threads>>>(out, 1.f, 1.f);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double groups = 3.0 * blocks * (threads / 32) * double(kIters) * 4;
+  const double clk_per_group = (ms * 1e-3) * (clk_ghz * 1e9) * (sms * 4) / groups;
+  printf("%-22s %2d warps/SMSP %8.3f ms  %6.2f clk/group/SMSP  %.3f warp-inst/clk/SMSP (%d per group)\n",
+         name, blocks_per_sm * 2, ms, clk_per_group, ops / clk_per_group, ops);
+}
+
 template <typename K, typename A>
 void run(const char *name, K kern, A a, A b, float *out, int sms, double clk_ghz) {
   const int blocks = sms * 8, threads = 256;
@@ -337,6 +437,20 @@ int main() {
   run("mufu_lg2", k_mufu_lg2, 1.f, 1.f, out, sms, ghz);
   run("mufu_sin", k_mufu_sin, 1.f, 1.f, out, sms, ghz);
   run("i2f_u32", k_i2f, 3u, 5u, out, sms, ghz);
+  // mixes: instructions per group incl. the xor of each multiply
+  run_mix("mufu_only", k_mix_mufu_imadw<0>, 1, 8, out, sms, ghz);
+  run_mix("mufu+1imadw", k_mix_mufu_imadw<1>, 3, 8, out, sms, ghz);
+  run_mix("mufu+2imadw", k_mix_mufu_imadw<2>, 5, 8, out, sms, ghz);
+  run_mix("mufu+4imadw", k_mix_mufu_imadw<4>, 9, 8, out, sms, ghz);
+  run_mix("fhn_mix 1:2:3:4", k_mix_fhn<1, 1, 4>, 10, 8, out, sms, ghz);
+  run_mix("fhn_mix 1:2:3:4", k_mix_fhn<1, 1, 4>, 10, 2, out, sms, ghz);
+  run_mix("fhn_mix 1:2:3:4", k_mix_fhn<1, 1, 4>, 10, 1, out, sms, ghz);
+  run_mix("lorenz_mix 1:2:3:3", k_mix_fhn<1, 1, 3>, 9, 8, out, sms, ghz);
+  run_mix("mix 1:2:3:0 (no FFMA)", k_mix_fhn<1, 1, 0>, 6, 8, out, sms, ghz);
+  run_mix("mix 1:2:3:2", k_mix_fhn<1, 1, 2>, 8, 8, out, sms, ghz);
+  run_mix("mix 0:2:3:4 (no MUFU)", k_mix_fhn<0, 1, 4>, 9, 8, out, sms, ghz);
+  run_mix("mix 0:2:3:8 (no MUFU)", k_mix_fhn<0, 1, 8>, 13, 8, out, sms, ghz);
+  run_mix("mix 1:2:3:8", k_mix_fhn<1, 1, 8>, 14, 8, out, sms, ghz);
   cudaError_t e = cudaDeviceSynchronize();
   printf("status: %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;

@@ -5,6 +5,7 @@ and the cfg1c launch list (the whole wide pipeline per step).
     python tools/update_profile_tables.py [round-prefix, default r02]
 """
 import csv
+import gzip
 import json
 import os
 import sys
@@ -26,6 +27,26 @@ def field(path, key):
 def num(path, key):
     parts = field(path, key)
     return float(parts[0]) * (UNITS.get(parts[1], 1.0) if len(parts) > 1 else 1.0)
+
+
+def opcode_counts(sass_gz):
+    """Executed warp instructions of the multi-slot opcodes, from the capture's SASS
+    source page (ncu --page source --csv): IMAD.WIDE / IMAD.HI (32x32 multiplies) and
+    MUFU - the inputs of bench.py's dispatch-slot model."""
+    rows = list(csv.reader(gzip.open(sass_gz, "rt")))
+    hdr = next(r for r in rows if "Source" in r and "Instructions Executed" in r)
+    isrc, iex = hdr.index("Source"), hdr.index("Instructions Executed")
+    out = {"imad_wide_per_launch": 0, "mufu_per_launch": 0}
+    for r in rows[rows.index(hdr) + 1:]:
+        if len(r) <= max(isrc, iex):
+            continue
+        ops = r[isrc].split()
+        op = ops[1] if ops and ops[0].startswith("@") and len(ops) > 1 else (ops[0] if ops else "")
+        if op.startswith("IMAD.WIDE") or op.startswith("IMAD.HI"):
+            out["imad_wide_per_launch"] += int(r[iex])
+        elif op.startswith("MUFU"):
+            out["mufu_per_launch"] += int(r[iex])
+    return out
 
 
 def wide_pipeline_bytes(csv_path):
@@ -60,6 +81,9 @@ def main(prefix="r02"):
             "dram_throughput_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             "warp_inst_per_launch": num(path, "smsp__inst_executed.sum"),
         }
+        sass = os.path.join(ROOT, f"{prefix}_ncu_{cap}_sass.csv.gz")
+        if os.path.exists(sass):
+            pipes[cfg].update(opcode_counts(sass))
     traffic["cfg1c"] = wide_pipeline_bytes(os.path.join(ROOT, f"{prefix}_launches_cfg1c.csv"))
     json.dump(traffic, open(os.path.join(ROOT, "traffic.json"), "w"), indent=1)
     json.dump(pipes, open(os.path.join(ROOT, "pipes.json"), "w"), indent=1)
