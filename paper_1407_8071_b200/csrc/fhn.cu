@@ -16,6 +16,7 @@
 // turns the kernel from HBM-bound into issue-bound (RNG dominated).
 #include "common.cuh"
 #include <type_traits>
+#include "bulk.cuh"
 #include "philox.cuh"
 #include "f32x2.cuh"
 
@@ -470,6 +471,15 @@ __global__ void __launch_bounds__(256, MINB) fhn_fast_kernel(
 // its vertical neighbours from its own halo (LDS.64), writes its new strip
 // with STS.128 + STS.64 and its boundary rows into the adjacent strips'
 // halos: 5 loads + 4 stores instead of 14 + 6.
+// PF_FHN_SPLIT: the per-step CTA barrier of fhn_cm_kernel as an mbarrier
+// arrive / wait pair with the last PF_FHN_SPLIT of the next step's three
+// Philox blocks generated in between (register-only work that hides the
+// skew between the warps).  cfg4 ms per interval, A/B on one box: classic
+// __syncthreads (-1) 37.45; 0 blocks 37.94; 1 block 36.96; 2 blocks 37.21;
+// all 3 (no Philox interleaved with the Box-Muller MUFUs any more) 37.56.
+#ifndef PF_FHN_SPLIT
+#define PF_FHN_SPLIT 1
+#endif
 constexpr int kCmPitch = 44;
 __host__ __device__ constexpr int cm_plane(int cols) { return cols * kCmPitch + 64; }
 
@@ -492,6 +502,14 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
   __shared__ uint32_t s_zero;
   const int tid = threadIdx.x;
   if (tid == 0) s_zero = 0;  // ordered before any read by the first prologue barrier
+#if PF_FHN_SPLIT >= 0
+  __shared__ __align__(8) uint64_t s_mbar;
+  if (tid == 0) {
+    mbar_init(&s_mbar, 256);
+    mbar_fence_init();
+  }
+  uint32_t phase = 0;
+#endif
   const int seg = tid / COLS;
   const int col = tid - seg * COLS;
   const bool active = seg < NSEG;
@@ -647,6 +665,66 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
       // branches, ptxas would otherwise hoist the lookahead Philox of both
       // unrolled steps into the first (128 registers; 39.7 ms per cfg4
       // interval instead of 37.7).
+#if PF_FHN_SPLIT >= 0
+      if constexpr (!X2 && PIPE) {
+        // split barrier: arrive once the new strip is stored, generate the
+        // last PF_FHN_SPLIT blocks of the next step's Philox words (no shared
+        // data), then wait
+        uint32_t zero;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];"
+                     : "=r"(zero)
+                     : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_zero))));
+        const uint32_t knext = (step0 + k + 1 + zero) ^ key.k0;
+        const float *cur = cms + PAR * P;
+        float *nxt = cms + (PAR ^ 1) * P;
+        const float4 l4 = *reinterpret_cast<const float4 *>(cur + lft);
+        const float2 l2 = *reinterpret_cast<const float2 *>(cur + lft + 4);
+        const float4 r4 = *reinterpret_cast<const float4 *>(cur + rgt);
+        const float2 r2 = *reinterpret_cast<const float2 *>(cur + rgt + 4);
+        const float2 hl = *reinterpret_cast<const float2 *>(cur + own + 6);
+        const float L[R] = {l4.x, l4.y, l4.z, l4.w, l2.x, l2.y};
+        const float Rt[R] = {r4.x, r4.y, r4.z, r4.w, r2.x, r2.y};
+        float up = top ? v[0] : hl.x;
+        const float dn_last = bottom ? v[R - 1] : hl.y;
+        float vn[R];
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q) {
+          float av, aw, tv[2], tw[2];
+          const uint4 rr = rpipe[q];
+          if (q < R / 2 - PF_FHN_SPLIT) rpipe[q] = philox10_t(pre[q], uni, knext, rk);
+          box_muller_rad_trig(rr.x, rr.y, s2v, av, tv[0], tv[1]);
+          box_muller_rad_trig(rr.z, rr.w, s2w, aw, tw[0], tw[1]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 2 * q + h;
+            const float u = v[r];
+            const float dn = r < R - 1 ? v[r + 1] : dn_last;
+            const float nb = ((up + dn) + L[r]) + Rt[r];
+            float un = fmaf(fmaf(fmaf(c.a3, u, c.a2), u, c.a1), u, c.a0);
+            un = fmaf(-c.dt, w[r], un);
+            un = fmaf(c.dtc, nb, un);
+            un = fmaf(av, tv[h], un);
+            w[r] = fmaf(aw, tw[h], fmaf(c.wc, w[r], fmaf(c.uc, u, c.c0)));
+            vn[r] = un;
+            up = u;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = vn[r];
+        put(nxt, v);
+        mbar_arrive(&s_mbar);
+        uint32_t zero2;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];"
+                     : "=r"(zero2)
+                     : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_zero))));
+        const uint32_t kn = (step0 + k + 1 + zero2) ^ key.k0;
+#pragma unroll
+        for (int q = R / 2 - PF_FHN_SPLIT; q < R / 2; ++q) rpipe[q] = philox10_t(pre[q], uni, kn, rk);
+        mbar_wait(&s_mbar, phase);
+        phase ^= 1u;
+        return;
+      }
+#endif
       uint32_t zero;
       asm volatile("ld.volatile.shared.u32 %0, [%1];"
                    : "=r"(zero)
