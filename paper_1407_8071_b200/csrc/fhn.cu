@@ -657,8 +657,12 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
 #pragma unroll
       for (int q = 0; q < R / 2; ++q) rpipe[q] = philox10_t(pre[q], uni, step0 ^ key.k0, rk);
     }
-    auto euler = [&](int k, auto par_c) {
+    auto euler = [&](int k, auto par_c, auto last_c) {
       constexpr int PAR = decltype(par_c)::value;
+      // LAST: the interval's final step generates no lookahead words and
+      // skips the barrier (the epilogue's __syncthreads orders its plane
+      // reads before the next particle's prologue stores)
+      constexpr bool LAST = decltype(last_c)::value;
       // The next step's Philox counter goes through a volatile shared load
       // of 0 issued after this step's barrier.  With the step body free of
       // branches, ptxas would otherwise hoist the lookahead Philox of both
@@ -669,11 +673,14 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
         // split barrier: arrive once the new strip is stored, generate the
         // last PF_FHN_SPLIT blocks of the next step's Philox words (no shared
         // data), then wait
-        uint32_t zero;
-        asm volatile("ld.volatile.shared.u32 %0, [%1];"
-                     : "=r"(zero)
-                     : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_zero))));
-        const uint32_t knext = (step0 + k + 1 + zero) ^ key.k0;
+        uint32_t knext = 0;
+        if constexpr (!LAST) {
+          uint32_t zero;
+          asm volatile("ld.volatile.shared.u32 %0, [%1];"
+                       : "=r"(zero)
+                       : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_zero))));
+          knext = (step0 + k + 1 + zero) ^ key.k0;
+        }
         const float *cur = cms + PAR * P;
         float *nxt = cms + (PAR ^ 1) * P;
         const float4 l4 = *reinterpret_cast<const float4 *>(cur + lft);
@@ -690,7 +697,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
         for (int q = 0; q < R / 2; ++q) {
           float av, aw, tv[2], tw[2];
           const uint4 rr = rpipe[q];
-          if (q < R / 2 - PF_FHN_SPLIT) rpipe[q] = philox10_t(pre[q], uni, knext, rk);
+          if (!LAST && q < R / 2 - PF_FHN_SPLIT) rpipe[q] = philox10_t(pre[q], uni, knext, rk);
           box_muller_rad_trig(rr.x, rr.y, s2v, av, tv[0], tv[1]);
           box_muller_rad_trig(rr.z, rr.w, s2w, aw, tw[0], tw[1]);
 #pragma unroll
@@ -711,6 +718,7 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = vn[r];
         put(nxt, v);
+        if constexpr (LAST) return;
         mbar_arrive(&s_mbar);
         uint32_t zero2;
         asm volatile("ld.volatile.shared.u32 %0, [%1];"
@@ -856,19 +864,34 @@ __global__ void __launch_bounds__(256, MINB) fhn_cm_kernel(
       __syncthreads();
     };
     // unrolled by four (37.4 vs 37.7 ms per cfg4 interval unrolled by two;
-    // passing the Box-Muller noise scale through the fence as well: 38.5)
+    // passing the Box-Muller noise scale through the fence as well: 38.5);
+    // the final step is peeled (no lookahead, no barrier)
+    using P0 = std::integral_constant<int, 0>;
+    using P1 = std::integral_constant<int, 1>;
+    constexpr std::false_type more{};
+    constexpr std::true_type last{};
+    const int n1 = c.n_sub - 1;
     int k = 0;
-    for (; k + 3 < c.n_sub; k += 4) {
-      euler(k, std::integral_constant<int, 0>{});
-      euler(k + 1, std::integral_constant<int, 1>{});
-      euler(k + 2, std::integral_constant<int, 0>{});
-      euler(k + 3, std::integral_constant<int, 1>{});
+    for (; k + 3 < n1; k += 4) {
+      euler(k, P0{}, more);
+      euler(k + 1, P1{}, more);
+      euler(k + 2, P0{}, more);
+      euler(k + 3, P1{}, more);
     }
-    for (; k + 1 < c.n_sub; k += 2) {
-      euler(k, std::integral_constant<int, 0>{});
-      euler(k + 1, std::integral_constant<int, 1>{});
+    for (; k + 1 < n1; k += 2) {
+      euler(k, P0{}, more);
+      euler(k + 1, P1{}, more);
     }
-    if (k < c.n_sub) euler(k, std::integral_constant<int, 0>{});
+    if (k < n1) {
+      euler(k, P0{}, more);
+      ++k;
+    }
+    if (k < c.n_sub) {
+      if (k & 1)
+        euler(k, P1{}, last);
+      else
+        euler(k, P0{}, last);
+    }
     if constexpr (X2) {
 #pragma unroll
       for (int q = 0; q < R / 2; ++q) {
