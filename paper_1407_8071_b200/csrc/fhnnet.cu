@@ -398,6 +398,12 @@ struct NetMeta {
 
 // NF: noise-free transition (transition_point_prediction, fhn.py:191-197): no
 // new stimulus, zero increments, no draws.
+// bulk-copy ring depth of the fast kernel; `net` workload ms per interval
+// (propagate kernel), A/B on one box: 2 stages 1.283, 3 stages 1.272,
+// 4 stages 1.372, 5 stages 1.500 (the ring's shared memory comes out of L1)
+#ifndef PF_NET_STAGES
+#define PF_NET_STAGES 3
+#endif
 template <int CW, int S, bool NF = false>
 __global__ void __launch_bounds__((CW + 1) * 32, CW >= 8 ? 4 : CW >= 4 ? 6 : CW >= 2 ? 8 : 12) fhnnet_fast_kernel(
     const float *__restrict__ xin, const uint32_t *__restrict__ qin,
@@ -819,9 +825,9 @@ int pf_fhnnet_step_ex(const pf_fhnnet_params *p, pf_dtype dtype, const void *x_i
   if (net_fast_ok(c, dtype, tape, flags)) {
 #define PF_NET_FAST(CW)                                                                       \
   return c.stochastic                                                                        \
-             ? launch_net_fast<CW, 3>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y,      \
+             ? launch_net_fast<CW, PF_NET_STAGES>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y,      \
                                       obs_idx, logw_out, MN, n32, keys, t, status, s)        \
-             : launch_net_fast<CW, 3, true>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y, \
+             : launch_net_fast<CW, PF_NET_STAGES, true>(c, x_in, q_in, anc, x_out, q_out, forcing_mask, y, \
                                             obs_idx, logw_out, MN, n32, keys, t, status, s)
     switch (net_fast_warps(c)) {
       case 1: PF_NET_FAST(1);
